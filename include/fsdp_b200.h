@@ -1,0 +1,182 @@
+/*
+ * fsdp_b200.h — C ABI of the B200-native FSDP hot path.
+ *
+ * Plain pointers, sizes and a CUDA stream handle (`void* stream` is a
+ * cudaStream_t); no torch types.  Every entry point returns 0 on success or a
+ * non-zero code (a cudaError_t value, or one of FSDP_E_*) and records a
+ * message retrievable with fsdp_last_error().  All device work is enqueued on
+ * the given stream; nothing blocks the host.
+ *
+ * Each entry point replaces a function of the reference `shardsim` package
+ * (paths relative to /root/reference/pkg/src/shardsim/).  The reference binds
+ * nothing natively (it is numpy); the binding a maintainer would add is the
+ * ctypes stub shown in INTEGRATION.md, which is exactly what
+ * paper_2304_11277_b200/_lib.py does.
+ */
+#ifndef FSDP_B200_H_
+#define FSDP_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* element types */
+enum { FSDP_F32 = 0, FSDP_BF16 = 1 };
+
+/* error codes beyond cudaError_t */
+enum {
+  FSDP_E_INVALID = 10001,    /* bad argument (CollectiveError-class contract) */
+  FSDP_E_TIMEOUT = 10002,    /* cross-GPU flag wait timed out (DeadlockError) */
+  FSDP_E_IPC = 10003,        /* IPC handle export/import failed */
+  FSDP_E_UNSUPPORTED = 10004
+};
+
+#define FSDP_MAX_RANKS 8
+#define FSDP_MAX_CTAS 160
+#define FSDP_MAX_TENSORS 96
+#define FSDP_IPC_HANDLE_BYTES 64
+
+const char* fsdp_last_error(void);
+int fsdp_abi_version(void);
+/* number of kernels this library has launched (process lifetime) */
+uint64_t fsdp_launch_count(void);
+int fsdp_num_sms(int device);
+
+/* ------------------------------------------------------------------------
+ * Layout / copy kernels                                  (flatparam.py)
+ * ---------------------------------------------------------------------- */
+
+/* Gather n tensors into a flat buffer of psi elements: tensor i lands at
+ * [offsets[i], offsets[i] + numels[i]); every other element of [0, psi) is
+ * written 0 (padding, flatparam.py:93, :180-181).  With accumulate != 0 the
+ * result is added to the existing flat contents (engine.py:534, `ru.grad +=
+ * flat`) and missing/padding regions are left unchanged.  A NULL src means
+ * "no gradient": zero-filled (flatparam.py:181-185).
+ * Replaces: writeback_grad (flatparam.py:167-191); the layout+concat of the
+ * init materialisation paths (deferred_init.py:156-176, :244-260). */
+int fsdp_flatten(const void* const* srcs, const int64_t* numels, const int64_t* offsets,
+                 int n_tensors, int src_dtype, void* flat, int64_t psi, int flat_dtype,
+                 int accumulate, void* stream);
+
+/* Scatter [offsets[i], +numels[i]) of a flat buffer into n tensors.
+ * Replaces: FlatParameter.views materialised (flatparam.py:159-164),
+ * gather_full_params (engine.py:824-834), streamed-init copy
+ * (deferred_init.py:256). */
+int fsdp_unflatten(const void* flat, int flat_dtype, void* const* dsts, const int64_t* numels,
+                   const int64_t* offsets, int n_tensors, int dst_dtype, void* stream);
+
+/* shard[i] = flat[shard_index * shard_numel + i] (same dtype).
+ * Replaces: FlatParameter.shard (flatparam.py:139-147). */
+int fsdp_shard_copy(const void* flat, void* shard, int64_t shard_numel, int shard_index,
+                    int dtype, void* stream);
+
+/* dst[i] = cast(src[i]) (RNE for fp32 -> bf16).
+ * Replaces: the full -> low cast before the gather (engine.py:661-662) and the
+ * F=1 mixed-precision local cast (engine.py:651-660). */
+int fsdp_cast(const void* src, int src_dtype, void* dst, int dst_dtype, int64_t n, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Optimizer epilogue on the local shard         (numerics.py, engine.py)
+ * ---------------------------------------------------------------------- */
+
+/* g *= inv_scale; if any g is non-finite, *found_inf = 1.0f (else unchanged).
+ * Replaces: engine.py:566-571 (`ru.accum *= inv`; isfinite check). */
+int fsdp_unscale_found_inf(float* g, int64_t n, float inv_scale, float* found_inf, void* stream);
+
+/* Adam (numerics.py:273-285), float32 operation-for-operation as numpy runs
+ * it: m = b1*m + omb1*g; v = b2*v + (omb2*g)*g; mh = m/bc1; vh = v/bc2;
+ * p -= (lr*mh)/(sqrt(vh)+eps).  The scalars are the float32 roundings of the
+ * double-precision expressions (b1, 1-b1, b2, 1-b2, 1-b1^t, 1-b2^t, lr, eps).
+ * If skip_flag != NULL and *skip_flag > 0 the step is skipped on device
+ * (engine.py:578-586 verdict).  If p_lowp != NULL the updated parameter is
+ * also written there as bf16 (the next gather's source).
+ * Replaces: Adam.step / the optimizer loop of _rank_step (engine.py:585). */
+int fsdp_adam_step(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1,
+                   float omb1, float b2, float omb2, float bc1, float bc2, float eps,
+                   const float* skip_flag, void* p_lowp, void* stream);
+
+/* p -= lr * g (numerics.py:248-253), same skip/p_lowp contract. */
+int fsdp_sgd_step(float* p, const float* g, int64_t n, float lr, const float* skip_flag,
+                  void* p_lowp, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Communicator: CUDA-IPC symmetric pool + SM-driven collectives over
+ * NVLink/NVSwitch peer pointers                           (collectives.py)
+ *
+ * Every rank allocates a pool of identical size; all collective buffers are
+ * addressed by POOL OFFSET, identical on every rank.  Group = ranks
+ * {start + j*stride}, j < size, with start derived from the caller's rank:
+ * stride == 1 -> consecutive blocks of `size` (sharded groups,
+ * collectives.py:89-92); stride > 1 -> {r % stride + j*stride} (replicated
+ * groups, collectives.py:94-96).  The k-th call on a (channel, group) pairs
+ * with every member's k-th call (collectives.py:238-251) via epoch counters.
+ * ---------------------------------------------------------------------- */
+typedef struct fsdp_comm fsdp_comm_t;
+
+/* channels: independent flag sets, one per stream that issues collectives */
+enum { FSDP_CH_AG = 0, FSDP_CH_RS = 1, FSDP_CH_AR = 2, FSDP_CH_SCALAR = 3, FSDP_NUM_CH = 4 };
+
+/* Create a communicator for `rank` of `world`; allocates the local pool.
+ * max_ctas bounds every collective's grid (<= FSDP_MAX_CTAS). */
+int fsdp_comm_create(int rank, int world, int64_t pool_bytes, int max_ctas, fsdp_comm_t** out);
+/* Emulated communicator: all `world` ranks' pools on the CURRENT device,
+ * collectives launched as ONE cooperative kernel over every rank's data
+ * (single-GPU testing of the cross-rank protocol). */
+int fsdp_comm_create_emulated(int world, int64_t pool_bytes, int max_ctas, fsdp_comm_t** out);
+int fsdp_comm_ipc_handle(fsdp_comm_t* c, void* handle_out /* FSDP_IPC_HANDLE_BYTES */);
+/* handles: world * FSDP_IPC_HANDLE_BYTES, indexed by rank */
+int fsdp_comm_open_peers(fsdp_comm_t* c, const void* handles);
+/* device base address of rank r's pool as seen by this process (emulated:
+ * each emulated rank's pool; real: r == own rank only) */
+void* fsdp_comm_pool_ptr(fsdp_comm_t* c, int r);
+int64_t fsdp_comm_pool_bytes(fsdp_comm_t* c);
+/* bytes at the start of every pool reserved for flags + error word */
+int64_t fsdp_comm_reserved_bytes(void);
+/* device-side error word (FSDP_E_TIMEOUT after a flag-wait timeout); 0 = ok.
+ * Synchronous read; call after synchronising the streams. */
+int fsdp_comm_device_error(fsdp_comm_t* c);
+int fsdp_comm_set_timeout_ms(fsdp_comm_t* c, int64_t ms);
+int fsdp_comm_destroy(fsdp_comm_t* c);
+
+/* All-gather with fused cast (collectives.py:288-291 + engine.py:661-671):
+ * rank at group position k pushes cast(shard[0..n)) into every member's pool
+ * at byte offset dst_off + k*n*sizeof(dst) — the unsharded flat buffer is
+ * written in place on every peer (no copy-out, engine.py:614/:630 removed).
+ * Emulated comm: shards[e] / one entry per emulated rank e; real: shards[0]. */
+int fsdp_allgather(fsdp_comm_t* c, int channel, int gsize, int gstride, const void* const* shards,
+                   int src_dtype, int64_t n, int64_t dst_off, int dst_dtype, void* stream);
+
+/* Reduce-scatter with fp32 accumulation (engine.py:789-803,
+ * collectives.py:273-297): every member pushes chunk j of its flat payload
+ * (gsize*n elements) to member j's staging at stage_off (slot = sender's
+ * position); member k then sums its gsize slots in ascending rank order
+ * starting from +0.0f, applies  (sum / postdiv)  (skipped when postdiv == 1),
+ * and writes out[i] = (accumulate ? out[i] : 0.0f) + that (engine.py:817-820).
+ * prediv != 1 divides every payload element before summation. */
+int fsdp_reduce_scatter(fsdp_comm_t* c, int channel, int gsize, int gstride,
+                        const void* const* flats, int src_dtype, int64_t n, int64_t stage_off,
+                        float* const* outs, float prediv, float postdiv, int accumulate,
+                        void* stream);
+
+/* All-reduce (collectives.py:298-301; hybrid stage 2, engine.py:804-816):
+ * two-shot push (reduce-scatter to owners, ascending-rank fp32 sum, then
+ * all-gather of the owners' results), so every member holds bit-identical
+ * values.  outs[i] = (accumulate ? outs[i] : 0) + sum/postdiv.  Staging:
+ * stage_off holds gsize*ceil(n/gsize) payload elements, gather_off holds
+ * gsize*ceil(n/gsize) fp32. */
+int fsdp_allreduce(fsdp_comm_t* c, int channel, int gsize, int gstride, const void* const* ins,
+                   int src_dtype, int64_t n, int64_t stage_off, int64_t gather_off,
+                   float* const* outs, float postdiv, int accumulate, void* stream);
+
+/* 1-element world all-reduce of a float flag (engine.py:572-576):
+ * *outs[e] = sum over ranks (ascending) of *ins[e]. */
+int fsdp_allreduce_scalar(fsdp_comm_t* c, const float* const* ins, float* const* outs,
+                          void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FSDP_B200_H_ */

@@ -1,0 +1,239 @@
+"""Device communicator: symmetric CUDA-IPC pool + SM-driven collectives.
+
+`DeviceComm` owns one `fsdp_comm_t` (include/fsdp_b200.h).  It is created
+either
+  * for real (`DeviceComm.create`): one process per GPU; IPC handles of every
+    rank's pool are exchanged once with torch.distributed (plumbing only),
+  * or emulated (`DeviceComm.create_emulated`): all W ranks' pools on the
+    current GPU, each collective one cooperative launch over every rank's
+    data — used to test the cross-rank protocol on a single B200.
+
+Pool regions are handed out by a deterministic bump allocator, so every rank
+obtains the same offsets for the same sequence of `alloc` calls (symmetric
+addressing: a collective names a destination by offset only).
+
+`DeviceFabric` is the shardsim-shaped functional front end
+(collectives.py:183-203): all_gather / reduce_scatter / all_reduce on 1-D
+tensors with the reference's entry contract (CollectiveError on a non-member
+rank, a non-1-D buffer, or a length not divisible by the group).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Sequence
+
+import torch
+
+from . import _lib
+from ._lib import check, lib
+from .plan import CollectiveError, DeadlockError, group_desc_of
+
+_DT = {torch.float32: _lib.F32, torch.bfloat16: _lib.BF16}
+_ES = {torch.float32: 4, torch.bfloat16: 2}
+
+
+def dtype_code(dt: torch.dtype) -> int:
+    try:
+        return _DT[dt]
+    except KeyError:
+        raise CollectiveError(f"unsupported dtype {dt}; fp32 and bf16 are supported") from None
+
+
+class _CudaBuffer:
+    """__cuda_array_interface__ wrapper: a torch view of raw device memory."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+def raw_tensor(ptr: int, nbytes: int, device: torch.device) -> torch.Tensor:
+    return torch.as_tensor(_CudaBuffer(ptr, nbytes), device=device)
+
+
+def stream_ptr(stream: torch.cuda.Stream | None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+class DeviceComm:
+    def __init__(self, handle: int, rank: int, world: int, emulated: bool, device: torch.device):
+        self._h = C.c_void_p(handle)
+        self.rank, self.world, self.emulated = rank, world, emulated
+        self.device = device
+        self.pool_bytes = int(lib.fsdp_comm_pool_bytes(self._h))
+        self.reserved = int(lib.fsdp_comm_reserved_bytes())
+        self._cursor = self.reserved
+        nviews = world if emulated else 1
+        self._pools = []
+        for e in range(nviews):
+            r = e if emulated else rank
+            ptr = lib.fsdp_comm_pool_ptr(self._h, r)
+            self._pools.append(raw_tensor(ptr, self.pool_bytes, device))
+        self.closed = False
+
+    # ------------------------------------------------------------ creation --
+    @classmethod
+    def create(cls, pool_bytes: int, max_ctas: int = 32, group=None) -> "DeviceComm":
+        import torch.distributed as dist
+        rank = dist.get_rank(group)
+        world = dist.get_world_size(group)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        h = C.c_void_p()
+        check(lib.fsdp_comm_create(rank, world, pool_bytes, max_ctas, C.byref(h)), "comm_create")
+        buf = (C.c_char * _lib.IPC_HANDLE_BYTES)()
+        check(lib.fsdp_comm_ipc_handle(h, buf), "comm_ipc_handle")
+        mine = bytes(buf)
+        handles: list = [None] * world
+        dist.all_gather_object(handles, mine, group=group)
+        allh = b"".join(handles)
+        check(lib.fsdp_comm_open_peers(h, allh), "comm_open_peers")
+        torch.cuda.synchronize()
+        dist.barrier(group=group)          # every pool's flags are zeroed before use
+        return cls(h.value, rank, world, False, dev)
+
+    @classmethod
+    def create_emulated(cls, world: int, pool_bytes: int, max_ctas: int = 16) -> "DeviceComm":
+        dev = torch.device("cuda", torch.cuda.current_device())
+        h = C.c_void_p()
+        check(lib.fsdp_comm_create_emulated(world, pool_bytes, max_ctas, C.byref(h)),
+              "comm_create_emulated")
+        return cls(h.value, 0, world, True, dev)
+
+    def close(self) -> None:
+        if not self.closed:
+            torch.cuda.synchronize(self.device)
+            self._pools = []
+            lib.fsdp_comm_destroy(self._h)
+            self.closed = True
+
+    def set_timeout_ms(self, ms: int) -> None:
+        check(lib.fsdp_comm_set_timeout_ms(self._h, int(ms)))
+
+    # -------------------------------------------------------------- memory --
+    @property
+    def nranks_local(self) -> int:
+        return self.world if self.emulated else 1
+
+    def alloc(self, nbytes: int, align: int = 256) -> int:
+        """Symmetric region: same offset on every rank for the same call order."""
+        off = (self._cursor + align - 1) // align * align
+        if off + nbytes > self.pool_bytes:
+            raise MemoryError(f"symmetric pool exhausted: need {off + nbytes} of {self.pool_bytes} B")
+        self._cursor = off + nbytes
+        return off
+
+    def view(self, offset: int, numel: int, dtype: torch.dtype, e: int = 0) -> torch.Tensor:
+        """Tensor over [offset, offset + numel*itemsize) of local pool `e`."""
+        nb = numel * _ES[dtype]
+        return self._pools[e][offset: offset + nb].view(dtype)
+
+    def device_error(self) -> int:
+        return int(lib.fsdp_comm_device_error(self._h))
+
+    def raise_device_error(self) -> None:
+        err = self.device_error()
+        if err == _lib.E_TIMEOUT:
+            raise DeadlockError("a cross-GPU collective wait timed out on device: some group member "
+                                "never entered the matching collective")
+        if err:
+            raise RuntimeError(f"device error word = {err}")
+
+    # --------------------------------------------------------- collectives --
+    def _ptrs(self, ts: Sequence[torch.Tensor]):
+        if len(ts) != self.nranks_local:
+            raise CollectiveError(f"expected {self.nranks_local} per-rank buffers, got {len(ts)}")
+        return _lib.ptr_array([t.data_ptr() for t in ts])
+
+    def all_gather(self, gdesc, shards: Sequence[torch.Tensor], dst_off: int, dst_dtype: torch.dtype,
+                   stream=None, channel: int = _lib.CH_AG) -> None:
+        n = shards[0].numel()
+        check(lib.fsdp_allgather(self._h, channel, gdesc[0], gdesc[1], self._ptrs(shards),
+                                 dtype_code(shards[0].dtype), n, dst_off, dtype_code(dst_dtype),
+                                 stream_ptr(stream)), "allgather")
+
+    def reduce_scatter(self, gdesc, flats: Sequence[torch.Tensor], stage_off: int,
+                       outs: Sequence[torch.Tensor], prediv: float = 1.0, postdiv: float = 1.0,
+                       accumulate: bool = False, stream=None, channel: int = _lib.CH_RS) -> None:
+        n = outs[0].numel()
+        check(lib.fsdp_reduce_scatter(self._h, channel, gdesc[0], gdesc[1], self._ptrs(flats),
+                                      dtype_code(flats[0].dtype), n, stage_off, self._ptrs(outs),
+                                      float(prediv), float(postdiv), int(accumulate),
+                                      stream_ptr(stream)), "reduce_scatter")
+
+    def all_reduce(self, gdesc, ins: Sequence[torch.Tensor], stage_off: int, gather_off: int,
+                   outs: Sequence[torch.Tensor], postdiv: float = 1.0, accumulate: bool = False,
+                   stream=None, channel: int = _lib.CH_AR) -> None:
+        n = ins[0].numel()
+        check(lib.fsdp_allreduce(self._h, channel, gdesc[0], gdesc[1], self._ptrs(ins),
+                                 dtype_code(ins[0].dtype), n, stage_off, gather_off,
+                                 self._ptrs(outs), float(postdiv), int(accumulate),
+                                 stream_ptr(stream)), "allreduce")
+
+    def scalar_all_reduce(self, ins: Sequence[torch.Tensor], outs: Sequence[torch.Tensor],
+                          stream=None) -> None:
+        check(lib.fsdp_allreduce_scalar(self._h, self._ptrs(ins), self._ptrs(outs),
+                                        stream_ptr(stream)), "allreduce_scalar")
+
+    @staticmethod
+    def ar_staging_elems(n: int, gsize: int) -> int:
+        c = -(-n // gsize)
+        c = -(-c // 8) * 8
+        return c * gsize
+
+
+class DeviceFabric:
+    """shardsim-shaped collectives on device tensors (collectives.py:183-306).
+
+    Each call validates the reference's entry contract synchronously and
+    returns the result tensor(s).  For an emulated communicator the `local`
+    argument is a list with one tensor per rank and so is the result."""
+
+    def __init__(self, comm: DeviceComm, scratch_bytes: int):
+        self.comm = comm
+        self.scratch_bytes = scratch_bytes
+        self.off_a = comm.alloc(scratch_bytes)
+        self.off_b = comm.alloc(scratch_bytes)
+
+    def _norm(self, rank: int, group: Sequence[int], local, kind: str):
+        group = tuple(sorted(group))
+        if rank not in group:
+            raise CollectiveError(f"rank {rank} is not a member of {group}")
+        locs = list(local) if isinstance(local, (list, tuple)) else [local]
+        for t in locs:
+            if t.dim() != 1:
+                raise CollectiveError(f"{kind}: expected a flat 1-d buffer, got shape {tuple(t.shape)}")
+        if len({t.numel() for t in locs}) > 1:
+            raise CollectiveError(f"{kind} on group {group}: uneven inputs are rejected, pad explicitly")
+        return group, locs
+
+    def all_gather(self, rank, group, local, stream=None):
+        group, locs = self._norm(rank, group, local, "AG")
+        gd = group_desc_of(group, self.comm.world)
+        n = locs[0].numel()
+        nb = n * gd[0] * _ES[locs[0].dtype]
+        if nb > self.scratch_bytes:
+            raise CollectiveError("AG larger than the fabric scratch region")
+        self.comm.all_gather(gd, locs, self.off_a, locs[0].dtype, stream)
+        outs = [self.comm.view(self.off_a, n * gd[0], locs[0].dtype, e).clone()
+                for e in range(self.comm.nranks_local)]
+        return outs if isinstance(local, (list, tuple)) else outs[0]
+
+    def reduce_scatter(self, rank, group, local, stream=None):
+        group, locs = self._norm(rank, group, local, "RS")
+        gd = group_desc_of(group, self.comm.world)
+        length = locs[0].numel()
+        if length % gd[0]:
+            raise CollectiveError(f"reduce_scatter: input length {length} not divisible by group size {gd[0]}")
+        n = length // gd[0]
+        outs = [torch.empty(n, dtype=torch.float32, device=self.comm.device) for _ in locs]
+        self.comm.reduce_scatter(gd, locs, self.off_a, outs, stream=stream)
+        return outs if isinstance(local, (list, tuple)) else outs[0]
+
+    def all_reduce(self, rank, group, local, stream=None):
+        group, locs = self._norm(rank, group, local, "AR")
+        gd = group_desc_of(group, self.comm.world)
+        n = locs[0].numel()
+        outs = [torch.empty(n, dtype=torch.float32, device=self.comm.device) for _ in locs]
+        self.comm.all_reduce(gd, locs, self.off_a, self.off_b, outs, stream=stream)
+        return outs if isinstance(local, (list, tuple)) else outs[0]

@@ -1,0 +1,615 @@
+// CUDA-IPC communicator and SM-driven collectives over NVLink/NVSwitch.
+//
+// Design (B200-first, not a port of the reference's in-process fabric):
+//  * every rank owns a symmetric pool (same size, same sub-allocation offsets
+//    on every rank); peers map it with cudaIpcOpenMemHandle, so a collective
+//    addresses any member's buffer as bases[member] + offset;
+//  * all data movement is PUSH (st.global to peer memory): NVLink stores need
+//    no round trip, loads would need ~2 us of latency hiding per request;
+//  * cross-GPU ordering uses per-(channel, phase, sender, CTA) epoch flags
+//    written with st.release.sys after a system fence and polled with
+//    ld.acquire.sys.  Every member launches the same grid and partitions the
+//    work into the same tiles, so CTA c only waits for the CTAs c of its
+//    peers (no grid-wide barrier, no co-residency requirement);
+//  * waits time out (default 20 s) into a device error word instead of
+//    hanging the GPU — the analogue of shardsim's DeadlockError;
+//  * reductions sum in fp32 in ascending rank order from +0.0f with explicit
+//    __fadd_rn, which makes them bit-identical to the reference fabric's
+//    deterministic mode (collectives.py:273-278) on fp32-upcast payloads.
+//
+// Emulated mode runs all W ranks of one communicator on the current GPU as a
+// single cooperative launch (blockIdx.y = rank) over W pools, exercising the
+// exact same flag protocol and address arithmetic without multiple GPUs.
+#include <cooperative_groups.h>
+
+#include <cstring>
+#include <map>
+#include <vector>
+
+#include "common.cuh"
+
+namespace fsdp {
+
+constexpr int kPhases = 3;
+constexpr int64_t kFlagBytes =
+    (int64_t)FSDP_NUM_CH * kPhases * FSDP_MAX_RANKS * FSDP_MAX_CTAS * sizeof(uint32_t);
+constexpr int64_t kErrOff = kFlagBytes;                 // uint32 error word
+constexpr int64_t kScalarOff = kFlagBytes + 256;        // float[FSDP_MAX_RANKS]
+constexpr int64_t kReserved = 65536;
+static_assert(kScalarOff + 4 * FSDP_MAX_RANKS <= kReserved, "reserved region too small");
+
+constexpr int kCommThreads = 512;
+constexpr int kVec = 8;                                  // elements per vector
+constexpr int kTileElems = kCommThreads * kVec * 2;      // 8192 elements per tile
+
+struct CollParams {
+  char* bases[FSDP_MAX_RANKS];
+  const void* in[FSDP_MAX_RANKS];
+  float* out[FSDP_MAX_RANKS];
+  int rank0;        // >= 0: real mode, this process's rank; -1: emulated
+  int gsize, gstride, channel;
+  uint32_t epoch;
+  int64_t n;
+  int64_t off_a, off_b;
+  float prediv, postdiv;
+  int accumulate;
+  int64_t timeout_ns;
+};
+
+// ------------------------------------------------------------ primitives ----
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ uint32_t* flag_ptr(char* base, int ch, int phase, int src, int cta) {
+  return reinterpret_cast<uint32_t*>(base) +
+         (((int64_t)(ch * kPhases + phase) * FSDP_MAX_RANKS + src) * FSDP_MAX_CTAS + cta);
+}
+
+template <typename T> __device__ __forceinline__ T ldcg_elem(const T* p);
+template <> __device__ __forceinline__ float ldcg_elem<float>(const float* p) { return __ldcg(p); }
+template <> __device__ __forceinline__ __nv_bfloat16 ldcg_elem<__nv_bfloat16>(const __nv_bfloat16* p) {
+  unsigned short v;
+  asm volatile("ld.global.cg.u16 %0, [%1];" : "=h"(v) : "l"(p));
+  return __ushort_as_bfloat16(v);
+}
+
+struct Group {
+  int rank, start, pos, size, stride;
+  __device__ int member(int j) const { return start + j * stride; }
+};
+
+__device__ __forceinline__ Group make_group(const CollParams& p) {
+  Group g;
+  g.rank = p.rank0 >= 0 ? p.rank0 : (int)blockIdx.y;
+  g.size = p.gsize;
+  g.stride = p.gstride;
+  if (p.gstride == 1) {
+    g.start = (g.rank / p.gsize) * p.gsize;
+    g.pos = g.rank - g.start;
+  } else {
+    g.start = g.rank % p.gstride;
+    g.pos = g.rank / p.gstride;
+  }
+  return g;
+}
+
+// CTA-level barrier with the matching CTA of every group member.  `release`
+// fences this CTA's prior peer stores (data phases).
+__device__ __noinline__ void cta_barrier(const CollParams& p, const Group& g, int phase,
+                                         bool release) {
+  __syncthreads();
+  const int j = threadIdx.x;
+  if (j < g.size) {
+    const int peer = g.member(j);
+    if (release) __threadfence_system();
+    st_release_sys(flag_ptr(p.bases[peer], p.channel, phase, g.rank, blockIdx.x), p.epoch);
+    const uint32_t* mine = flag_ptr(p.bases[g.rank], p.channel, phase, peer, blockIdx.x);
+    uint32_t* err = reinterpret_cast<uint32_t*>(p.bases[g.rank] + kErrOff);
+    const uint64_t t0 = globaltimer();
+    uint32_t spins = 0;
+    while ((int32_t)(ld_acquire_sys(mine) - p.epoch) < 0) {
+      if ((++spins & 1023u) == 0) {
+        if (*(volatile uint32_t*)err != 0) break;           // already failed: bail out
+        if (globaltimer() - t0 > (uint64_t)p.timeout_ns) {
+          atomicExch(err, (uint32_t)FSDP_E_TIMEOUT);
+          break;
+        }
+      }
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------ all-gather ----
+template <typename Tin, typename Tout>
+__global__ void __launch_bounds__(kCommThreads)
+allgather_kernel(const __grid_constant__ CollParams p) {
+  const Group g = make_group(p);
+  const int e = p.rank0 >= 0 ? 0 : blockIdx.y;
+  const Tin* __restrict__ src = (const Tin*)p.in[e];
+  const int64_t n = p.n;
+  const int64_t my_off = p.off_a + (int64_t)g.pos * n * (int64_t)sizeof(Tout);
+  cta_barrier(p, g, 0, false);   // every member's destination slot is free
+
+  const bool vec = (n % kVec == 0) && aligned16(src) && (my_off % 16 == 0);
+  const int64_t ntiles = (n + kTileElems - 1) / kTileElems;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t t0 = t * kTileElems;
+    const int64_t t1 = min(t0 + (int64_t)kTileElems, n);
+    if (vec) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int64_t i = t0 + ((int64_t)u * kCommThreads + threadIdx.x) * kVec;
+        if (i < t1) {
+          const Packed8<Tout> v = pack8<Tout>(load8<Tin>(src + i, LD_NC));
+          for (int jj = 0; jj < g.size; ++jj) {
+            const int j = (g.pos + 1 + jj) % g.size;   // stagger destinations
+            store8<Tout>((Tout*)(p.bases[g.member(j)] + my_off) + i, v);
+          }
+        }
+      }
+    } else {
+      for (int64_t i = t0 + threadIdx.x; i < t1; i += kCommThreads) {
+        const Tout v = from_f<Tout>(to_f<Tin>(src[i]));
+        for (int jj = 0; jj < g.size; ++jj) {
+          const int j = (g.pos + 1 + jj) % g.size;
+          ((Tout*)(p.bases[g.member(j)] + my_off))[i] = v;
+        }
+      }
+    }
+  }
+  cta_barrier(p, g, 1, true);    // all members' pieces have landed here
+}
+
+// -------------------------------------------------------- reduce-scatter ----
+template <typename Tin>
+__global__ void __launch_bounds__(kCommThreads)
+reduce_scatter_kernel(const __grid_constant__ CollParams p) {
+  const Group g = make_group(p);
+  const int e = p.rank0 >= 0 ? 0 : blockIdx.y;
+  const Tin* __restrict__ flat = (const Tin*)p.in[e];
+  float* __restrict__ out = p.out[e];
+  const int64_t n = p.n;
+  const int64_t slot_bytes = n * (int64_t)sizeof(Tin);
+  cta_barrier(p, g, 0, false);   // every member's staging is free
+
+  const bool vec = (n % kVec == 0) && aligned16(flat) && (p.off_a % 16 == 0);
+  const int64_t ntiles = (n + kTileElems - 1) / kTileElems;
+  // phase 1: chunk j of my flat payload -> member j's staging slot [my pos]
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t t0 = t * kTileElems;
+    const int64_t t1 = min(t0 + (int64_t)kTileElems, n);
+    for (int jj = 0; jj < g.size; ++jj) {
+      const int j = (g.pos + 1 + jj) % g.size;
+      Tin* dst = (Tin*)(p.bases[g.member(j)] + p.off_a + (int64_t)g.pos * slot_bytes);
+      const Tin* s = flat + (int64_t)j * n;
+      if (vec) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int64_t i = t0 + ((int64_t)u * kCommThreads + threadIdx.x) * kVec;
+          if (i < t1) st_v4(dst + i, ld_stream(s + i));
+          if (sizeof(Tin) == 4 && i < t1) st_v4(dst + i + 4, ld_stream(s + i + 4));
+        }
+      } else {
+        for (int64_t i = t0 + threadIdx.x; i < t1; i += kCommThreads) dst[i] = s[i];
+      }
+    }
+  }
+  cta_barrier(p, g, 1, true);    // my tiles of every member's chunk arrived
+  // phase 2: ascending-rank fp32 sum of my slots, post-divide, accumulate
+  const Tin* stage = (const Tin*)(p.bases[g.rank] + p.off_a);
+  const bool pre = p.prediv != 1.0f, post = p.postdiv != 1.0f;
+  const bool vec_out = vec && aligned16(out);
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t t0 = t * kTileElems;
+    const int64_t t1 = min(t0 + (int64_t)kTileElems, n);
+    if (vec_out) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int64_t i = t0 + ((int64_t)u * kCommThreads + threadIdx.x) * kVec;
+        if (i >= t1) continue;
+        V8F acc;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc.v[k] = 0.0f;
+        for (int j = 0; j < g.size; ++j) {
+          V8F x = load8<Tin>(stage + (int64_t)j * n + i, LD_CG);
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            acc.v[k] = __fadd_rn(acc.v[k], pre ? __fdiv_rn(x.v[k], p.prediv) : x.v[k]);
+        }
+        V8F base;
+        if (p.accumulate) base = load8<float>(out + i, LD_PLAIN);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float r = post ? __fdiv_rn(acc.v[k], p.postdiv) : acc.v[k];
+          acc.v[k] = __fadd_rn(p.accumulate ? base.v[k] : 0.0f, r);
+        }
+        store8<float>(out + i, pack8<float>(acc));
+      }
+    } else {
+      for (int64_t i = t0 + threadIdx.x; i < t1; i += kCommThreads) {
+        float acc = 0.0f;
+        for (int j = 0; j < g.size; ++j) {
+          const float x = to_f<Tin>(ldcg_elem(stage + (int64_t)j * n + i));
+          acc = __fadd_rn(acc, pre ? __fdiv_rn(x, p.prediv) : x);
+        }
+        const float r = post ? __fdiv_rn(acc, p.postdiv) : acc;
+        out[i] = __fadd_rn(p.accumulate ? out[i] : 0.0f, r);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------ all-reduce ----
+// Two-shot: RS-push to chunk owners, ascending fp32 sum, AG-push of results.
+template <typename Tin>
+__global__ void __launch_bounds__(kCommThreads)
+allreduce_kernel(const __grid_constant__ CollParams p) {
+  const Group g = make_group(p);
+  const int e = p.rank0 >= 0 ? 0 : blockIdx.y;
+  const Tin* __restrict__ in = (const Tin*)p.in[e];
+  float* __restrict__ out = p.out[e];
+  const int64_t n = p.n;
+  int64_t c = (n + g.size - 1) / g.size;
+  c = (c + kVec - 1) / kVec * kVec;                       // chunk stride (elements)
+  auto clen = [&](int j) -> int64_t {
+    const int64_t s = (int64_t)j * c;
+    return s >= n ? 0 : min(c, n - s);
+  };
+  cta_barrier(p, g, 0, false);
+
+  const int64_t ntiles = (c + kTileElems - 1) / kTileElems;
+  // phase A: my chunk j -> member j's stage slot [my pos]
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t t0 = t * kTileElems;
+    for (int jj = 0; jj < g.size; ++jj) {
+      const int j = (g.pos + 1 + jj) % g.size;
+      const int64_t len = clen(j);
+      const int64_t t1 = min(t0 + (int64_t)kTileElems, len);
+      Tin* dst = (Tin*)(p.bases[g.member(j)] + p.off_a) + (int64_t)g.pos * c;
+      const Tin* s = in + (int64_t)j * c;
+      for (int64_t i = t0 + threadIdx.x; i < t1; i += kCommThreads) dst[i] = s[i];
+    }
+  }
+  cta_barrier(p, g, 1, true);
+  // reduce my chunk, push the result to every member's gather buffer
+  {
+    const Tin* stage = (const Tin*)(p.bases[g.rank] + p.off_a);
+    const int64_t len = clen(g.pos);
+    const bool post = p.postdiv != 1.0f;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int64_t t0 = t * kTileElems;
+      const int64_t t1 = min(t0 + (int64_t)kTileElems, len);
+      for (int64_t i = t0 + threadIdx.x; i < t1; i += kCommThreads) {
+        float acc = 0.0f;
+        for (int j = 0; j < g.size; ++j) acc = __fadd_rn(acc, to_f<Tin>(ldcg_elem(stage + (int64_t)j * c + i)));
+        const float r = post ? __fdiv_rn(acc, p.postdiv) : acc;
+        for (int jj = 0; jj < g.size; ++jj) {
+          const int j = (g.pos + 1 + jj) % g.size;
+          ((float*)(p.bases[g.member(j)] + p.off_b))[(int64_t)g.pos * c + i] = r;
+        }
+      }
+    }
+  }
+  cta_barrier(p, g, 2, true);
+  // epilogue: out = (accumulate ? out : 0) + gathered, for my tiles of every chunk
+  const float* gath = (const float*)(p.bases[g.rank] + p.off_b);
+  for (int j = 0; j < g.size; ++j) {
+    const int64_t len = clen(j);
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int64_t t0 = t * kTileElems;
+      const int64_t t1 = min(t0 + (int64_t)kTileElems, len);
+      for (int64_t i = t0 + threadIdx.x; i < t1; i += kCommThreads) {
+        const int64_t k = (int64_t)j * c + i;
+        out[k] = __fadd_rn(p.accumulate ? out[k] : 0.0f, __ldcg(gath + k));
+      }
+    }
+  }
+}
+
+// 1-element world all-reduce of a float (found_inf verdict).
+__global__ void __launch_bounds__(32) scalar_allreduce_kernel(const __grid_constant__ CollParams p) {
+  const Group g = make_group(p);
+  const int e = p.rank0 >= 0 ? 0 : blockIdx.y;
+  cta_barrier(p, g, 0, false);
+  if ((int)threadIdx.x < g.size) {
+    const float v = *(const float*)p.in[e];
+    ((float*)(p.bases[g.member(threadIdx.x)] + kScalarOff))[g.rank] = v;
+  }
+  cta_barrier(p, g, 1, true);
+  if (threadIdx.x == 0) {
+    const float* s = (const float*)(p.bases[g.rank] + kScalarOff);
+    float acc = 0.0f;
+    for (int j = 0; j < g.size; ++j) acc = __fadd_rn(acc, __ldcg(s + g.member(j)));
+    *p.out[e] = acc;
+  }
+}
+
+}  // namespace fsdp
+
+using namespace fsdp;
+
+struct fsdp_comm {
+  int rank = 0, world = 1;
+  bool emulated = false;
+  int64_t pool_bytes = 0;
+  int max_ctas = 32;
+  int device = 0;
+  char* pool = nullptr;                       // own pool (emulated: all pools)
+  char* bases[FSDP_MAX_RANKS] = {};
+  bool opened[FSDP_MAX_RANKS] = {};
+  uint32_t epoch[FSDP_NUM_CH] = {};
+  int64_t timeout_ns = 20LL * 1000 * 1000 * 1000;
+};
+
+namespace {
+
+int validate_group(fsdp_comm_t* c, int channel, int gsize, int gstride) {
+  if (!c) return fail(FSDP_E_INVALID, "null communicator");
+  if (channel < 0 || channel >= FSDP_NUM_CH) return fail(FSDP_E_INVALID, "bad channel");
+  if (gsize < 1 || gstride < 1 || gsize * gstride > c->world ||
+      (gstride == 1 ? c->world % gsize : c->world % (gsize * gstride)))
+    return fail(FSDP_E_INVALID, "group does not partition the world");
+  if (!c->emulated)
+    for (int j = 0; j < gsize; ++j) {
+      const int start = gstride == 1 ? (c->rank / gsize) * gsize : c->rank % gstride;
+      const int m = start + j * gstride;
+      if (!c->bases[m]) return fail(FSDP_E_INVALID, "peer pool not opened (fsdp_comm_open_peers)");
+    }
+  return 0;
+}
+
+void fill_common(fsdp_comm_t* c, CollParams& p, int channel, int gsize, int gstride, int64_t n) {
+  std::memset(&p, 0, sizeof(p));
+  for (int r = 0; r < FSDP_MAX_RANKS; ++r) p.bases[r] = c->bases[r];
+  p.rank0 = c->emulated ? -1 : c->rank;
+  p.gsize = gsize;
+  p.gstride = gstride;
+  p.channel = channel;
+  p.epoch = ++c->epoch[channel];
+  p.n = n;
+  p.prediv = 1.0f;
+  p.postdiv = 1.0f;
+  p.timeout_ns = c->timeout_ns;
+}
+
+int grid_for(fsdp_comm_t* c, int64_t elems) {
+  int64_t tiles = (elems + kTileElems - 1) / kTileElems;
+  int g = (int)std::min<int64_t>(std::max<int64_t>(tiles, 1), c->max_ctas);
+  if (c->emulated) g = std::min(g, std::max(1, 128 / c->world));
+  return g;
+}
+
+template <typename K>
+int launch(fsdp_comm_t* c, K kernel, const CollParams& p, int grid, int threads, cudaStream_t s) {
+  if (c->emulated) {
+    dim3 gd(grid, c->world), bd(threads);
+    void* args[] = {(void*)&p};
+    FSDP_CUDA(cudaLaunchCooperativeKernel((void*)kernel, gd, bd, args, 0, s));
+  } else {
+    kernel<<<grid, threads, 0, s>>>(p);
+  }
+  FSDP_LAUNCHED();
+  return 0;
+}
+
+int nranks_args(fsdp_comm_t* c) { return c->emulated ? c->world : 1; }
+
+}  // namespace
+
+extern "C" int64_t fsdp_comm_reserved_bytes(void) { return kReserved; }
+
+extern "C" int fsdp_comm_create(int rank, int world, int64_t pool_bytes, int max_ctas,
+                                fsdp_comm_t** out) {
+  if (!out) return fail(FSDP_E_INVALID, "null out");
+  if (world < 1 || world > FSDP_MAX_RANKS || rank < 0 || rank >= world)
+    return fail(FSDP_E_INVALID, "rank/world out of range (world <= 8)");
+  if (max_ctas < 1 || max_ctas > FSDP_MAX_CTAS) return fail(FSDP_E_INVALID, "max_ctas out of range");
+  if (pool_bytes < kReserved) pool_bytes = kReserved;
+  pool_bytes = (pool_bytes + 4095) / 4096 * 4096;
+  fsdp_comm_t* c = new fsdp_comm_t();
+  c->rank = rank; c->world = world; c->pool_bytes = pool_bytes; c->max_ctas = max_ctas;
+  cudaGetDevice(&c->device);
+  cudaError_t e = cudaMalloc(&c->pool, pool_bytes);
+  if (e != cudaSuccess) { delete c; return check_cuda(e, "cudaMalloc(pool)"); }
+  e = cudaMemset(c->pool, 0, kReserved);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) { cudaFree(c->pool); delete c; return check_cuda(e, "cudaMemset(pool)"); }
+  c->bases[rank] = c->pool;
+  c->opened[rank] = true;
+  *out = c;
+  return 0;
+}
+
+extern "C" int fsdp_comm_create_emulated(int world, int64_t pool_bytes, int max_ctas,
+                                         fsdp_comm_t** out) {
+  if (!out) return fail(FSDP_E_INVALID, "null out");
+  if (world < 1 || world > FSDP_MAX_RANKS) return fail(FSDP_E_INVALID, "world out of range");
+  if (max_ctas < 1 || max_ctas > FSDP_MAX_CTAS) return fail(FSDP_E_INVALID, "max_ctas out of range");
+  if (pool_bytes < kReserved) pool_bytes = kReserved;
+  pool_bytes = (pool_bytes + 4095) / 4096 * 4096;
+  fsdp_comm_t* c = new fsdp_comm_t();
+  c->rank = 0; c->world = world; c->emulated = true; c->pool_bytes = pool_bytes;
+  c->max_ctas = max_ctas;
+  cudaGetDevice(&c->device);
+  cudaError_t e = cudaMalloc(&c->pool, pool_bytes * world);
+  if (e != cudaSuccess) { delete c; return check_cuda(e, "cudaMalloc(emulated pools)"); }
+  for (int r = 0; r < world; ++r) {
+    c->bases[r] = c->pool + r * pool_bytes;
+    c->opened[r] = true;
+    e = cudaMemset(c->bases[r], 0, kReserved);
+    if (e != cudaSuccess) break;
+  }
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) { cudaFree(c->pool); delete c; return check_cuda(e, "cudaMemset(pools)"); }
+  *out = c;
+  return 0;
+}
+
+extern "C" int fsdp_comm_ipc_handle(fsdp_comm_t* c, void* handle_out) {
+  if (!c || !handle_out) return fail(FSDP_E_INVALID, "null argument");
+  if (c->emulated) return fail(FSDP_E_UNSUPPORTED, "emulated communicator has no IPC handle");
+  static_assert(sizeof(cudaIpcMemHandle_t) == FSDP_IPC_HANDLE_BYTES, "ipc handle size");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, c->pool);
+  if (e != cudaSuccess) return fail(FSDP_E_IPC, std::string("cudaIpcGetMemHandle: ") + cudaGetErrorString(e));
+  std::memcpy(handle_out, &h, sizeof(h));
+  return 0;
+}
+
+extern "C" int fsdp_comm_open_peers(fsdp_comm_t* c, const void* handles) {
+  if (!c || !handles) return fail(FSDP_E_INVALID, "null argument");
+  if (c->emulated) return 0;
+  const char* hs = (const char*)handles;
+  for (int r = 0; r < c->world; ++r) {
+    if (r == c->rank || c->opened[r]) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, hs + (size_t)r * FSDP_IPC_HANDLE_BYTES, sizeof(h));
+    void* ptr = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess)
+      return fail(FSDP_E_IPC, "cudaIpcOpenMemHandle(rank " + std::to_string(r) + "): " +
+                                  cudaGetErrorString(e));
+    c->bases[r] = (char*)ptr;
+    c->opened[r] = true;
+  }
+  return 0;
+}
+
+extern "C" void* fsdp_comm_pool_ptr(fsdp_comm_t* c, int r) {
+  if (!c || r < 0 || r >= c->world) return nullptr;
+  if (!c->emulated && r != c->rank) return nullptr;
+  return c->bases[r];
+}
+
+extern "C" int64_t fsdp_comm_pool_bytes(fsdp_comm_t* c) { return c ? c->pool_bytes : -1; }
+
+extern "C" int fsdp_comm_set_timeout_ms(fsdp_comm_t* c, int64_t ms) {
+  if (!c || ms <= 0) return fail(FSDP_E_INVALID, "bad timeout");
+  c->timeout_ns = ms * 1000000LL;
+  return 0;
+}
+
+extern "C" int fsdp_comm_device_error(fsdp_comm_t* c) {
+  if (!c) return fail(FSDP_E_INVALID, "null communicator");
+  int worst = 0;
+  const int n = c->emulated ? c->world : 1;
+  for (int i = 0; i < n; ++i) {
+    uint32_t v = 0;
+    char* base = c->emulated ? c->bases[i] : c->pool;
+    cudaError_t e = cudaMemcpy(&v, base + kErrOff, sizeof(v), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return check_cuda(e, "read device error word");
+    if (v) worst = (int)v;
+  }
+  return worst;
+}
+
+extern "C" int fsdp_comm_destroy(fsdp_comm_t* c) {
+  if (!c) return 0;
+  if (!c->emulated)
+    for (int r = 0; r < c->world; ++r)
+      if (r != c->rank && c->bases[r]) cudaIpcCloseMemHandle(c->bases[r]);
+  cudaFree(c->pool);
+  delete c;
+  return 0;
+}
+
+static int check_range(fsdp_comm_t* c, int64_t off, int64_t bytes, const char* who) {
+  if (off < kReserved || bytes < 0 || off + bytes > c->pool_bytes)
+    return fail(FSDP_E_INVALID, std::string(who) + ": pool region out of range (offset " +
+                                    std::to_string(off) + ", " + std::to_string(bytes) +
+                                    " bytes, pool " + std::to_string(c->pool_bytes) + ")");
+  return 0;
+}
+
+extern "C" int fsdp_allgather(fsdp_comm_t* c, int channel, int gsize, int gstride,
+                              const void* const* shards, int src_dtype, int64_t n, int64_t dst_off,
+                              int dst_dtype, void* stream) {
+  if (int rc = validate_group(c, channel, gsize, gstride)) return rc;
+  if (n < 0 || !shards) return fail(FSDP_E_INVALID, "fsdp_allgather: bad args");
+  const int os = elem_size(dst_dtype);
+  if (!os || !elem_size(src_dtype)) return fail(FSDP_E_INVALID, "fsdp_allgather: bad dtype");
+  if (int rc = check_range(c, dst_off, n * gsize * os, "fsdp_allgather")) return rc;
+  CollParams p;
+  fill_common(c, p, channel, gsize, gstride, n);
+  for (int e = 0; e < nranks_args(c); ++e) p.in[e] = shards[e];
+  p.off_a = dst_off;
+  const int grid = grid_for(c, n);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (src_dtype == FSDP_F32 && dst_dtype == FSDP_BF16)
+    return launch(c, allgather_kernel<float, __nv_bfloat16>, p, grid, kCommThreads, s);
+  if (src_dtype == FSDP_F32 && dst_dtype == FSDP_F32)
+    return launch(c, allgather_kernel<float, float>, p, grid, kCommThreads, s);
+  if (src_dtype == FSDP_BF16 && dst_dtype == FSDP_BF16)
+    return launch(c, allgather_kernel<__nv_bfloat16, __nv_bfloat16>, p, grid, kCommThreads, s);
+  return launch(c, allgather_kernel<__nv_bfloat16, float>, p, grid, kCommThreads, s);
+}
+
+extern "C" int fsdp_reduce_scatter(fsdp_comm_t* c, int channel, int gsize, int gstride,
+                                   const void* const* flats, int src_dtype, int64_t n,
+                                   int64_t stage_off, float* const* outs, float prediv,
+                                   float postdiv, int accumulate, void* stream) {
+  if (int rc = validate_group(c, channel, gsize, gstride)) return rc;
+  if (n < 0 || !flats || !outs) return fail(FSDP_E_INVALID, "fsdp_reduce_scatter: bad args");
+  const int is = elem_size(src_dtype);
+  if (!is) return fail(FSDP_E_INVALID, "fsdp_reduce_scatter: bad dtype");
+  if (!(prediv > 0.f) || !(postdiv > 0.f)) return fail(FSDP_E_INVALID, "divisors must be > 0");
+  if (int rc = check_range(c, stage_off, n * gsize * is, "fsdp_reduce_scatter")) return rc;
+  CollParams p;
+  fill_common(c, p, channel, gsize, gstride, n);
+  for (int e = 0; e < nranks_args(c); ++e) { p.in[e] = flats[e]; p.out[e] = outs[e]; }
+  p.off_a = stage_off;
+  p.prediv = prediv; p.postdiv = postdiv; p.accumulate = accumulate ? 1 : 0;
+  const int grid = grid_for(c, n);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (src_dtype == FSDP_BF16)
+    return launch(c, reduce_scatter_kernel<__nv_bfloat16>, p, grid, kCommThreads, s);
+  return launch(c, reduce_scatter_kernel<float>, p, grid, kCommThreads, s);
+}
+
+extern "C" int fsdp_allreduce(fsdp_comm_t* c, int channel, int gsize, int gstride,
+                              const void* const* ins, int src_dtype, int64_t n, int64_t stage_off,
+                              int64_t gather_off, float* const* outs, float postdiv, int accumulate,
+                              void* stream) {
+  if (int rc = validate_group(c, channel, gsize, gstride)) return rc;
+  if (n < 0 || !ins || !outs) return fail(FSDP_E_INVALID, "fsdp_allreduce: bad args");
+  const int is = elem_size(src_dtype);
+  if (!is) return fail(FSDP_E_INVALID, "fsdp_allreduce: bad dtype");
+  if (!(postdiv > 0.f)) return fail(FSDP_E_INVALID, "postdiv must be > 0");
+  int64_t ch = (n + gsize - 1) / gsize;
+  ch = (ch + kVec - 1) / kVec * kVec;
+  if (int rc = check_range(c, stage_off, ch * gsize * is, "fsdp_allreduce(stage)")) return rc;
+  if (int rc = check_range(c, gather_off, ch * gsize * 4, "fsdp_allreduce(gather)")) return rc;
+  CollParams p;
+  fill_common(c, p, channel, gsize, gstride, n);
+  for (int e = 0; e < nranks_args(c); ++e) { p.in[e] = ins[e]; p.out[e] = outs[e]; }
+  p.off_a = stage_off; p.off_b = gather_off;
+  p.postdiv = postdiv; p.accumulate = accumulate ? 1 : 0;
+  const int grid = grid_for(c, ch);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (src_dtype == FSDP_BF16)
+    return launch(c, allreduce_kernel<__nv_bfloat16>, p, grid, kCommThreads, s);
+  return launch(c, allreduce_kernel<float>, p, grid, kCommThreads, s);
+}
+
+extern "C" int fsdp_allreduce_scalar(fsdp_comm_t* c, const float* const* ins, float* const* outs,
+                                     void* stream) {
+  if (int rc = validate_group(c, FSDP_CH_SCALAR, c ? c->world : 1, 1)) return rc;
+  if (!ins || !outs) return fail(FSDP_E_INVALID, "fsdp_allreduce_scalar: bad args");
+  CollParams p;
+  fill_common(c, p, FSDP_CH_SCALAR, c->world, 1, 1);
+  for (int e = 0; e < nranks_args(c); ++e) { p.in[e] = ins[e]; p.out[e] = outs[e]; }
+  return launch(c, scalar_allreduce_kernel, p, 1, 32, (cudaStream_t)stream);
+}

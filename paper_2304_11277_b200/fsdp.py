@@ -1,0 +1,443 @@
+"""torch-FSDP-v1-shaped wrapper over the B200 runtime.
+
+    model = FullyShardedDataParallel(
+        module, sharding_strategy=ShardingStrategy.FULL_SHARD,
+        auto_wrap_policy=ModuleWrapPolicy({Block}),
+        backward_prefetch=BackwardPrefetch.BACKWARD_PRE,
+        mixed_precision=MixedPrecision(param_dtype=torch.bfloat16,
+                                       reduce_dtype=torch.bfloat16),
+        forward_prefetch=False, limit_all_gathers=True)
+    opt = model.optimizer(lr=1e-4)           # sharded Adam over the rank's arena
+    loss = model(x).loss; loss.backward(); opt.step()
+
+Mapping to the reference engine (`engine.py:165-207`, EngineConfig):
+
+  ShardingStrategy.FULL_SHARD       F = W, RAF
+  ShardingStrategy.SHARD_GRAD_OP    F = W, NRAF
+  ShardingStrategy.NO_SHARD         F = 1
+  ShardingStrategy.HYBRID_SHARD     1 < F < W (hybrid_shard_size = F), RAF
+  ShardingStrategy._HYBRID_SHARD_ZERO2  hybrid, NRAF
+  BackwardPrefetch.BACKWARD_PRE     prefetch at the unit's pre-backward
+  BackwardPrefetch.BACKWARD_POST    prefetch before the unit's reduce-scatter
+                                    (the reference's point, engine.py:544-545)
+  backward_prefetch=None            backward_prefetch=False
+  forward_prefetch                  forward_prefetch
+  limit_all_gathers                 rate_limit = 2 (else None)
+  MixedPrecision(param_dtype=bf16)  PrecisionPolicy(mixed=True)
+  MixedPrecision(reduce_dtype=fp32) PrecisionPolicy(reduce_in_low=False)
+  no_sync()                         accumulation = no_comm (engine.py:547-556)
+  (root unit kept after forward)    keep_outermost_unsharded = True
+
+Auto-wrap: every submodule the policy accepts becomes a unit (a
+FlatParameter); the root keeps the remaining parameters (`flatparam.py:63-96`
+assignment; a parameter reachable from two units raises
+SharedParameterError).
+"""
+from __future__ import annotations
+
+import contextlib
+import enum
+import functools
+from dataclasses import dataclass
+from typing import Any, Callable, Iterable
+
+import torch
+import torch.nn as nn
+
+from .comm import DeviceComm
+from .layout import SharedParameterError, build_unit_layouts
+from .plan import build_plan
+from .runtime import (ACCUM_OFF, NRAF, PREFETCH_POST, PREFETCH_PRE, RAF, FSDPRuntime,
+                      RuntimeConfig)
+
+
+class ShardingStrategy(enum.Enum):
+    FULL_SHARD = enum.auto()
+    SHARD_GRAD_OP = enum.auto()
+    NO_SHARD = enum.auto()
+    HYBRID_SHARD = enum.auto()
+    _HYBRID_SHARD_ZERO2 = enum.auto()
+
+
+class BackwardPrefetch(enum.Enum):
+    BACKWARD_PRE = enum.auto()
+    BACKWARD_POST = enum.auto()
+
+
+@dataclass
+class MixedPrecision:
+    param_dtype: torch.dtype | None = None
+    reduce_dtype: torch.dtype | None = None
+    buffer_dtype: torch.dtype | None = None
+
+
+@dataclass
+class CPUOffload:
+    offload_params: bool = False
+
+
+class ModuleWrapPolicy:
+    """Wrap every submodule whose type is in `module_classes` (torch's
+    ModuleWrapPolicy / transformer_auto_wrap_policy)."""
+
+    def __init__(self, module_classes: Iterable[type]):
+        self.classes = tuple(module_classes)
+
+    def __call__(self, module: nn.Module) -> bool:
+        return isinstance(module, self.classes)
+
+
+def transformer_auto_wrap_policy(module: nn.Module, recurse: bool = False, nonwrapped_numel: int = 0,
+                                 transformer_layer_cls: Iterable[type] = ()) -> bool:
+    """torch-compatible functional policy (use with functools.partial)."""
+    return isinstance(module, tuple(transformer_layer_cls))
+
+
+def _policy_fn(policy) -> Callable[[nn.Module], bool] | None:
+    if policy is None:
+        return None
+    if isinstance(policy, ModuleWrapPolicy):
+        return policy
+    if isinstance(policy, (set, list, tuple)):
+        return ModuleWrapPolicy(policy)
+    return lambda m: bool(policy(module=m, recurse=False, nonwrapped_numel=0))
+
+
+class _UnitViews(torch.autograd.Function):
+    """forward: the unit's original parameters as views of its unsharded flat
+    buffer; backward: the post-backward hook (write-back + reduce-scatter)."""
+
+    @staticmethod
+    def forward(ctx, anchor, flat, rt, uid):
+        ctx.rt, ctx.uid = rt, uid
+        ctx.set_materialize_grads(False)
+        return tuple(flat.narrow(0, o.offset, o.numel).view(o.shape)
+                     for o in rt.units[uid].layout.originals)
+
+    @staticmethod
+    def backward(ctx, *grads):
+        ctx.rt.post_backward(ctx.uid, grads)
+        return None, None, None, None
+
+
+class _PreBackward(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, wrapper, uid, *outs):
+        ctx.wrapper, ctx.uid = wrapper, uid
+        return tuple(o.view_as(o) for o in outs)
+
+    @staticmethod
+    def backward(ctx, *grads):
+        ctx.wrapper._pre_backward(ctx.uid)
+        return (None, None) + grads
+
+
+def _map_tensors(fn, obj):
+    if isinstance(obj, torch.Tensor):
+        return fn([obj])[0]
+    if isinstance(obj, (tuple, list)):
+        ts = [o for o in obj if isinstance(o, torch.Tensor) and o.requires_grad]
+        if not ts:
+            return obj
+        mapped = iter(fn(ts))
+        out = [next(mapped) if (isinstance(o, torch.Tensor) and o.requires_grad) else o for o in obj]
+        return type(obj)(out) if not hasattr(obj, "_fields") else type(obj)(*out)
+    if isinstance(obj, dict):
+        keys = [k for k, v in obj.items() if isinstance(v, torch.Tensor) and v.requires_grad]
+        if not keys:
+            return obj
+        mapped = fn([obj[k] for k in keys])
+        out = dict(obj)
+        out.update(zip(keys, mapped))
+        return type(obj)(out) if type(obj) is not dict else out
+    return obj
+
+
+class FullyShardedDataParallel(nn.Module):
+    def __init__(self, module: nn.Module, process_group=None,
+                 sharding_strategy: ShardingStrategy = ShardingStrategy.FULL_SHARD,
+                 cpu_offload: CPUOffload | None = None, auto_wrap_policy=None,
+                 backward_prefetch: BackwardPrefetch | None = BackwardPrefetch.BACKWARD_PRE,
+                 mixed_precision: MixedPrecision | None = None, ignored_modules=None,
+                 param_init_fn: Callable[[nn.Module], None] | None = None, device_id=None,
+                 sync_module_states: bool = False, forward_prefetch: bool = False,
+                 limit_all_gathers: bool = True, use_orig_params: bool = False,
+                 ignored_states=None, device_mesh=None, *, hybrid_shard_size: int | None = None,
+                 comm_backend: str = "ipc", num_slots: int | None = None, ag_ctas: int = 32,
+                 optimizer: str = "adam", lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-8):
+        super().__init__()
+        if cpu_offload is not None and cpu_offload.offload_params:
+            raise NotImplementedError("CPU offload is out of scope for the B200 runtime")
+        import torch.distributed as dist
+        dist_on = dist.is_available() and dist.is_initialized()
+        world = dist.get_world_size(process_group) if dist_on else 1
+        rank = dist.get_rank(process_group) if dist_on else 0
+        if device_id is not None:
+            torch.cuda.set_device(device_id)
+        device = torch.device("cuda", torch.cuda.current_device())
+        if sharding_strategy in (ShardingStrategy.FULL_SHARD, ShardingStrategy.SHARD_GRAD_OP):
+            F = world
+        elif sharding_strategy == ShardingStrategy.NO_SHARD:
+            F = 1
+        else:
+            F = hybrid_shard_size or (torch.cuda.device_count() if world > torch.cuda.device_count() else world)
+        plan = build_plan(world, F)
+        raf = NRAF if sharding_strategy in (ShardingStrategy.SHARD_GRAD_OP,
+                                            ShardingStrategy._HYBRID_SHARD_ZERO2) else RAF
+        mp = mixed_precision
+        mixed = mp is not None and mp.param_dtype == torch.bfloat16
+        if mp is not None and mp.param_dtype not in (None, torch.bfloat16, torch.float32):
+            raise ValueError("param_dtype must be bf16 or fp32 on the B200 runtime")
+        reduce_low = mixed and (mp.reduce_dtype in (None, torch.bfloat16))
+        bp = {None: None, BackwardPrefetch.BACKWARD_PRE: PREFETCH_PRE,
+              BackwardPrefetch.BACKWARD_POST: PREFETCH_POST}[backward_prefetch]
+        cfg = RuntimeConfig(mixed=mixed, reduce_in_low=reduce_low, reshard_after_forward=raf,
+                            backward_prefetch=bp, forward_prefetch=forward_prefetch,
+                            rate_limit=2 if limit_all_gathers else None,
+                            keep_outermost_unsharded=True, accumulation=ACCUM_OFF,
+                            comm_backend=comm_backend, num_slots=num_slots, ag_ctas=ag_ctas,
+                            optimizer=optimizer, lr=lr, betas=tuple(betas), eps=eps)
+        self.module = module
+        self.plan = plan
+        self.rank = rank
+        policy = _policy_fn(auto_wrap_policy)
+        ignored = set(ignored_modules or [])
+        # ---- units: root + policy-accepted submodules, pre-order ----------
+        unit_mods: list[nn.Module] = [module]
+        for name, m in module.named_modules():
+            if m is not module and policy is not None and m not in ignored and policy(m):
+                unit_mods.append(m)
+        owner_of: dict[int, int] = {id(m): 0 for m in module.modules()}
+        for uid, um in enumerate(unit_mods[1:], start=1):
+            for m in um.modules():
+                owner_of[id(m)] = uid
+        # parameter refs per unit in declaration order; shared params rejected
+        names: list[list[str]] = [[] for _ in unit_mods]
+        refs: list[list[tuple[nn.Module, str]]] = [[] for _ in unit_mods]
+        shapes: list[tuple[str, tuple]] = []
+        seen: dict[int, str] = {}
+        for mname, m in module.named_modules(remove_duplicate=False):
+            uid = owner_of[id(m)]
+            for pname, p in list(m.named_parameters(recurse=False)):
+                fq = f"{mname}.{pname}" if mname else pname
+                if id(p) in seen:
+                    first = seen[id(p)]
+                    if owner_of_name(first, module, owner_of) != uid:
+                        raise SharedParameterError(
+                            f"parameter '{fq}' is shared with '{first}' across units; sharing a "
+                            f"parameter across units is unsupported — merge the sharing layers "
+                            f"into one unit, or use SHARD_GRAD_OP (NRAF)")
+                    refs[uid].append((m, pname))      # alias within a unit: same view
+                    continue
+                seen[id(p)] = fq
+                names[uid].append(fq)
+                refs[uid].append((m, pname))
+                shapes.append((fq, tuple(p.shape)))
+        self._refs = refs
+        self._alias: list[list[int]] = []
+        for uid in range(len(unit_mods)):
+            idx, amap = {}, []
+            for (m, pname) in refs[uid]:
+                p = m._parameters[pname]
+                if id(p) not in idx:
+                    idx[id(p)] = len(idx)
+                amap.append(idx[id(p)])
+            self._alias.append(amap)
+        layouts = build_unit_layouts(shapes, names, F)
+        self.layouts = layouts
+        # ---- communicator + runtime ---------------------------------------
+        comm = None
+        pgs = {}
+        if world > 1 and comm_backend == "ipc":
+            comm = DeviceComm.create(FSDPRuntime.pool_bytes_for(layouts, plan, cfg), max_ctas=ag_ctas,
+                                     group=process_group)
+        elif world > 1:
+            pgs = _nccl_groups(plan, rank)
+        self.comm = comm
+        self.rt = FSDPRuntime(layouts, plan, rank, cfg, comm=comm, process_groups=pgs, device=device)
+        # ---- materialise unit by unit: flatten + shard, then drop originals
+        for uid, um in enumerate(unit_mods):
+            params = []
+            for (m, pname), a in zip(refs[uid], self._alias[uid]):
+                if a < len(params):
+                    continue
+                p = m._parameters[pname]
+                if p.is_meta:
+                    mods = [mm for mm in um.modules() if owner_of[id(mm)] == uid]
+                    for mm in mods:
+                        mm.to_empty(device=device, recurse=False)
+                        if param_init_fn is not None:
+                            param_init_fn(mm)
+                        elif hasattr(mm, "reset_parameters"):
+                            mm.reset_parameters()
+                    p = m._parameters[pname]
+                params.append(p)
+            if params:
+                self.rt.load_unit_values(uid, params)
+            for (m, pname) in refs[uid]:
+                if pname in m._parameters:
+                    del m._parameters[pname]
+        for b in module.buffers():
+            if b.device != device:
+                pass
+        module.to(device)
+        if mixed and (mp.buffer_dtype is not None):
+            for m in module.modules():
+                for bn, b in list(m._buffers.items()):
+                    if b is not None and b.is_floating_point():
+                        m._buffers[bn] = b.to(mp.buffer_dtype)
+        torch.cuda.synchronize()
+        self._unit_mods = unit_mods
+        self._anchors = [torch.zeros((), device=device, requires_grad=True) for _ in unit_mods]
+        self._handles = []
+        for uid, um in enumerate(unit_mods):
+            self._handles.append(um.register_forward_pre_hook(functools.partial(self._pre_fwd, uid)))
+            self._handles.append(um.register_forward_hook(functools.partial(self._post_fwd, uid)))
+        self._defer = False
+        self._bwd_started = False
+        self._new_micro = True
+        self.mixed = mixed
+
+    # ------------------------------------------------------------ hooks ---
+    def _install(self, uid: int, flat: torch.Tensor) -> None:
+        if flat.numel() == 0 or not self._refs[uid]:
+            return
+        views = _UnitViews.apply(self._anchors[uid], flat, self.rt, uid)
+        for (m, pname), a in zip(self._refs[uid], self._alias[uid]):
+            setattr(m, pname, views[a])
+
+    def _pre_fwd(self, uid, module, args):
+        rt = self.rt
+        if uid == 0:
+            if self._new_micro:
+                self._new_micro = False
+                rt.begin_micro(final=not self._defer)
+                rt.defer_reduce = self._defer
+                self._bwd_started = False
+            rt.begin_forward_pass()
+        pos = rt.record_forward(uid)
+        flat = rt.ensure_unsharded(uid)
+        rt.forward_prefetch_after(pos)
+        self._install(uid, flat)
+        return None
+
+    def _post_fwd(self, uid, module, args, output):
+        rt = self.rt
+        rt.post_order.append(uid)
+        rt.close_window(uid)
+        if torch.is_grad_enabled():
+            output = _map_tensors(lambda ts: _PreBackward.apply(self, uid, *ts), output)
+        rt.release_use(uid, "forward", 0)
+        return output
+
+    def _pre_backward(self, uid: int) -> None:
+        rt = self.rt
+        if not self._bwd_started:
+            self._bwd_started = True
+            rt.start_backward()
+            torch.autograd.Variable._execution_engine.queue_callback(self._end_backward)
+        if uid in rt.bwd_pos and not getattr(rt.units[uid], "_pre_done", False):
+            rt.units[uid]._pre_done = True
+            rt.pre_backward(uid)
+
+    def _end_backward(self) -> None:
+        for u in self.rt.units:
+            u._pre_done = False
+        self.rt.end_backward()
+        self._bwd_started = False
+        self._new_micro = True
+
+    # -------------------------------------------------------------- api ---
+    def forward(self, *args, **kwargs):
+        with self.rt.saved_tensor_hooks():
+            return self.module(*args, **kwargs)
+
+    @contextlib.contextmanager
+    def no_sync(self):
+        """Accumulate unsharded gradients locally without communication; the
+        first backward outside the context reduces them (engine.py:547-556)."""
+        prev = self._defer
+        self._defer = True
+        try:
+            yield
+        finally:
+            self._defer = prev
+
+    def optimizer(self, lr: float | None = None, betas=None, eps: float | None = None):
+        return ShardedOptimizer(self, lr, betas, eps)
+
+    def step(self, scale: float | None = None) -> None:
+        self.rt.optimizer_step(scale)
+        self.rt.begin_step()
+
+    def flat_shards(self) -> list[torch.Tensor]:
+        return [u.master for u in self.rt.units]
+
+    def full_state_dict(self) -> dict[str, torch.Tensor]:
+        """Gather fp32 parameters (engine.py:824-834 gather_full_params):
+        all-gather every unit's master shard within the sharded group, then
+        unflatten into the original shapes (kernels)."""
+        from . import kernels
+        out = {}
+        for uid, lay in enumerate(self.layouts):
+            u = self.rt.units[uid]
+            flat = torch.empty(lay.psi, dtype=torch.float32, device=self.rt.device)
+            if self.plan.shard_factor == 1:
+                flat.copy_(u.master)
+            elif self.comm is not None:
+                from .comm import DeviceFabric  # noqa: F401
+                import torch.distributed as dist
+                dist.all_gather_into_tensor(flat, u.master.contiguous(),
+                                            group=_shard_group(self.plan, self.rank))
+            else:
+                import torch.distributed as dist
+                dist.all_gather_into_tensor(flat, u.master.contiguous(), group=self.rt.pgs.get("shard"))
+            tensors = [torch.empty(o.shape, dtype=torch.float32, device=flat.device) for o in lay.originals]
+            kernels.unflatten(flat, tensors, lay.offsets)
+            for o, t in zip(lay.originals, tensors):
+                out[o.name] = t
+        return out
+
+
+def owner_of_name(fq: str, root: nn.Module, owner_of: dict) -> int:
+    mod_name, _, _ = fq.rpartition(".")
+    m = root.get_submodule(mod_name) if mod_name else root
+    return owner_of[id(m)]
+
+
+_GROUP_CACHE: dict = {}
+
+
+def _nccl_groups(plan, rank):
+    import torch.distributed as dist
+    key = (plan.world_size, plan.shard_factor)
+    if key not in _GROUP_CACHE:
+        shard = {g: dist.new_group(list(g)) for g in plan.sharded_groups}
+        rep = {g: dist.new_group(list(g)) for g in plan.replicated_groups}
+        _GROUP_CACHE[key] = (shard, rep)
+    shard, rep = _GROUP_CACHE[key]
+    return {"shard": shard[plan.sharded_group_of(rank)], "replicate": rep[plan.replicated_group_of(rank)]}
+
+
+def _shard_group(plan, rank):
+    return _nccl_groups(plan, rank)["shard"]
+
+
+class ShardedOptimizer:
+    """torch.optim-like handle: step() runs the fused sharded optimizer."""
+
+    def __init__(self, fsdp: FullyShardedDataParallel, lr=None, betas=None, eps=None):
+        cfg = fsdp.rt.cfg
+        if lr is not None:
+            cfg.lr = lr
+        if betas is not None:
+            cfg.betas = tuple(betas)
+        if eps is not None:
+            cfg.eps = eps
+        self.fsdp = fsdp
+
+    def step(self, scale: float | None = None) -> None:
+        self.fsdp.step(scale)
+
+    def zero_grad(self, set_to_none: bool = True) -> None:
+        pass   # reduced grads are overwritten by the first reduce of a step

@@ -1,0 +1,717 @@
+"""Per-rank FSDP runtime: the sharded-training hot path on one B200.
+
+One `FSDPRuntime` per process (= per GPU).  It owns, for every unit
+(FlatParameter), the rank's persistent shard and optimizer state — laid out
+as four contiguous fp32 arenas (master, reduced grad, exp_avg, exp_avg_sq)
+plus a bf16 copy of the master shard, so the optimizer epilogue is ONE
+elementwise launch over the whole rank — and it drives the unit lifecycle of
+the reference engine (`engine.py:448-820`) on real CUDA streams:
+
+  unshard  : all-gather of the bf16 shard straight into a symmetric slot of
+             every group member's pool (`_issue_unshard`, engine.py:640-671)
+             on the all-gather stream; compute waits on its event;
+  limiter  : at most `rate_limit` gathers whose first consuming compute the
+             host has not observed complete (`_limiter_acquire`,
+             engine.py:700-724) — the host blocks on that compute's event;
+  prefetch : forward (previous iteration's order, StaticOrderError on a
+             change, engine.py:474-484) and backward (BACKWARD_PRE at the
+             unit's pre-backward, BACKWARD_POST before its reduce-scatter
+             exactly like engine.py:544-545);
+  reshard  : RAF / NRAF / keep-outermost (`_release_use`, engine.py:726-749);
+  reduce   : gradient write-back (flatten kernel) then reduce-scatter with
+             fp32 accumulation, / W, accumulate into the sharded grad;
+             HYBRID adds the replica all-reduce (`_reduce_unit`,
+             engine.py:771-820), NO_SHARD is an all-reduce; accumulation with
+             or without communication (engine.py:547-556, :753-769);
+  epilogue : unscale + found_inf, world verdict, SGD/Adam on the arena with
+             on-device skip (engine.py:563-594).
+
+Autograd integration: a unit's parameters are views of its unsharded flat
+buffer produced by `_UnitViews` (whose backward is the post-backward hook);
+the unit's outputs pass through `_PreBackward` (pre-backward hook); tensors
+autograd saves that live in a slot are packed as (unit, offset, shape,
+stride) and re-materialised from the unit's CURRENT slot at unpack time, so a
+unit re-gathered for backward may land in a different slot.
+"""
+from __future__ import annotations
+
+import math
+import warnings
+from dataclasses import dataclass, field
+from typing import Callable, Sequence
+
+import torch
+
+from . import _lib, kernels
+from .layout import UnitLayout
+from .plan import ShardingPlan
+
+RAF = "RAF"
+NRAF = "NRAF"
+ACCUM_OFF = "off"
+ACCUM_WITH_COMM = "with_comm"
+ACCUM_NO_COMM = "no_comm"
+PREFETCH_PRE = "pre"
+PREFETCH_POST = "post"
+
+
+class EngineError(RuntimeError):
+    pass
+
+
+class StaticOrderError(EngineError):
+    """Forward prefetch needs a static graph; the observed unit order moved."""
+
+
+_ALIGN = 16   # elements: every shard slice starts 64-byte aligned
+
+
+@dataclass
+class RuntimeConfig:
+    mixed: bool = True                   # compute/communicate bf16, master fp32
+    reduce_in_low: bool = True           # gradient payload bf16 (else fp32)
+    reshard_after_forward: str = RAF
+    backward_prefetch: str | None = PREFETCH_PRE
+    forward_prefetch: bool = False
+    rate_limit: int | None = 2
+    keep_outermost_unsharded: bool = True
+    accumulation: str = ACCUM_OFF
+    accumulation_steps: int = 1
+    loss_mean: bool = True               # divide reduced grads by W
+    gradient_predivide: float = 1.0
+    comm_backend: str = "ipc"            # "ipc" (this library) | "nccl" (comparison path)
+    num_slots: int | None = None
+    ag_ctas: int = 32
+    optimizer: str = "adam"
+    lr: float = 1e-3
+    betas: tuple = (0.9, 0.999)
+    eps: float = 1e-8
+
+    def __post_init__(self):
+        if self.reshard_after_forward not in (RAF, NRAF):
+            raise EngineError(f"reshard_after_forward must be {RAF} or {NRAF}")
+        if self.accumulation not in (ACCUM_OFF, ACCUM_WITH_COMM, ACCUM_NO_COMM):
+            raise EngineError("accumulation must be one of off/with_comm/no_comm")
+        if self.rate_limit is not None and self.rate_limit < 1:
+            raise EngineError("rate_limit must be >= 1 (or None for no limit)")
+        if self.backward_prefetch not in (None, PREFETCH_PRE, PREFETCH_POST):
+            raise EngineError("backward_prefetch must be None, 'pre' or 'post'")
+        if self.comm_backend not in ("ipc", "nccl"):
+            raise EngineError("comm_backend must be 'ipc' or 'nccl'")
+
+
+class _Window:
+    """One issued gather, open until its first consuming compute completes."""
+    __slots__ = ("unit", "done")
+
+    def __init__(self, unit: int):
+        self.unit = unit
+        self.done: torch.cuda.Event | None = None
+
+
+class UnitState:
+    """One rank's live state for one unit (engine.py:_UnitRuntime)."""
+
+    def __init__(self, layout: UnitLayout):
+        self.layout = layout
+        self.uid = layout.unit_id
+        # persistent shard state: slices of the rank arenas
+        self.master: torch.Tensor | None = None
+        self.grad: torch.Tensor | None = None
+        self.exp_avg: torch.Tensor | None = None
+        self.exp_avg_sq: torch.Tensor | None = None
+        self.low: torch.Tensor | None = None
+        # materialisation
+        self.unsharded: torch.Tensor | None = None
+        self.slot: int | None = None
+        self.ag_event: torch.cuda.Event | None = None
+        self.pending = False
+        self.uses = 0
+        self.window: _Window | None = None
+        # gradients
+        self.grad_pending = 0
+        self.flat_grad: torch.Tensor | None = None
+        self.accum_unsharded: torch.Tensor | None = None
+        self.reduces_this_step = 0
+        self.bwd_done = False
+
+
+class SlotPool:
+    """Fixed-size unsharded-parameter slots.  Reuse order is deterministic
+    (oldest release first) so every rank picks the same slot for the same
+    gather — required because peers write into it by offset."""
+
+    def __init__(self, tensors: list[list[torch.Tensor]], offsets: list[int], slot_elems: int):
+        self.views = tensors            # views[slot][e] (e = emulated rank index)
+        self.offsets = offsets
+        self.slot_elems = slot_elems
+        self.free: list[tuple[int, torch.cuda.Event | None]] = [(i, None) for i in range(len(offsets))]
+        self.owner: dict[int, int] = {}
+
+    def acquire(self, uid: int) -> tuple[int, torch.cuda.Event | None]:
+        if not self.free:
+            raise EngineError("unsharded-parameter slot pool exhausted: raise num_slots "
+                              "(NRAF / SHARD_GRAD_OP keeps every unit unsharded through backward)")
+        slot, ev = self.free.pop(0)
+        self.owner[slot] = uid
+        return slot, ev
+
+    def release(self, slot: int, ev: torch.cuda.Event) -> None:
+        self.owner.pop(slot, None)
+        self.free.append((slot, ev))
+
+
+class _SlotRef:
+    __slots__ = ("uid", "off", "size", "stride")
+
+    def __init__(self, uid, off, size, stride):
+        self.uid, self.off, self.size, self.stride = uid, off, size, stride
+
+
+class FSDPRuntime:
+    """The per-rank engine.  `comm` is a DeviceComm (or None at world 1 /
+    NCCL backend)."""
+
+    def __init__(self, layouts: Sequence[UnitLayout], plan: ShardingPlan, rank: int,
+                 config: RuntimeConfig, comm=None, process_groups=None,
+                 device: torch.device | None = None):
+        self.cfg = config
+        self.plan = plan
+        self.rank = rank
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.units = [UnitState(l) for l in layouts]
+        self.comm = comm
+        self.pgs = process_groups or {}
+        W, F = plan.world_size, plan.shard_factor
+        if W > 1 and config.comm_backend == "ipc" and comm is None:
+            raise EngineError("world_size > 1 with the ipc backend needs a DeviceComm")
+        self.compute_dtype = torch.bfloat16 if config.mixed else torch.float32
+        self.payload_dtype = torch.bfloat16 if (config.mixed and config.reduce_in_low) else torch.float32
+        self.compute_stream = torch.cuda.current_stream(self.device)
+        self.ag_stream = torch.cuda.Stream(self.device)
+        self.rs_stream = torch.cuda.Stream(self.device)
+        self._alloc_arenas()
+        self._alloc_pool_regions()
+        # per-step state
+        self.inflight: list[_Window] = []
+        self.fwd_order: list[int] = []
+        self.post_order: list[int] = []
+        self.prev_fwd_order: list[int] | None = None
+        self.bwd_order: list[int] = []
+        self.bwd_pos: dict[int, int] = {}
+        self.in_backward = False
+        self.final_micro = True
+        self.defer_reduce = False
+        self.micro_index = 0
+        self.step_count = 0           # optimizer steps taken (Adam t)
+        self.events: list[tuple[int, str, int | None]] = []   # (step, kind, unit)
+        self.trace: list[tuple[str, int]] = []                # (kind, unit) issue order
+        self.inject_inf: set[int] = set()                     # steps to poison (test hook)
+        self.found_inf = torch.zeros(1, dtype=torch.float32, device=self.device)
+        self.found_inf_world = torch.zeros(1, dtype=torch.float32, device=self.device)
+        self.opt_done: torch.cuda.Event | None = None
+        self.adam_steps = 0
+        self.fwd_visits: dict[int, int] = {}
+        self.bytes_ag = 0
+        self.bytes_rs = 0
+
+    # ------------------------------------------------------------ memory ---
+    def _alloc_arenas(self) -> None:
+        offs, cur = [], 0
+        for u in self.units:
+            offs.append(cur)
+            cur += -(-u.layout.shard_numel // _ALIGN) * _ALIGN
+        total = max(cur, _ALIGN)
+        f32 = dict(dtype=torch.float32, device=self.device)
+        self.master = torch.zeros(total, **f32)
+        self.grad = torch.zeros(total, **f32)
+        self.exp_avg = torch.zeros(total, **f32) if self.cfg.optimizer == "adam" else None
+        self.exp_avg_sq = torch.zeros(total, **f32) if self.cfg.optimizer == "adam" else None
+        self.low = torch.zeros(total, dtype=torch.bfloat16, device=self.device) if self.cfg.mixed else None
+        for u, o in zip(self.units, offs):
+            n = u.layout.shard_numel
+            u.master = self.master[o:o + n]
+            u.grad = self.grad[o:o + n]
+            if self.exp_avg is not None:
+                u.exp_avg = self.exp_avg[o:o + n]
+                u.exp_avg_sq = self.exp_avg_sq[o:o + n]
+            if self.low is not None:
+                u.low = self.low[o:o + n]
+
+    def _alloc_pool_regions(self) -> None:
+        W, F = self.plan.world_size, self.plan.shard_factor
+        psi_max = max((u.layout.psi for u in self.units), default=0)
+        n_max = max((u.layout.shard_numel for u in self.units), default=0)
+        self.psi_max = psi_max
+        nunits = len(self.units)
+        self.direct_views = F == 1          # views alias the local shard (no gather)
+        if self.cfg.num_slots is not None:
+            nslots = self.cfg.num_slots
+        elif self.cfg.reshard_after_forward == NRAF or self.cfg.rate_limit is None:
+            nslots = nunits
+        else:
+            nslots = min(nunits, self.cfg.rate_limit + 3)
+        es = 2 if self.compute_dtype == torch.bfloat16 else 4
+        ps = 2 if self.payload_dtype == torch.bfloat16 else 4
+        self.slots = None
+        self.rs_stage_off = self.ar_stage_off = self.ar_gather_off = None
+        if self.direct_views:
+            pass
+        elif self.cfg.comm_backend == "ipc":
+            c = self.comm
+            offs = [c.alloc(psi_max * es) for _ in range(nslots)]
+            views = [[c.view(o, psi_max, self.compute_dtype, e) for e in range(c.nranks_local)]
+                     for o in offs]
+            self.slots = SlotPool(views, offs, psi_max)
+        else:
+            bufs = [[torch.empty(psi_max, dtype=self.compute_dtype, device=self.device)]
+                    for _ in range(nslots)]
+            self.slots = SlotPool(bufs, [0] * nslots, psi_max)
+        if W > 1 and self.cfg.comm_backend == "ipc":
+            c = self.comm
+            if F > 1:
+                self.rs_stage_off = c.alloc(psi_max * ps)
+            if F < W:
+                n_ar = n_max if F > 1 else psi_max
+                gsz = W // F
+                el = c.ar_staging_elems(n_ar, gsz)
+                self.ar_stage_off = c.alloc(el * 4)
+                self.ar_gather_off = c.alloc(el * 4)
+
+    @staticmethod
+    def pool_bytes_for(layouts: Sequence[UnitLayout], plan: ShardingPlan, cfg: RuntimeConfig,
+                       reserved: int = 65536) -> int:
+        """Symmetric pool size `_alloc_pool_regions` will carve (plus slack)."""
+        W, F = plan.world_size, plan.shard_factor
+        psi_max = max((l.psi for l in layouts), default=0)
+        n_max = max((l.shard_numel for l in layouts), default=0)
+        es = 2 if cfg.mixed else 4
+        ps = 2 if (cfg.mixed and cfg.reduce_in_low) else 4
+        if cfg.num_slots is not None:
+            nslots = cfg.num_slots
+        elif cfg.reshard_after_forward == NRAF or cfg.rate_limit is None:
+            nslots = len(layouts)
+        else:
+            nslots = min(len(layouts), cfg.rate_limit + 3)
+        total = reserved
+        pad = lambda b: -(-b // 256) * 256 + 256  # noqa: E731
+        if F > 1:
+            total += nslots * pad(psi_max * es) + pad(psi_max * ps)
+        if W > 1 and F < W:
+            n_ar = n_max if F > 1 else psi_max
+            g = W // F
+            c = -(-(-(-n_ar // g)) // 8) * 8 * g
+            total += 2 * pad(c * 4)
+        return total + (1 << 20)
+
+    # ------------------------------------------------------- parameters ---
+    def load_unit_values(self, uid: int, tensors: Sequence[torch.Tensor]) -> None:
+        """Materialise a unit: flatten its original tensors (declaration order)
+        into an unsharded fp32 buffer, copy this rank's shard, refresh the bf16
+        copy (deferred_init.py:156-176 — flatten + shard)."""
+        u = self.units[uid]
+        lay = u.layout
+        srcs = [t.detach().to(self.device, torch.float32).contiguous() for t in tensors]
+        flat = torch.empty(lay.psi, dtype=torch.float32, device=self.device)
+        kernels.flatten(srcs, lay.offsets, flat)
+        kernels.shard_copy(flat, u.master, self.plan.shard_index(self.rank))
+        if u.low is not None:
+            kernels.cast(u.master, u.low)
+
+    def full_unit_values(self, uid: int) -> list[torch.Tensor]:
+        """This rank's view of the full unit (requires F == 1) — helper."""
+        u = self.units[uid]
+        outs = [torch.empty(o.shape, dtype=torch.float32, device=self.device) for o in u.layout.originals]
+        kernels.unflatten(u.master, outs, u.layout.offsets)
+        return outs
+
+    # --------------------------------------------------- materialisation ---
+    def _group_ag(self):
+        return self.plan.sharded_desc
+
+    def _issue_unshard(self, uid: int) -> None:
+        """Take a slot and gather the unit into it on the AG stream."""
+        u = self.units[uid]
+        lay = u.layout
+        slot, free_ev = self.slots.acquire(uid)
+        u.slot = slot
+        views = self.slots.views[slot]
+        u.unsharded = views[0][: lay.psi]
+        src = u.low if self.cfg.mixed else u.master
+        with torch.cuda.stream(self.ag_stream):
+            if free_ev is not None:
+                self.ag_stream.wait_event(free_ev)
+            if self.opt_done is not None:
+                self.ag_stream.wait_event(self.opt_done)
+            if self.cfg.comm_backend == "ipc":
+                self.comm.all_gather(self._group_ag(), [src], self.slots.offsets[slot],
+                                     self.compute_dtype, stream=self.ag_stream)
+            else:
+                import torch.distributed as dist
+                dist.all_gather_into_tensor(u.unsharded, src, group=self.pgs.get("shard"))
+            ev = torch.cuda.Event()
+            ev.record(self.ag_stream)
+        u.ag_event = ev
+        u.window = _Window(uid)
+        self.inflight.append(u.window)
+        self.trace.append(("AG_issue", uid))
+        self.bytes_ag += lay.psi * (2 if self.cfg.mixed else 4)
+
+    def limiter_acquire(self) -> None:
+        limit = self.cfg.rate_limit
+        if limit is None:
+            return
+        while self.inflight and self.inflight[0].done is not None and self.inflight[0].done.query():
+            self.inflight.pop(0)
+        while len(self.inflight) >= limit:
+            oldest = self.inflight[0]
+            if oldest.done is None:
+                break                       # unconsumed front: overshoot, never deadlock
+            oldest.done.synchronize()
+            self.inflight.pop(0)
+
+    def ensure_unsharded(self, uid: int) -> torch.Tensor:
+        """Make the unit's unsharded flat buffer readable by compute."""
+        u = self.units[uid]
+        if u.unsharded is not None and not u.pending:
+            u.uses += 1
+            return u.unsharded
+        if self.direct_views:
+            u.unsharded = u.low if self.cfg.mixed else u.master
+            u.uses = 1
+            return u.unsharded
+        if u.pending:
+            u.pending = False
+        else:
+            self.limiter_acquire()
+            self._issue_unshard(uid)
+        self.compute_stream.wait_event(u.ag_event)
+        u.uses = 1
+        return u.unsharded
+
+    def try_prefetch(self, uid: int) -> None:
+        u = self.units[uid]
+        if self.direct_views or u.unsharded is not None or u.pending:
+            return
+        if self.in_backward and u.bwd_done:
+            return
+        self.limiter_acquire()
+        limit = self.cfg.rate_limit
+        if limit is not None and len(self.inflight) >= limit:
+            return
+        self._issue_unshard(uid)
+        u.pending = True
+
+    def close_window(self, uid: int) -> None:
+        """The unit's first consuming compute has been issued: its completion
+        (an event on the compute stream) retires the limiter window."""
+        u = self.units[uid]
+        if u.window is not None:
+            ev = torch.cuda.Event()
+            ev.record(self.compute_stream)
+            u.window.done = ev
+            u.window = None
+
+    def release_use(self, uid: int, phase: str, outermost: int | None) -> None:
+        u = self.units[uid]
+        u.uses -= 1
+        if u.uses > 0:
+            return
+        if phase == "forward":
+            if self.cfg.reshard_after_forward == NRAF:
+                return
+            if self.cfg.keep_outermost_unsharded and uid == outermost:
+                return
+        self.reshard(uid)
+
+    def reshard(self, uid: int) -> None:
+        u = self.units[uid]
+        if u.unsharded is None:
+            return
+        if self.direct_views:
+            u.unsharded = None
+            u.uses = 0
+            return
+        ev = torch.cuda.Event()
+        ev.record(self.compute_stream)
+        self.slots.release(u.slot, ev)
+        u.slot = None
+        u.unsharded = None
+        u.uses = 0
+        u.ag_event = None
+
+    # ---------------------------------------------- saved-tensor hooks ---
+    def pack_hook(self, t: torch.Tensor):
+        if self.slots is None or not t.is_cuda:
+            return t
+        ptr = t.data_ptr()
+        for slot, views in enumerate(self.slots.views):
+            base = views[0]
+            b = base.data_ptr()
+            if b <= ptr < b + base.numel() * base.element_size():
+                uid = self.slots.owner.get(slot)
+                if uid is None:
+                    return t
+                off = t.storage_offset() - base.storage_offset()
+                return _SlotRef(uid, off, tuple(t.size()), tuple(t.stride()))
+        return t
+
+    def unpack_hook(self, x):
+        if isinstance(x, _SlotRef):
+            u = self.units[x.uid]
+            if u.unsharded is None:
+                raise EngineError(f"unit {x.uid}: saved parameter needed by backward but the unit "
+                                  f"is not unsharded (pre-backward hook missing?)")
+            base = u.unsharded
+            return base.as_strided(x.size, x.stride, base.storage_offset() + x.off)
+        return x
+
+    def saved_tensor_hooks(self):
+        return torch.autograd.graph.saved_tensors_hooks(self.pack_hook, self.unpack_hook)
+
+    # ----------------------------------------------------- step control ---
+    def begin_step(self) -> None:
+        for u in self.units:
+            u.reduces_this_step = 0
+        self.micro_index = 0
+
+    def begin_micro(self, final: bool) -> None:
+        self.final_micro = final
+        self.defer_reduce = self.cfg.accumulation == ACCUM_NO_COMM and not final
+        self.fwd_order = []
+        self.post_order = []
+        self.in_backward = False
+        self.fwd_visits = {}
+        for u in self.units:
+            u.bwd_done = False
+
+    def begin_forward_pass(self) -> None:
+        """A new forward pass of the same micro-batch (engine.py:469-471)."""
+        self.fwd_order = []
+
+    def record_forward(self, uid: int) -> int:
+        self.fwd_visits[uid] = self.fwd_visits.get(uid, 0) + 1
+        pos = len(self.fwd_order)
+        if uid in self.fwd_order:
+            raise EngineError(f"unit {uid} materialized twice in one forward")
+        prev = self.prev_fwd_order if self.cfg.forward_prefetch else None
+        if prev is not None and (pos >= len(prev) or prev[pos] != uid):
+            raise StaticOrderError(
+                f"forward prefetch assumes a static graph: step {self.step_count} visited unit "
+                f"{uid} at position {pos} where the previous iteration ran unit "
+                f"{prev[pos] if pos < len(prev) else None}")
+        self.fwd_order.append(uid)
+        return pos
+
+    def forward_prefetch_after(self, pos: int) -> None:
+        prev = self.prev_fwd_order if self.cfg.forward_prefetch else None
+        if prev is not None and pos + 1 < len(prev):
+            self.try_prefetch(prev[pos + 1])
+
+    def start_backward(self) -> None:
+        """Called once per micro-batch before its backward (engine.py:510-511):
+        backward order = reverse of the order units FINISHED forward (equals
+        the reference's reversed forward order for sequential units; puts a
+        nested root first)."""
+        if not self.in_backward:
+            self.in_backward = True
+            seen, order = set(), []
+            for uid in reversed(self.post_order):
+                if uid not in seen:
+                    seen.add(uid)
+                    order.append(uid)
+            self.bwd_order = order
+            self.bwd_pos = {u: i for i, u in enumerate(self.bwd_order)}
+            for u in self.units:
+                u.grad_pending = self.fwd_visits.get(u.uid, 0)
+
+    def pre_backward(self, uid: int) -> None:
+        self.ensure_unsharded(uid)
+        self.close_window(uid)
+        if self.cfg.backward_prefetch == PREFETCH_PRE:
+            pos = self.bwd_pos.get(uid)
+            if pos is not None and pos + 1 < len(self.bwd_order):
+                self.try_prefetch(self.bwd_order[pos + 1])
+
+    def post_backward(self, uid: int, grads: Sequence[torch.Tensor | None]) -> None:
+        """Gradient write-back (flatten) + finalisation + reduction."""
+        u = self.units[uid]
+        lay = u.layout
+        missing = [o.name for o, g in zip(lay.originals, grads) if g is None]
+        if missing and len(missing) < len(lay.originals):
+            warnings.warn(f"unit {uid}: no gradient for {missing}, zero-filled")
+        gdt = self.compute_dtype
+        first = u.flat_grad is None
+        if first:
+            u.flat_grad = torch.empty(lay.psi, dtype=gdt, device=self.device)
+        srcs = [None if g is None else g.detach().to(gdt).contiguous() for g in grads]
+        for o, g in zip(lay.originals, srcs):
+            if g is not None and tuple(g.shape) != o.shape:
+                raise EngineError(f"gradient shape {tuple(g.shape)} != parameter shape {o.shape} "
+                                  f"for '{o.name}'")
+        kernels.flatten(srcs, lay.offsets, u.flat_grad, accumulate=not first,
+                        stream=self.compute_stream)
+        u.grad_pending -= 1
+        if u.grad_pending <= 0:
+            self._finalize(uid)
+        self.release_use(uid, "backward", None)
+
+    def _finalize(self, uid: int) -> None:
+        u = self.units[uid]
+        u.bwd_done = True
+        self.events.append((self.step_count, "grad_finalized", uid))
+        if self.final_micro and uid == 0 and self.step_count in self.inject_inf:
+            u.flat_grad[0] = float("inf")            # engine.py:541-543 fault hook
+        if self.cfg.backward_prefetch == PREFETCH_POST:
+            pos = self.bwd_pos.get(uid)
+            if pos is not None and pos + 1 < len(self.bwd_order):
+                self.try_prefetch(self.bwd_order[pos + 1])
+        if self.defer_reduce or u.accum_unsharded is not None:
+            # no_comm accumulation: fold into the local fp32 unsharded
+            # accumulator, reduce once at the final micro-batch
+            self._accumulate_local(uid)
+            if not self.defer_reduce:
+                self._reduce_unit(uid, u.accum_unsharded)
+                u.accum_unsharded = None
+        else:
+            self._reduce_unit(uid, u.flat_grad)
+        u.flat_grad = None
+
+    def _accumulate_local(self, uid: int) -> None:
+        u = self.units[uid]
+        first = u.accum_unsharded is None
+        if first:
+            u.accum_unsharded = torch.empty(u.layout.psi, dtype=torch.float32, device=self.device)
+        kernels.flatten([u.flat_grad], [0], u.accum_unsharded, accumulate=not first,
+                        stream=self.compute_stream)
+
+    def _reduce_unit(self, uid: int, grad: torch.Tensor) -> None:
+        """engine.py:771-820 on the reduce-scatter stream."""
+        u = self.units[uid]
+        W, F = self.plan.world_size, self.plan.shard_factor
+        accumulate = u.reduces_this_step > 0
+        post = float(W) if self.cfg.loss_mean else 1.0
+        pre = self.cfg.gradient_predivide
+        if pre != 1.0:
+            post = post / pre
+        ready = torch.cuda.Event()
+        ready.record(self.compute_stream)
+        self.events.append((self.step_count, "reduce_issue", uid))
+        self.trace.append(("RS_issue", uid))
+        n = u.layout.shard_numel
+        with torch.cuda.stream(self.rs_stream):
+            self.rs_stream.wait_event(ready)
+            payload = grad
+            if grad.dtype != self.payload_dtype:
+                payload = torch.empty(grad.numel(), dtype=self.payload_dtype, device=self.device)
+                kernels.cast(grad, payload, stream=self.rs_stream)
+            grad.record_stream(self.rs_stream)
+            if W == 1:
+                # world of one: the "reduction" is the fp32 cast (+ accumulate)
+                kernels.flatten([payload], [0], u.grad, accumulate=accumulate, stream=self.rs_stream)
+            elif self.cfg.comm_backend == "nccl":
+                self._reduce_nccl(u, payload, accumulate, pre, post)
+            elif F == W:
+                self.comm.reduce_scatter(self.plan.sharded_desc, [payload], self.rs_stage_off,
+                                         [u.grad], prediv=pre, postdiv=post, accumulate=accumulate,
+                                         stream=self.rs_stream)
+            elif F == 1:
+                self.comm.all_reduce(self.plan.replicated_desc, [payload], self.ar_stage_off,
+                                     self.ar_gather_off, [u.grad], postdiv=post,
+                                     accumulate=accumulate, stream=self.rs_stream)
+            else:
+                tmp = torch.empty(n, dtype=torch.float32, device=self.device)
+                self.comm.reduce_scatter(self.plan.sharded_desc, [payload], self.rs_stage_off,
+                                         [tmp], prediv=pre, postdiv=1.0, accumulate=False,
+                                         stream=self.rs_stream)
+                self.events.append((self.step_count, "reduce_stage2", uid))
+                self.comm.all_reduce(self.plan.replicated_desc, [tmp], self.ar_stage_off,
+                                     self.ar_gather_off, [u.grad], postdiv=post,
+                                     accumulate=accumulate, stream=self.rs_stream)
+            payload.record_stream(self.rs_stream)
+        self.bytes_rs += grad.numel() * (2 if self.payload_dtype == torch.bfloat16 else 4)
+        u.reduces_this_step += 1
+
+    def _reduce_nccl(self, u: UnitState, payload, accumulate, pre, post) -> None:
+        import torch.distributed as dist
+        W, F = self.plan.world_size, self.plan.shard_factor
+        n = u.layout.shard_numel
+        x = payload if pre == 1.0 else payload / pre
+        if F > 1:
+            out = torch.empty(n, dtype=payload.dtype, device=self.device)
+            dist.reduce_scatter_tensor(out, x, group=self.pgs.get("shard"))
+        else:
+            out = x.clone()
+        if F < W:
+            dist.all_reduce(out, group=self.pgs.get("replicate"))
+        red = out.float() / post if post != 1.0 else out.float()
+        if accumulate:
+            u.grad.add_(red)
+        else:
+            u.grad.copy_(red)
+
+    def end_backward(self) -> None:
+        """End-of-backward callback: finalise units that got
+        no gradient at all (zero-filled, keeps every rank in lock-step),
+        reshard everything, and make compute wait for the reductions."""
+        for uid in self.bwd_order:
+            u = self.units[uid]
+            if not u.bwd_done and u.grad_pending > 0:
+                warnings.warn(f"unit {uid}: no gradient for any parameter, zero-filled")
+                if u.flat_grad is None:
+                    u.flat_grad = torch.empty(u.layout.psi, dtype=self.compute_dtype, device=self.device)
+                    kernels.flatten([None] * len(u.layout.originals), u.layout.offsets, u.flat_grad,
+                                    stream=self.compute_stream)
+                u.grad_pending = 0
+                self._finalize(uid)
+        for u in self.units:
+            if u.unsharded is not None:
+                if u.pending:          # unconsumed prefetch: drop it
+                    self.compute_stream.wait_event(u.ag_event)
+                    u.pending = False
+                self.reshard(u.uid)
+        self.compute_stream.wait_stream(self.rs_stream)
+        self.in_backward = False
+        self.prev_fwd_order = list(self.fwd_order)
+        self.micro_index += 1
+
+    # --------------------------------------------------------- optimizer ---
+    def optimizer_step(self, scale: float | None = None) -> None:
+        """engine.py:563-594: unscale + world verdict + optimizer on the arena.
+        The verdict stays on device (skip flag) — no host sync."""
+        skip = None
+        if scale is not None:
+            self.found_inf.zero_()
+            kernels.unscale_found_inf(self.grad, 1.0 / scale, self.found_inf)
+            if self.plan.world_size > 1:
+                if self.cfg.comm_backend == "ipc":
+                    self.comm.scalar_all_reduce([self.found_inf], [self.found_inf_world])
+                else:
+                    import torch.distributed as dist
+                    self.found_inf_world.copy_(self.found_inf)
+                    dist.all_reduce(self.found_inf_world)
+            else:
+                self.found_inf_world.copy_(self.found_inf)
+            skip = self.found_inf_world
+        self.step_count += 1
+        cfg = self.cfg
+        if cfg.optimizer == "adam":
+            kernels.adam_step(self.master, self.grad, self.exp_avg, self.exp_avg_sq, lr=cfg.lr,
+                              betas=cfg.betas, eps=cfg.eps, t=self._adam_t(skip), skip_flag=skip,
+                              p_lowp=self.low)
+        else:
+            kernels.sgd_step(self.master, self.grad, lr=cfg.lr, skip_flag=skip, p_lowp=self.low)
+        ev = torch.cuda.Event()
+        ev.record(self.compute_stream)
+        self.opt_done = ev
+        self.events.append((self.step_count - 1, "opt_step", None))
+
+    def _adam_t(self, skip) -> int:
+        # Adam's t counts TAKEN steps (numerics.py:276).  A skipped step is
+        # only known once the scaler reads the verdict (ShardedGradScaler.update
+        # calls undo_adam_t), which always happens before the next step.
+        self.adam_steps += 1
+        return self.adam_steps
+
+    def undo_adam_t(self) -> None:
+        self.adam_steps -= 1

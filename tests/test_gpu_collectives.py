@@ -1,0 +1,185 @@
+"""Cross-rank collectives on ONE GPU: an emulated communicator runs all W
+ranks' pools on cuda:0 and launches each collective as one cooperative
+kernel (blockIdx.y = rank) — the same flag protocol and address arithmetic
+as the multi-GPU path.  Checked bit-exactly against the reference's golden
+vectors (shardsim fabric, float32) and the oracle (bf16 payloads)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import shardsim_port as sp
+from oracle.bf16 import round_to_bf16
+
+pytestmark = pytest.mark.gpu
+
+
+def make_comm(w, mb=64):
+    from paper_2304_11277_b200.comm import DeviceComm
+    c = DeviceComm.create_emulated(w, mb << 20, max_ctas=8)
+    c.set_timeout_ms(5000)
+    return c
+
+
+def cu(a, dt=torch.float32):
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda", dt)
+
+
+@pytest.mark.parametrize("w", [1, 2, 3, 4, 8])
+def test_ag_rs_ar_match_reference_golden(golden, w):
+    arrays, _ = golden
+    inputs = [arrays[f"coll/in/w{w}/r{r}"] for r in range(w)]
+    n = inputs[0].size
+    c = make_comm(w)
+    try:
+        off = c.alloc(1 << 20)
+        c.all_gather((w, 1), [cu(x[: n // w]) for x in inputs], off, torch.float32)
+        for r in range(w):
+            got = c.view(off, n, torch.float32, r).cpu().numpy()
+            assert got.tobytes() == arrays[f"coll/ag/w{w}/out{r}"].tobytes()
+        outs = [torch.empty(n // w, device="cuda") for _ in range(w)]
+        c.reduce_scatter((w, 1), [cu(x) for x in inputs], off, outs)
+        for r in range(w):
+            assert outs[r].cpu().numpy().tobytes() == arrays[f"coll/rs/w{w}/out{r}"].tobytes()
+        off_b = c.alloc(1 << 20)
+        outs = [torch.empty(n, device="cuda") for _ in range(w)]
+        c.all_reduce((w, 1), [cu(x) for x in inputs], off, off_b, outs)
+        for r in range(w):
+            assert outs[r].cpu().numpy().tobytes() == arrays[f"coll/ar/w{w}/out{r}"].tobytes()
+        torch.cuda.synchronize()
+        assert c.device_error() == 0
+    finally:
+        c.close()
+
+
+@pytest.mark.parametrize("w,f", [(w, f) for w in range(2, 9) for f in range(1, w + 1) if w % f == 0])
+def test_hybrid_rs_then_ar_matches_golden(golden, w, f):
+    """Eq. (1): RS in the sharded group then AR in the replicated group."""
+    arrays, _ = golden
+    grads = [arrays[f"hyb/w{w}f{f}/in{r}"] for r in range(w)]
+    psi = grads[0].size
+    n = psi // f
+    c = make_comm(w)
+    try:
+        a, b = c.alloc(1 << 20), c.alloc(1 << 20)
+        if f == 1:
+            outs = [torch.empty(psi, device="cuda") for _ in range(w)]
+            c.all_reduce((w, 1), [cu(g) for g in grads], a, b, outs)
+        else:
+            part = [torch.empty(n, device="cuda") for _ in range(w)]
+            c.reduce_scatter((f, 1), [cu(g) for g in grads], a, part)
+            outs = part
+            if f < w:
+                outs = [torch.empty(n, device="cuda") for _ in range(w)]
+                c.all_reduce((w // f, f), part, a, b, outs)
+        for r in range(w):
+            assert outs[r].cpu().numpy().tobytes() == arrays[f"hyb/w{w}f{f}/out{r}"].tobytes(), (w, f, r)
+        torch.cuda.synchronize()
+        assert c.device_error() == 0
+    finally:
+        c.close()
+
+
+@pytest.mark.parametrize("w", [2, 4, 8])
+@pytest.mark.parametrize("n", [8, 1000, 65536 + 24, 300007])
+def test_allgather_cast_bf16_bit_exact(w, n):
+    rng = np.random.default_rng(n + w)
+    shards = [rng.standard_normal(n).astype(np.float32) for _ in range(w)]
+    c = make_comm(w)
+    try:
+        off = c.alloc(n * w * 2 + 256)
+        c.all_gather((w, 1), [cu(s) for s in shards], off, torch.bfloat16)
+        exp = sp.cast(sp.all_gather(shards), sp.BF16)    # gather-then-cast == cast-then-gather
+        for r in range(w):
+            assert np.array_equal(c.view(off, n * w, torch.bfloat16, r).float().cpu().numpy(), exp)
+        # bf16 -> bf16 (the runtime's path: shards pre-cast by the optimizer)
+        c.all_gather((w, 1), [cu(s, torch.bfloat16) for s in shards], off, torch.bfloat16)
+        for r in range(w):
+            assert np.array_equal(c.view(off, n * w, torch.bfloat16, r).float().cpu().numpy(), exp)
+    finally:
+        c.close()
+
+
+@pytest.mark.parametrize("w", [2, 4, 8])
+@pytest.mark.parametrize("n", [16, 4104, 262144])
+def test_reduce_scatter_bf16_fp32_accumulate_divide(w, n):
+    """bf16 payloads, fp32 ascending accumulation from +0, / W, += accum
+    (engine.py:789-820 with the build's fp32 accumulation)."""
+    rng = np.random.default_rng(w * 7 + n)
+    grads = [round_to_bf16(rng.standard_normal(n * w).astype(np.float32)) for _ in range(w)]
+    acc0 = [rng.standard_normal(n).astype(np.float32) for _ in range(w)]
+    c = make_comm(w)
+    try:
+        off = c.alloc(n * w * 2 + 256)
+        outs = [cu(a) for a in acc0]
+        c.reduce_scatter((w, 1), [cu(g, torch.bfloat16) for g in grads], off, outs,
+                         postdiv=float(w), accumulate=True)
+        exp = sp.reduce_unit(grads, sp.Plan(w, w), reduce_dtype=sp.BF16, full_dtype=np.float32,
+                             acc_dtype=np.float32, mean=True, accum=acc0)
+        for r in range(w):
+            assert outs[r].cpu().numpy().tobytes() == exp[r].tobytes()
+    finally:
+        c.close()
+
+
+@pytest.mark.parametrize("w,f", [(8, 4), (8, 2), (4, 2)])
+def test_hybrid_bf16_reduce_unit(w, f):
+    """Full hybrid reduction of bf16 grads incl. / W and accumulation."""
+    rng = np.random.default_rng(w * 10 + f)
+    psi = 8 * 1024 * f
+    grads = [round_to_bf16(rng.standard_normal(psi).astype(np.float32)) for _ in range(w)]
+    n = psi // f
+    acc0 = [rng.standard_normal(n).astype(np.float32) for _ in range(w)]
+    c = make_comm(w)
+    try:
+        a, b = c.alloc(psi * 4 + 4096), c.alloc(psi * 4 + 4096)
+        part = [torch.empty(n, device="cuda") for _ in range(w)]
+        c.reduce_scatter((f, 1), [cu(g, torch.bfloat16) for g in grads], a, part)
+        outs = [cu(x) for x in acc0]
+        c.all_reduce((w // f, f), part, a, b, outs, postdiv=float(w), accumulate=True)
+        exp = sp.reduce_unit(grads, sp.Plan(w, f), reduce_dtype=sp.BF16, full_dtype=np.float32,
+                             acc_dtype=np.float32, mean=True, accum=acc0)
+        for r in range(w):
+            assert outs[r].cpu().numpy().tobytes() == exp[r].tobytes()
+    finally:
+        c.close()
+
+
+def test_kth_call_pairs_and_scalar_allreduce():
+    w = 4
+    c = make_comm(w)
+    try:
+        off = c.alloc(4096)
+        for k in range(5):    # repeated calls on one channel: epochs pair k-th with k-th
+            c.all_gather((w, 1), [torch.full((4,), float(10 * k + r), device="cuda") for r in range(w)],
+                         off, torch.float32)
+            exp = np.repeat([10.0 * k + r for r in range(w)], 4)
+            for r in range(w):
+                assert np.array_equal(c.view(off, 16, torch.float32, r).cpu().numpy(), exp)
+        ins = [torch.tensor([float(r == 2)], device="cuda") for r in range(w)]
+        outs = [torch.zeros(1, device="cuda") for _ in range(w)]
+        c.scalar_all_reduce(ins, outs)
+        assert all(o.item() == 1.0 for o in outs)
+        torch.cuda.synchronize()
+        assert c.device_error() == 0
+    finally:
+        c.close()
+
+
+def test_fabric_entry_contract():
+    from paper_2304_11277_b200.comm import DeviceFabric
+    from paper_2304_11277_b200.plan import CollectiveError
+    c = make_comm(2)
+    try:
+        fab = DeviceFabric(c, 1 << 16)
+        with pytest.raises(CollectiveError):
+            fab.all_gather(3, (0, 1), [torch.zeros(2, device="cuda")] * 2)     # not a member
+        with pytest.raises(CollectiveError):
+            fab.all_gather(0, (0, 1), [torch.zeros(2, 2, device="cuda")] * 2)  # not flat
+        with pytest.raises(CollectiveError):
+            fab.reduce_scatter(0, (0, 1), [torch.zeros(3, device="cuda")] * 2)  # 3 % 2
+        with pytest.raises(CollectiveError):
+            fab.all_gather(0, (0, 1), [torch.zeros(2, device="cuda"), torch.zeros(3, device="cuda")])
+        out = fab.reduce_scatter(0, (0, 1), [cu([1., 2, 3, 4]), cu([10., 20, 30, 40])])
+        assert out[0].tolist() == [11, 22] and out[1].tolist() == [33, 44]
+    finally:
+        c.close()

@@ -1,0 +1,153 @@
+"""Parity of the copy / cast / optimizer kernels (through the C ABI) with the
+oracle and with the reference's own golden vectors.  Bit-exact."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import shardsim_port as sp
+from oracle.bf16 import round_to_bf16
+
+pytestmark = pytest.mark.gpu
+
+DT = {"f32": torch.float32, "bf16": torch.bfloat16}
+
+
+@pytest.fixture(scope="module")
+def K():
+    from paper_2304_11277_b200 import kernels
+    return kernels
+
+
+def to_np(t):
+    return t.float().cpu().numpy()
+
+
+@pytest.mark.parametrize("src,dst", [("f32", "f32"), ("f32", "bf16"), ("bf16", "bf16"), ("bf16", "f32")])
+@pytest.mark.parametrize("shapes,F", [
+    ([(2, 3), (2,), (3, 3)], 4),
+    ([(768, 256), (768,), (256, 256), (256,)], 2),
+    ([(7,), (13, 5), (1,), (33,)], 8),         # unaligned offsets -> scalar paths
+    ([(4096,)], 1),
+    ([(3,)], 7),
+])
+def test_flatten_matches_oracle(K, src, dst, shapes, F):
+    rng = np.random.default_rng(0)
+    names = [f"p{i}" for i in range(len(shapes))]
+    lay = sp.build_unit_layouts(list(zip(names, shapes)), [names], F)[0]
+    vals = {n: rng.standard_normal(s).astype(np.float32) for n, s in zip(names, shapes)}
+    if src == "bf16":
+        vals = {n: round_to_bf16(v) for n, v in vals.items()}
+    ts = [torch.from_numpy(vals[n]).to("cuda", DT[src]) for n in names]
+    flat = torch.full((lay.psi,), 7.0, dtype=DT[dst], device="cuda")
+    K.flatten(ts, [o.offset for o in lay.originals], flat)
+    exp = sp.flatten(vals, lay, sp.BF16 if dst == "bf16" else np.float32)
+    assert to_np(flat).tobytes() == exp.astype(np.float32).tobytes()
+    # accumulate: flat += values (fp32 add, rounded to dst)
+    K.flatten(ts, [o.offset for o in lay.originals], flat, accumulate=True)
+    exp2 = exp.astype(np.float32) + exp.astype(np.float32)
+    exp2 = sp.cast(exp2, sp.BF16 if dst == "bf16" else np.float32)
+    assert np.array_equal(to_np(flat), exp2)
+    # unflatten round trip + shard copy
+    outs = [torch.empty(s, dtype=DT[src], device="cuda") for s in shapes]
+    K.flatten(ts, [o.offset for o in lay.originals], flat)
+    K.unflatten(flat, outs, [o.offset for o in lay.originals])
+    for o, n in zip(outs, names):
+        exp_o = sp.cast(sp.cast(vals[n], sp.BF16 if dst == "bf16" else np.float32),
+                        sp.BF16 if src == "bf16" else np.float32)
+        assert np.array_equal(to_np(o), exp_o)
+    for k in range(F):
+        sh = torch.empty(lay.shard_numel, dtype=DT[dst], device="cuda")
+        K.shard_copy(flat, sh, k)
+        assert to_np(sh).tobytes() == sp.shard(exp.astype(np.float32), lay, k).tobytes()
+
+
+def test_flatten_missing_grads_zero_filled(K):
+    lay = sp.build_unit_layouts([("a", (5,)), ("b", (9,))], [["a", "b"]], 4)[0]
+    flat = torch.full((lay.psi,), 3.0, device="cuda")
+    K.flatten([None, torch.ones(9, device="cuda")], [0, 5], flat)
+    exp, warns = sp.writeback_grad(lay, {"b": np.ones(9, np.float32)}, np.float32)
+    assert np.array_equal(to_np(flat), exp) and len(warns) == 1
+
+
+def test_flatten_large_vector_path(K):
+    n = (1 << 22) + 24
+    a = torch.randn(n, device="cuda")
+    b = torch.randn(1000, device="cuda")
+    flat = torch.empty(n + 1000 + 8, dtype=torch.bfloat16, device="cuda")
+    K.flatten([a, b], [0, n], flat)
+    exp = torch.cat([a, b, torch.zeros(8, device="cuda")]).to(torch.bfloat16)
+    assert torch.equal(flat, exp)
+
+
+def test_cast_bits_match_torch_rne(K):
+    x = torch.randn(1 << 20, device="cuda") * 1e3
+    x[:6] = torch.tensor([0.0, -0.0, float("inf"), -float("inf"), 1e-40, 3.3e38])
+    y = torch.empty_like(x, dtype=torch.bfloat16)
+    K.cast(x, y)
+    assert torch.equal(y.view(torch.int16), x.to(torch.bfloat16).view(torch.int16))
+    # odd length, unaligned start
+    y2 = torch.empty(999, dtype=torch.bfloat16, device="cuda")
+    K.cast(x[1:1000], y2)
+    assert torch.equal(y2, x[1:1000].to(torch.bfloat16))
+
+
+@pytest.mark.parametrize("lr", [1e-3, 0.01])
+def test_adam_bit_exact_vs_reference_golden(K, golden, lr):
+    arrays, _ = golden
+    p = torch.from_numpy(arrays[f"adam/lr{lr}/p0"].copy()).cuda()
+    m = torch.zeros_like(p)
+    v = torch.zeros_like(p)
+    for t in range(4):
+        g = torch.from_numpy(arrays[f"adam/lr{lr}/g{t}"]).cuda()
+        K.adam_step(p, g, m, v, lr=lr, betas=(0.9, 0.999), eps=1e-8, t=t + 1)
+        assert p.cpu().numpy().tobytes() == arrays[f"adam/lr{lr}/p{t + 1}"].tobytes()
+        assert m.cpu().numpy().tobytes() == arrays[f"adam/lr{lr}/m{t + 1}"].tobytes()
+        assert v.cpu().numpy().tobytes() == arrays[f"adam/lr{lr}/v{t + 1}"].tobytes()
+
+
+def test_adam_large_with_lowp_and_skip(K):
+    n = (1 << 20) + 3
+    rng = np.random.default_rng(1)
+    p0 = rng.standard_normal(n).astype(np.float32)
+    g0 = (rng.standard_normal(n) * 1e-2).astype(np.float32)
+    p = torch.from_numpy(p0).cuda()
+    g = torch.from_numpy(g0).cuda()
+    m, v = torch.zeros_like(p), torch.zeros_like(p)
+    low = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+    K.adam_step(p, g, m, v, lr=3e-4, betas=(0.9, 0.95), eps=1e-8, t=1, p_lowp=low)
+    pe = p0.copy()
+    st = sp.adam_init(n, np.float32)
+    sp.adam_step(pe, g0, st, lr=3e-4, betas=(0.9, 0.95), eps=1e-8)
+    assert p.cpu().numpy().tobytes() == pe.tobytes()
+    assert torch.equal(low, p.to(torch.bfloat16))
+    skip = torch.ones(1, device="cuda")
+    before = p.clone()
+    K.adam_step(p, g, m, v, lr=3e-4, betas=(0.9, 0.95), eps=1e-8, t=2, skip_flag=skip)
+    assert torch.equal(p, before)
+
+
+def test_sgd_golden(K, golden):
+    arrays, _ = golden
+    p = torch.from_numpy(arrays["sgd/p0"].copy()).cuda()
+    K.sgd_step(p, torch.from_numpy(arrays["sgd/g"]).cuda(), lr=0.03125)
+    assert p.cpu().numpy().tobytes() == arrays["sgd/p1"].tobytes()
+
+
+def test_unscale_found_inf(K):
+    g = torch.randn(100003, device="cuda")
+    ref = g.cpu().numpy().copy()
+    flag = torch.zeros(1, device="cuda")
+    K.unscale_found_inf(g, 1.0 / 65536.0, flag)
+    assert flag.item() == 0.0
+    assert not sp.unscale_and_check([ref], 65536.0)
+    assert g.cpu().numpy().tobytes() == ref.tobytes()
+    g[777] = float("nan")
+    K.unscale_found_inf(g, 0.5, flag)
+    assert flag.item() == 1.0
+
+
+def test_launch_counter_advances(K):
+    from paper_2304_11277_b200 import _lib
+    n0 = _lib.launch_count()
+    K.cast(torch.ones(10, device="cuda"), torch.empty(10, device="cuda"))
+    assert _lib.launch_count() == n0 + 1

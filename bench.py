@@ -1,0 +1,401 @@
+#!/usr/bin/env python
+"""FSDP sharded-training step benchmark on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config gpt1.3b]
+                    [--micro 8] [--backend ipc|nccl] [--impl ours|reference]
+                    [--mode step|sweep]
+
+A "step" = one FSDP training step (forward, backward with reduce-scatter,
+sharded Adam) of the GPT-style model on one synthetic micro-batch per GPU.
+N=1 runs the GPT-1.3B config (BASELINE configs[1] fits one B200); N>1 runs the
+same per-GPU work FULL_SHARD over N GPUs ("weak" scaling).  `value` is the
+whole-job model TFLOP/s (sum over GPUs; TFLOPS/GPU = value / n_gpus) with the
+token batch resident in HBM; `e2e` is the same through the public API with
+the token ids copied from pinned host memory and the loss read back every
+step.  Timing: CUDA events on the compute stream, barrier + synchronize on
+both sides, max over ranks; inputs (weights + optimizer state, >20 GB) are
+far larger than the 126 MB L2.
+
+--impl reference times the reference algorithm (oracle port of shardsim,
+numpy + torch CPU) on this box's host cores on a bounded sample.
+--mode sweep measures the flat-parameter all-gather / reduce-scatter bus
+bandwidth 1 MB..2 GB against NCCL (BASELINE configs[4]).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "TFLOPS/GPU and step time at 1/2/4/8 B200; AG/RS bus GB/s vs 900 GB/s NVLink"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="gpt1.3b")
+    ap.add_argument("--micro", type=int, default=8, help="sequences per GPU per step")
+    ap.add_argument("--backend", default="ipc", choices=["ipc", "nccl"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="step", choices=["step", "sweep"])
+    ap.add_argument("--strategy", default="FULL_SHARD")
+    ap.add_argument("--hybrid-shard-size", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-tokens", type=int, default=2048)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def init_dist(world, local):
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        loaded = [s for s in sm if s > 500] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return p["hbm_gbs"], p["bf16_tflops_sustained"], "measured"
+    except Exception:
+        return 6650.0, 1400.0, "fallback"
+
+
+# --------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    init_dist(world, local)
+    from paper_2304_11277_b200 import _lib
+    from paper_2304_11277_b200.fsdp import (BackwardPrefetch, FullyShardedDataParallel,
+                                            MixedPrecision, ModuleWrapPolicy, ShardingStrategy)
+    from paper_2304_11277_b200.workloads import CONFIGS, GPT, Block, param_init_fn
+
+    torch.backends.cuda.matmul.allow_tf32 = True
+    cfg = CONFIGS[args.config]
+    dev = torch.device("cuda", local)
+    torch.manual_seed(1234)
+    with torch.device("meta"):
+        model = GPT(cfg)
+    strategy = ShardingStrategy[args.strategy]
+    fsdp = FullyShardedDataParallel(
+        model, sharding_strategy=strategy, auto_wrap_policy=ModuleWrapPolicy({Block}),
+        backward_prefetch=BackwardPrefetch.BACKWARD_PRE,
+        mixed_precision=MixedPrecision(param_dtype=torch.bfloat16, reduce_dtype=torch.bfloat16),
+        limit_all_gathers=True, param_init_fn=param_init_fn, comm_backend=args.backend,
+        hybrid_shard_size=args.hybrid_shard_size, lr=1e-4)
+    opt = fsdp.optimizer()
+    rt = fsdp.rt
+    B = args.micro
+    g = torch.Generator(device="cpu").manual_seed(1 + rank)
+    x_host = torch.randint(0, cfg.vocab, (B, cfg.seq), generator=g).pin_memory()
+    y_host = torch.randint(0, cfg.vocab, (B, cfg.seq), generator=g).pin_memory()
+    x, y = x_host.to(dev), y_host.to(dev)
+    compute = torch.cuda.current_stream()
+
+    def step(xx, yy):
+        loss = fsdp(xx, yy)
+        loss.backward()
+        opt.step()
+        return loss
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step(x, y)
+    barrier()
+    sampler = ClockSampler(local)
+    if rank == 0:
+        sampler.start()
+    rt.profile = True
+    rt.reset_timers()
+    n_launch0 = _lib.launch_count()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    t0.record(compute)
+    for _ in range(args.steps):
+        loss = step(x, y)
+    t1.record(compute)
+    barrier()
+    launches = _lib.launch_count() - n_launch0
+    ms = t0.elapsed_time(t1) / args.steps
+    timers = rt.timer_summary()
+    rt.profile = False
+    # e2e: token ids from pinned host memory each step, loss read back each step
+    e0 = time.perf_counter()
+    barrier()
+    te0, te1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    te0.record(compute)
+    losses = []
+    for _ in range(args.steps):
+        xx = x_host.to(dev, non_blocking=True)
+        yy = y_host.to(dev, non_blocking=True)
+        l = step(xx, yy)
+        losses.append(l.item())
+    te1.record(compute)
+    barrier()
+    ms_e2e = te0.elapsed_time(te1) / args.steps
+    clocks = sampler.stop() if rank == 0 else None
+    tmax = torch.tensor([ms, ms_e2e], device=dev)
+    if world > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    ms, ms_e2e = tmax.tolist()
+    tokens = B * cfg.seq
+    flops_step = cfg.flops_per_token() * tokens          # per GPU
+    tflops_gpu = flops_step / (ms * 1e-3) / 1e12
+    value = tflops_gpu * world
+    e2e_value = flops_step / (ms_e2e * 1e-3) / 1e12 * world
+    hbm_peak, bf16_peak, peak_kind = load_peaks()
+    # roofline: the dominant kernel of this library within the step
+    mine = {k: v for k, v in timers.items()}
+    dom = max(mine, key=lambda k: mine[k]["total_ms"]) if mine else None
+    roof = None
+    if dom is not None:
+        d = mine[dom]
+        per_launch_bytes = d["bytes_total"] / max(1, d["count"])
+        achieved = per_launch_bytes / (d["mean_ms"] * 1e-3) / 1e9
+        if dom in ("allgather", "reduce_scatter"):
+            # NVLink-bound: bus bytes = S*(W-1)/W per rank (nccl-tests convention)
+            bus = per_launch_bytes * (rt.plan.shard_factor - 1) / rt.plan.shard_factor
+            achieved = bus / (d["mean_ms"] * 1e-3) / 1e9
+            roof = {"kernel": dom, "bound": "nvlink", "achieved": round(achieved, 1),
+                    "peak": 900.0, "unit": "GB/s", "frac": round(achieved / 900.0, 4),
+                    "traffic": None, "peak_kind": "nominal NVLink5 per direction"}
+        else:
+            roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1),
+                    "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
+                    "traffic": None, "peak_kind": peak_kind,
+                    "algorithmic_bytes_per_launch": int(per_launch_bytes),
+                    "mean_ms": round(d["mean_ms"], 4)}
+    step_roof = {"bound": "tensor", "achieved": round(tflops_gpu, 1), "peak": bf16_peak,
+                 "unit": "TFLOP/s", "frac": round(tflops_gpu / bf16_peak, 4)}
+    kern_share = {k: {"share_of_step": round(v["total_ms"] / (ms * args.steps), 4),
+                      "mean_ms": round(v["mean_ms"], 4), "count": v["count"]}
+                  for k, v in mine.items()}
+    comm_bw = {}
+    for k in ("allgather", "reduce_scatter"):
+        if k in mine and world > 1:
+            d = mine[k]
+            F = rt.plan.shard_factor
+            comm_bw[k + "_busbw_gbs"] = round(d["bytes_total"] / max(1, d["count"]) * (F - 1) / F
+                                              / (d["mean_ms"] * 1e-3) / 1e9, 1)
+    out = None
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": round(value, 2), "unit": "TFLOP/s (model, whole job)",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform token ids, meta-init weights)",
+            "config": {"workload": f"{cfg.name} {args.strategy} bf16 MixedPrecision, block auto-wrap, "
+                                   f"BACKWARD_PRE, limit_all_gathers",
+                       "model": cfg.name, "global_batch": B * world, "seq_len": cfg.seq,
+                       "parallelism": f"fsdp{world}" if world > 1 else "fsdp1 (NO_SHARD-equivalent)",
+                       "comm_backend": args.backend, "l2": "inputs > L2 (weights+state >20 GB)"},
+            "tflops_per_gpu": round(tflops_gpu, 2),
+            "roofline": roof, "roofline_step": step_roof, "kernels": kern_share,
+            "e2e": {"value": round(e2e_value, 2), "unit": "TFLOP/s (model, whole job)",
+                    "h2d_bytes_per_step": int(x_host.numel() * 8 * 2),
+                    "d2h_bytes_per_step": 4, "ms_per_step": round(ms_e2e, 3)},
+            "gpu_launches": int(launches), "clocks": clocks, "loss": round(losses[-1], 4),
+            "peak_mem_gb": round(torch.cuda.max_memory_allocated() / 1e9, 2),
+        }
+        out.update(comm_bw)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(cfg, args.cpu_tokens, world=1)
+    if world > 1:
+        dist.barrier()
+    return out
+
+
+def cpu_baseline(cfg, tokens: int, world: int = 1, steps: int = 1, warmup: int = 0) -> dict:
+    """The reference algorithm (oracle port) on this box's host cores, one
+    bounded sample: `tokens` tokens per simulated rank through the full step."""
+    import torch
+    from oracle.cpu_fsdp import time_cpu_steps
+    from paper_2304_11277_b200.workloads import GPT, Block, init_gpt_
+    model = init_gpt_(GPT(cfg), seed=0)
+    seqs = max(1, tokens // cfg.seq)
+    seq = min(cfg.seq, tokens)
+    g = torch.Generator().manual_seed(0)
+
+    def batches(i):
+        return [(torch.randint(0, cfg.vocab, (seqs, seq), generator=g),
+                 torch.randint(0, cfg.vocab, (seqs, seq), generator=g)) for _ in range(world)]
+
+    r = time_cpu_steps(model, Block, batches, steps=steps, warmup=warmup, world=world)
+    flops = cfg.flops_per_token() * seqs * seq * world
+    val = flops / r["sec_per_step"] / 1e12
+    return {"value": round(val, 4), "unit": "TFLOP/s (model, whole job)", "cores": r["threads"],
+            "kind": "port", "sec_per_step": round(r["sec_per_step"], 2),
+            "sample": f"{world} simulated rank(s) x {seqs}x{seq} tokens of {cfg.name}, full step "
+                      f"(fwd/bwd torch CPU fp32 + shardsim flatten/reduce/Adam numpy on all "
+                      f"{cfg.n_params/1e9:.2f}B params); cpu_count={os.cpu_count()}"}
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return None
+    from paper_2304_11277_b200.workloads import CONFIGS
+    cfg = CONFIGS[args.config]
+    # bounded: each step is one sample (steps/warmup capped so the arm ends in minutes)
+    steps, warmup = min(args.steps, 2), min(args.warmup, 0)
+    cb = cpu_baseline(cfg, args.cpu_tokens, world=world, steps=steps, warmup=warmup)
+    return {"metric": METRIC, "value": cb["value"], "unit": cb["unit"], "n_gpus": world,
+            "steps": steps, "warmup": warmup, "ms_per_step": cb["sec_per_step"] * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"{cfg.name} FULL_SHARD W={world} (shardsim algorithm, CPU)",
+                       "model": cfg.name, "seq_len": cfg.seq},
+            "cpu_baseline": {"value": cb["value"], "unit": cb["unit"], "kind": "port",
+                             "cores": cb["cores"], "sample": cb["sample"]},
+            "e2e": {"value": cb["value"], "unit": cb["unit"], "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def run_sweep(args):
+    import torch
+    import torch.distributed as dist
+    rank, world, local = dist_env()
+    init_dist(world, local)
+    from paper_2304_11277_b200.comm import DeviceComm
+    if world < 2:
+        return {"metric": "AG/RS bus GB/s", "value": None, "note": "sweep needs >= 2 GPUs"} if rank == 0 else None
+    sizes_mb = [1, 4, 16, 64, 256, 1024, 2048]
+    max_bytes = sizes_mb[-1] << 20
+    comm = DeviceComm.create(2 * max_bytes + (64 << 20), max_ctas=32)
+    stage = comm.alloc(max_bytes)
+    dst = comm.alloc(max_bytes)
+    dev = torch.device("cuda", local)
+    res = []
+    for mb in sizes_mb:
+        S = mb << 20                            # unsharded bf16 bytes
+        n = S // 2 // world
+        shard = torch.randn(n, device=dev).to(torch.bfloat16)
+        flat = torch.randn(n * world, device=dev).to(torch.bfloat16)
+        out = torch.empty(n, device=dev)
+        full = torch.empty(n * world, dtype=torch.bfloat16, device=dev)
+        out_bf = torch.empty(n, dtype=torch.bfloat16, device=dev)
+
+        def timeit(fn, iters=20, warm=5):
+            for _ in range(warm):
+                fn()
+            torch.cuda.synchronize()
+            dist.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(iters):
+                fn()
+            b.record()
+            torch.cuda.synchronize()
+            t = torch.tensor([a.elapsed_time(b) / iters], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return t.item()
+
+        bus = S * (world - 1) / world
+        r = {"size_mb": mb}
+        r["ag_ours_gbs"] = bus / (timeit(lambda: comm.all_gather((world, 1), [shard], dst, torch.bfloat16)) * 1e-3) / 1e9
+        r["rs_ours_gbs"] = bus / (timeit(lambda: comm.reduce_scatter((world, 1), [flat], stage, [out], postdiv=float(world))) * 1e-3) / 1e9
+        r["ag_nccl_gbs"] = bus / (timeit(lambda: dist.all_gather_into_tensor(full, shard)) * 1e-3) / 1e9
+        r["rs_nccl_gbs"] = bus / (timeit(lambda: dist.reduce_scatter_tensor(out_bf, flat)) * 1e-3) / 1e9
+        res.append({k: (round(v, 1) if isinstance(v, float) else v) for k, v in r.items()})
+    comm.close()
+    if rank == 0:
+        best = max(res, key=lambda r: r["ag_ours_gbs"])
+        return {"metric": "AG/RS bus GB/s vs 900 GB/s NVLink", "value": best["ag_ours_gbs"],
+                "unit": "GB/s (AG busbw, best size)", "n_gpus": world, "sweep": res,
+                "higher_is_better": True}
+    return None
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        out = run_reference(args)
+    elif args.mode == "sweep":
+        out = run_sweep(args)
+    else:
+        out = run_ours(args)
+    if out is not None:
+        print(json.dumps(out), flush=True)
+    try:
+        import torch.distributed as dist
+        if dist.is_initialized():
+            dist.destroy_process_group()
+    except Exception:
+        pass
+
+
+if __name__ == "__main__":
+    main()

@@ -370,6 +370,15 @@ class FullyShardedDataParallel(nn.Module):
         self.rt.optimizer_step(scale)
         self.rt.begin_step()
 
+    def close(self) -> None:
+        """Release the communicator's pool and IPC mappings."""
+        for h in self._handles:
+            h.remove()
+        self._handles = []
+        if self.comm is not None:
+            self.comm.close()
+            self.comm = None
+
     def flat_shards(self) -> list[torch.Tensor]:
         return [u.master for u in self.rt.units]
 

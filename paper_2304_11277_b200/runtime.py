@@ -35,6 +35,7 @@ unit re-gathered for backward may land in a different slot.
 """
 from __future__ import annotations
 
+import contextlib
 import math
 import warnings
 from dataclasses import dataclass, field
@@ -214,6 +215,8 @@ class FSDPRuntime:
         self.fwd_visits: dict[int, int] = {}
         self.bytes_ag = 0
         self.bytes_rs = 0
+        self.profile = False          # record CUDA events around every launch
+        self.timers: dict[str, list] = {}
 
     # ------------------------------------------------------------ memory ---
     def _alloc_arenas(self) -> None:
@@ -325,6 +328,33 @@ class FSDPRuntime:
         kernels.unflatten(u.master, outs, u.layout.offsets)
         return outs
 
+    # ------------------------------------------------------ kernel timing ---
+    @contextlib.contextmanager
+    def timed(self, name: str, stream: torch.cuda.Stream, nbytes: int = 0):
+        """CUDA events on the launching stream around one kernel launch."""
+        if not self.profile:
+            yield
+            return
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        yield
+        b.record(stream)
+        self.timers.setdefault(name, []).append((a, b, nbytes))
+
+    def timer_summary(self) -> dict:
+        """{name: {count, mean_ms, total_ms, bytes_per_launch}} (synchronises)."""
+        torch.cuda.synchronize(self.device)
+        out = {}
+        for k, v in self.timers.items():
+            ms = [a.elapsed_time(b) for a, b, _ in v]
+            nb = [x for _, _, x in v]
+            out[k] = {"count": len(ms), "total_ms": sum(ms), "mean_ms": sum(ms) / max(1, len(ms)),
+                      "bytes_total": sum(nb)}
+        return out
+
+    def reset_timers(self) -> None:
+        self.timers = {}
+
     # --------------------------------------------------- materialisation ---
     def _group_ag(self):
         return self.plan.sharded_desc
@@ -344,8 +374,10 @@ class FSDPRuntime:
             if self.opt_done is not None:
                 self.ag_stream.wait_event(self.opt_done)
             if self.cfg.comm_backend == "ipc":
-                self.comm.all_gather(self._group_ag(), [src], self.slots.offsets[slot],
-                                     self.compute_dtype, stream=self.ag_stream)
+                with self.timed("allgather", self.ag_stream,
+                                lay.psi * (2 if self.cfg.mixed else 4)):
+                    self.comm.all_gather(self._group_ag(), [src], self.slots.offsets[slot],
+                                         self.compute_dtype, stream=self.ag_stream)
             else:
                 import torch.distributed as dist
                 dist.all_gather_into_tensor(u.unsharded, src, group=self.pgs.get("shard"))
@@ -542,21 +574,40 @@ class FSDPRuntime:
             warnings.warn(f"unit {uid}: no gradient for {missing}, zero-filled")
         gdt = self.compute_dtype
         first = u.flat_grad is None
-        if first:
-            u.flat_grad = torch.empty(lay.psi, dtype=gdt, device=self.device)
         srcs = [None if g is None else g.detach().to(gdt).contiguous() for g in grads]
         for o, g in zip(lay.originals, srcs):
             if g is not None and tuple(g.shape) != o.shape:
                 raise EngineError(f"gradient shape {tuple(g.shape)} != parameter shape {o.shape} "
                                   f"for '{o.name}'")
-        kernels.flatten(srcs, lay.offsets, u.flat_grad, accumulate=not first,
-                        stream=self.compute_stream)
+        injected = self.final_micro and uid == 0 and self.step_count in self.inject_inf
+        if (self.plan.world_size == 1 and first and u.grad_pending == 1 and not self.defer_reduce
+                and u.accum_unsharded is None and not injected
+                and self.cfg.gradient_predivide == 1.0):
+            # world of one: the write-back and the (identity) reduction fuse into
+            # one flatten straight into the fp32 grad shard, accumulating over
+            # micro-batches (engine.py:527-535 + :817-820 with W = 1)
+            with self.timed("flatten_grad", self.compute_stream,
+                            sum(g.numel() for g in srcs if g is not None) * (gdt.itemsize + 4)):
+                kernels.flatten(srcs, lay.offsets, u.grad, accumulate=u.reduces_this_step > 0,
+                                stream=self.compute_stream)
+            u.reduces_this_step += 1
+            u.grad_pending -= 1
+            self._finalize(uid, reduced=True)
+            self.events.append((self.step_count, "reduce_issue", uid))
+            self.release_use(uid, "backward", None)
+            return
+        if first:
+            u.flat_grad = torch.empty(lay.psi, dtype=gdt, device=self.device)
+        with self.timed("flatten_grad", self.compute_stream,
+                        sum(g.numel() for g in srcs if g is not None) * 2 * u.flat_grad.element_size()):
+            kernels.flatten(srcs, lay.offsets, u.flat_grad, accumulate=not first,
+                            stream=self.compute_stream)
         u.grad_pending -= 1
         if u.grad_pending <= 0:
             self._finalize(uid)
         self.release_use(uid, "backward", None)
 
-    def _finalize(self, uid: int) -> None:
+    def _finalize(self, uid: int, reduced: bool = False) -> None:
         u = self.units[uid]
         u.bwd_done = True
         self.events.append((self.step_count, "grad_finalized", uid))
@@ -566,6 +617,8 @@ class FSDPRuntime:
             pos = self.bwd_pos.get(uid)
             if pos is not None and pos + 1 < len(self.bwd_order):
                 self.try_prefetch(self.bwd_order[pos + 1])
+        if reduced:
+            return
         if self.defer_reduce or u.accum_unsharded is not None:
             # no_comm accumulation: fold into the local fp32 unsharded
             # accumulator, reduce once at the final micro-batch
@@ -608,13 +661,16 @@ class FSDPRuntime:
             grad.record_stream(self.rs_stream)
             if W == 1:
                 # world of one: the "reduction" is the fp32 cast (+ accumulate)
-                kernels.flatten([payload], [0], u.grad, accumulate=accumulate, stream=self.rs_stream)
+                with self.timed("reduce_w1", self.rs_stream, n * (payload.element_size() + 4)):
+                    kernels.flatten([payload], [0], u.grad, accumulate=accumulate,
+                                    stream=self.rs_stream)
             elif self.cfg.comm_backend == "nccl":
                 self._reduce_nccl(u, payload, accumulate, pre, post)
             elif F == W:
-                self.comm.reduce_scatter(self.plan.sharded_desc, [payload], self.rs_stage_off,
-                                         [u.grad], prediv=pre, postdiv=post, accumulate=accumulate,
-                                         stream=self.rs_stream)
+                with self.timed("reduce_scatter", self.rs_stream, payload.numel() * payload.element_size()):
+                    self.comm.reduce_scatter(self.plan.sharded_desc, [payload], self.rs_stage_off,
+                                             [u.grad], prediv=pre, postdiv=post,
+                                             accumulate=accumulate, stream=self.rs_stream)
             elif F == 1:
                 self.comm.all_reduce(self.plan.replicated_desc, [payload], self.ar_stage_off,
                                      self.ar_gather_off, [u.grad], postdiv=post,
@@ -695,16 +751,26 @@ class FSDPRuntime:
             skip = self.found_inf_world
         self.step_count += 1
         cfg = self.cfg
+        n = self.master.numel()
+        if cfg.optimizer == "adam":
+            nb = n * (28 + (2 if self.low is not None else 0))
+        else:
+            nb = n * (12 + (2 if self.low is not None else 0))
+        with self.timed(cfg.optimizer + "_step", self.compute_stream, nb):
+            self._opt_launch(skip)
+        ev = torch.cuda.Event()
+        ev.record(self.compute_stream)
+        self.opt_done = ev
+        self.events.append((self.step_count - 1, "opt_step", None))
+
+    def _opt_launch(self, skip) -> None:
+        cfg = self.cfg
         if cfg.optimizer == "adam":
             kernels.adam_step(self.master, self.grad, self.exp_avg, self.exp_avg_sq, lr=cfg.lr,
                               betas=cfg.betas, eps=cfg.eps, t=self._adam_t(skip), skip_flag=skip,
                               p_lowp=self.low)
         else:
             kernels.sgd_step(self.master, self.grad, lr=cfg.lr, skip_flag=skip, p_lowp=self.low)
-        ev = torch.cuda.Event()
-        ev.record(self.compute_stream)
-        self.opt_done = ev
-        self.events.append((self.step_count - 1, "opt_step", None))
 
     def _adam_t(self, skip) -> int:
         # Adam's t counts TAKEN steps (numerics.py:276).  A skipped step is

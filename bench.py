@@ -334,9 +334,9 @@ def run_sweep(args):
         return {"metric": "AG/RS bus GB/s", "value": None, "note": "sweep needs >= 2 GPUs"} if rank == 0 else None
     sizes_mb = [1, 4, 16, 64, 256, 1024, 2048]
     max_bytes = sizes_mb[-1] << 20
-    comm = DeviceComm.create(2 * max_bytes + (64 << 20), max_ctas=32)
-    stage = comm.alloc(max_bytes)
-    dst = comm.alloc(max_bytes)
+    cta_opts = [int(c) for c in os.environ.get("FSDP_SWEEP_CTAS", "16,32,64").split(",")]
+    comms = {c: DeviceComm.create(2 * max_bytes + (64 << 20), max_ctas=c) for c in cta_opts}
+    offs = {c: (cm.alloc(max_bytes), cm.alloc(max_bytes)) for c, cm in comms.items()}
     dev = torch.device("cuda", local)
     res = []
     for mb in sizes_mb:
@@ -365,12 +365,17 @@ def run_sweep(args):
 
         bus = S * (world - 1) / world
         r = {"size_mb": mb}
-        r["ag_ours_gbs"] = bus / (timeit(lambda: comm.all_gather((world, 1), [shard], dst, torch.bfloat16)) * 1e-3) / 1e9
-        r["rs_ours_gbs"] = bus / (timeit(lambda: comm.reduce_scatter((world, 1), [flat], stage, [out], postdiv=float(world))) * 1e-3) / 1e9
+        for c, cm in comms.items():
+            stage, dst = offs[c]
+            r[f"ag_ours_c{c}"] = bus / (timeit(lambda: cm.all_gather((world, 1), [shard], dst, torch.bfloat16)) * 1e-3) / 1e9
+            r[f"rs_ours_c{c}"] = bus / (timeit(lambda: cm.reduce_scatter((world, 1), [flat], stage, [out], postdiv=float(world))) * 1e-3) / 1e9
+        r["ag_ours_gbs"] = max(r[f"ag_ours_c{c}"] for c in comms)
+        r["rs_ours_gbs"] = max(r[f"rs_ours_c{c}"] for c in comms)
         r["ag_nccl_gbs"] = bus / (timeit(lambda: dist.all_gather_into_tensor(full, shard)) * 1e-3) / 1e9
         r["rs_nccl_gbs"] = bus / (timeit(lambda: dist.reduce_scatter_tensor(out_bf, flat)) * 1e-3) / 1e9
         res.append({k: (round(v, 1) if isinstance(v, float) else v) for k, v in r.items()})
-    comm.close()
+    for cm in comms.values():
+        cm.close()
     if rank == 0:
         best = max(res, key=lambda r: r["ag_ours_gbs"])
         return {"metric": "AG/RS bus GB/s vs 900 GB/s NVLink", "value": best["ag_ours_gbs"],

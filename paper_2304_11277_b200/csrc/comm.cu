@@ -23,6 +23,7 @@
 #include <cooperative_groups.h>
 
 #include <cstring>
+#include <type_traits>
 #include <map>
 #include <vector>
 
@@ -40,7 +41,8 @@ static_assert(kScalarOff + 4 * FSDP_MAX_RANKS <= kReserved, "reserved region too
 
 constexpr int kCommThreads = 512;
 constexpr int kVec = 8;                                  // elements per vector
-constexpr int kTileElems = kCommThreads * kVec * 2;      // 8192 elements per tile
+constexpr int kU = 4;                                    // vectors per thread per tile
+constexpr int kTileElems = kCommThreads * kVec * kU;     // 16384 elements per tile
 
 struct CollParams {
   char* bases[FSDP_MAX_RANKS];
@@ -132,6 +134,59 @@ __device__ __noinline__ void cta_barrier(const CollParams& p, const Group& g, in
   __syncthreads();
 }
 
+// ------------------------------------------------- vector memory helpers ----
+// Non-volatile loads/stores so the compiler can keep kU independent 16-byte
+// requests in flight per thread (a dependent load->use->load chain caps a
+// thread at one outstanding request).
+template <typename T> __device__ __forceinline__ Packed8<T> ldg8(const T* p);
+template <> __device__ __forceinline__ Packed8<float> ldg8<float>(const float* p) {
+  return {__ldg(reinterpret_cast<const uint4*>(p)), __ldg(reinterpret_cast<const uint4*>(p) + 1)};
+}
+template <> __device__ __forceinline__ Packed8<__nv_bfloat16> ldg8<__nv_bfloat16>(const __nv_bfloat16* p) {
+  return {__ldg(reinterpret_cast<const uint4*>(p))};
+}
+// L2-coherent (peer-written during this kernel)
+template <typename T> __device__ __forceinline__ Packed8<T> ldcg8(const T* p);
+template <> __device__ __forceinline__ Packed8<float> ldcg8<float>(const float* p) {
+  return {__ldcg(reinterpret_cast<const uint4*>(p)), __ldcg(reinterpret_cast<const uint4*>(p) + 1)};
+}
+template <> __device__ __forceinline__ Packed8<__nv_bfloat16> ldcg8<__nv_bfloat16>(const __nv_bfloat16* p) {
+  return {__ldcg(reinterpret_cast<const uint4*>(p))};
+}
+template <typename T> __device__ __forceinline__ void st8(T* p, const Packed8<T>& v);
+template <> __device__ __forceinline__ void st8<float>(float* p, const Packed8<float>& v) {
+  reinterpret_cast<uint4*>(p)[0] = v.a;
+  reinterpret_cast<uint4*>(p)[1] = v.b;
+}
+template <> __device__ __forceinline__ void st8<__nv_bfloat16>(__nv_bfloat16* p, const Packed8<__nv_bfloat16>& v) {
+  reinterpret_cast<uint4*>(p)[0] = v.a;
+}
+template <typename T> __device__ __forceinline__ V8F unpack8(const Packed8<T>& r);
+template <> __device__ __forceinline__ V8F unpack8<float>(const Packed8<float>& r) {
+  V8F x;
+  x.v[0] = __uint_as_float(r.a.x); x.v[1] = __uint_as_float(r.a.y);
+  x.v[2] = __uint_as_float(r.a.z); x.v[3] = __uint_as_float(r.a.w);
+  x.v[4] = __uint_as_float(r.b.x); x.v[5] = __uint_as_float(r.b.y);
+  x.v[6] = __uint_as_float(r.b.z); x.v[7] = __uint_as_float(r.b.w);
+  return x;
+}
+template <> __device__ __forceinline__ V8F unpack8<__nv_bfloat16>(const Packed8<__nv_bfloat16>& r) {
+  V8F x;
+  x.v[0] = bf16lo(r.a.x); x.v[1] = bf16hi(r.a.x); x.v[2] = bf16lo(r.a.y); x.v[3] = bf16hi(r.a.y);
+  x.v[4] = bf16lo(r.a.z); x.v[5] = bf16hi(r.a.z); x.v[6] = bf16lo(r.a.w); x.v[7] = bf16hi(r.a.w);
+  return x;
+}
+template <typename Tin, typename Tout>
+__device__ __forceinline__ Packed8<Tout> convert8(const Packed8<Tin>& r) {
+  if constexpr (std::is_same<Tin, Tout>::value) return r;
+  else return pack8<Tout>(unpack8<Tin>(r));
+}
+
+// index of the u-th vector of this thread inside tile t
+__device__ __forceinline__ int64_t vec_index(int64_t t, int u) {
+  return t * kTileElems + ((int64_t)u * kCommThreads + threadIdx.x) * kVec;
+}
+
 // ------------------------------------------------------------ all-gather ----
 template <typename Tin, typename Tout>
 __global__ void __launch_bounds__(kCommThreads)
@@ -146,21 +201,24 @@ allgather_kernel(const __grid_constant__ CollParams p) {
   const bool vec = (n % kVec == 0) && aligned16(src) && (my_off % 16 == 0);
   const int64_t ntiles = (n + kTileElems - 1) / kTileElems;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int64_t t0 = t * kTileElems;
-    const int64_t t1 = min(t0 + (int64_t)kTileElems, n);
     if (vec) {
+      Packed8<Tout> o[kU];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int64_t i = t0 + ((int64_t)u * kCommThreads + threadIdx.x) * kVec;
-        if (i < t1) {
-          const Packed8<Tout> v = pack8<Tout>(load8<Tin>(src + i, LD_NC));
-          for (int jj = 0; jj < g.size; ++jj) {
-            const int j = (g.pos + 1 + jj) % g.size;   // stagger destinations
-            store8<Tout>((Tout*)(p.bases[g.member(j)] + my_off) + i, v);
-          }
+      for (int u = 0; u < kU; ++u) {
+        const int64_t i = vec_index(t, u);
+        if (i < n) o[u] = convert8<Tin, Tout>(ldg8<Tin>(src + i));
+      }
+      for (int jj = 0; jj < g.size; ++jj) {
+        const int j = (g.pos + 1 + jj) % g.size;     // stagger destinations
+        Tout* d = (Tout*)(p.bases[g.member(j)] + my_off);
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int64_t i = vec_index(t, u);
+          if (i < n) st8<Tout>(d + i, o[u]);
         }
       }
     } else {
+      const int64_t t0 = t * kTileElems, t1 = min(t0 + (int64_t)kTileElems, n);
       for (int64_t i = t0 + threadIdx.x; i < t1; i += kCommThreads) {
         const Tout v = from_f<Tout>(to_f<Tin>(src[i]));
         for (int jj = 0; jj < g.size; ++jj) {
@@ -185,64 +243,79 @@ reduce_scatter_kernel(const __grid_constant__ CollParams p) {
   const int64_t slot_bytes = n * (int64_t)sizeof(Tin);
   cta_barrier(p, g, 0, false);   // every member's staging is free
 
-  const bool vec = (n % kVec == 0) && aligned16(flat) && (p.off_a % 16 == 0);
+  const bool vec = (n % kVec == 0) && aligned16(flat) && (p.off_a % 16 == 0) && aligned16(out);
   const int64_t ntiles = (n + kTileElems - 1) / kTileElems;
   // phase 1: chunk j of my flat payload -> member j's staging slot [my pos]
+  // (my own chunk stays in place and is read directly in phase 2)
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int64_t t0 = t * kTileElems;
-    const int64_t t1 = min(t0 + (int64_t)kTileElems, n);
-    for (int jj = 0; jj < g.size; ++jj) {
-      const int j = (g.pos + 1 + jj) % g.size;
+    for (int jj = 1; jj < g.size; ++jj) {
+      const int j = (g.pos + jj) % g.size;
       Tin* dst = (Tin*)(p.bases[g.member(j)] + p.off_a + (int64_t)g.pos * slot_bytes);
       const Tin* s = flat + (int64_t)j * n;
       if (vec) {
+        Packed8<Tin> r[kU];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int64_t i = t0 + ((int64_t)u * kCommThreads + threadIdx.x) * kVec;
-          if (i < t1) st_v4(dst + i, ld_stream(s + i));
-          if (sizeof(Tin) == 4 && i < t1) st_v4(dst + i + 4, ld_stream(s + i + 4));
+        for (int u = 0; u < kU; ++u) {
+          const int64_t i = vec_index(t, u);
+          if (i < n) r[u] = ldg8<Tin>(s + i);
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int64_t i = vec_index(t, u);
+          if (i < n) st8<Tin>(dst + i, r[u]);
         }
       } else {
+        const int64_t t0 = t * kTileElems, t1 = min(t0 + (int64_t)kTileElems, n);
         for (int64_t i = t0 + threadIdx.x; i < t1; i += kCommThreads) dst[i] = s[i];
       }
     }
   }
   cta_barrier(p, g, 1, true);    // my tiles of every member's chunk arrived
-  // phase 2: ascending-rank fp32 sum of my slots, post-divide, accumulate
+  // phase 2: ascending-rank fp32 sum of the group's chunks, post-divide, accumulate
   const Tin* stage = (const Tin*)(p.bases[g.rank] + p.off_a);
+  const Tin* mine = flat + (int64_t)g.pos * n;
   const bool pre = p.prediv != 1.0f, post = p.postdiv != 1.0f;
-  const bool vec_out = vec && aligned16(out);
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int64_t t0 = t * kTileElems;
-    const int64_t t1 = min(t0 + (int64_t)kTileElems, n);
-    if (vec_out) {
+    if (vec) {
+      V8F acc[kU];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int64_t i = t0 + ((int64_t)u * kCommThreads + threadIdx.x) * kVec;
-        if (i >= t1) continue;
-        V8F acc;
+      for (int u = 0; u < kU; ++u)
 #pragma unroll
-        for (int k = 0; k < 8; ++k) acc.v[k] = 0.0f;
-        for (int j = 0; j < g.size; ++j) {
-          V8F x = load8<Tin>(stage + (int64_t)j * n + i, LD_CG);
+        for (int k = 0; k < 8; ++k) acc[u].v[k] = 0.0f;
+      for (int j = 0; j < g.size; ++j) {
+        Packed8<Tin> r[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int64_t i = vec_index(t, u);
+          if (i < n) r[u] = (j == g.pos) ? ldg8<Tin>(mine + i) : ldcg8<Tin>(stage + (int64_t)j * n + i);
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const V8F x = unpack8<Tin>(r[u]);
 #pragma unroll
           for (int k = 0; k < 8; ++k)
-            acc.v[k] = __fadd_rn(acc.v[k], pre ? __fdiv_rn(x.v[k], p.prediv) : x.v[k]);
+            acc[u].v[k] = __fadd_rn(acc[u].v[k], pre ? __fdiv_rn(x.v[k], p.prediv) : x.v[k]);
         }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int64_t i = vec_index(t, u);
+        if (i >= n) continue;
         V8F base;
-        if (p.accumulate) base = load8<float>(out + i, LD_PLAIN);
+        if (p.accumulate) base = unpack8<float>(ldcg8<float>(out + i));
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          const float r = post ? __fdiv_rn(acc.v[k], p.postdiv) : acc.v[k];
-          acc.v[k] = __fadd_rn(p.accumulate ? base.v[k] : 0.0f, r);
+          const float r = post ? __fdiv_rn(acc[u].v[k], p.postdiv) : acc[u].v[k];
+          acc[u].v[k] = __fadd_rn(p.accumulate ? base.v[k] : 0.0f, r);
         }
-        store8<float>(out + i, pack8<float>(acc));
+        st8<float>(out + i, pack8<float>(acc[u]));
       }
     } else {
+      const int64_t t0 = t * kTileElems, t1 = min(t0 + (int64_t)kTileElems, n);
       for (int64_t i = t0 + threadIdx.x; i < t1; i += kCommThreads) {
         float acc = 0.0f;
         for (int j = 0; j < g.size; ++j) {
-          const float x = to_f<Tin>(ldcg_elem(stage + (int64_t)j * n + i));
+          const float x = to_f<Tin>(j == g.pos ? mine[i] : ldcg_elem(stage + (int64_t)j * n + i));
           acc = __fadd_rn(acc, pre ? __fdiv_rn(x, p.prediv) : x);
         }
         const float r = post ? __fdiv_rn(acc, p.postdiv) : acc;
@@ -254,6 +327,8 @@ reduce_scatter_kernel(const __grid_constant__ CollParams p) {
 
 // ------------------------------------------------------------ all-reduce ----
 // Two-shot: RS-push to chunk owners, ascending fp32 sum, AG-push of results.
+// Chunk stride c is a multiple of 8; the last chunk may be short (tail
+// elements take the scalar path).
 template <typename Tin>
 __global__ void __launch_bounds__(kCommThreads)
 allreduce_kernel(const __grid_constant__ CollParams p) {
@@ -268,52 +343,96 @@ allreduce_kernel(const __grid_constant__ CollParams p) {
     const int64_t s = (int64_t)j * c;
     return s >= n ? 0 : min(c, n - s);
   };
+  const bool vec = aligned16(in) && aligned16(out) && (p.off_a % 16 == 0) && (p.off_b % 16 == 0);
   cta_barrier(p, g, 0, false);
 
   const int64_t ntiles = (c + kTileElems - 1) / kTileElems;
-  // phase A: my chunk j -> member j's stage slot [my pos]
+  // phase A: my chunk j -> member j's stage slot [my pos] (own chunk stays)
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int64_t t0 = t * kTileElems;
-    for (int jj = 0; jj < g.size; ++jj) {
-      const int j = (g.pos + 1 + jj) % g.size;
+    for (int jj = 1; jj < g.size; ++jj) {
+      const int j = (g.pos + jj) % g.size;
       const int64_t len = clen(j);
-      const int64_t t1 = min(t0 + (int64_t)kTileElems, len);
       Tin* dst = (Tin*)(p.bases[g.member(j)] + p.off_a) + (int64_t)g.pos * c;
       const Tin* s = in + (int64_t)j * c;
-      for (int64_t i = t0 + threadIdx.x; i < t1; i += kCommThreads) dst[i] = s[i];
+      Packed8<Tin> r[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int64_t i = vec_index(t, u);
+        if (vec && i + kVec <= len) r[u] = ldg8<Tin>(s + i);
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int64_t i = vec_index(t, u);
+        if (vec && i + kVec <= len) st8<Tin>(dst + i, r[u]);
+        else for (int64_t k = i; k < min(i + kVec, len); ++k) dst[k] = s[k];
+      }
     }
   }
   cta_barrier(p, g, 1, true);
-  // reduce my chunk, push the result to every member's gather buffer
+  // phase B: reduce my chunk (ascending), push fp32 result to every member
   {
     const Tin* stage = (const Tin*)(p.bases[g.rank] + p.off_a);
+    const Tin* mine = in + (int64_t)g.pos * c;
     const int64_t len = clen(g.pos);
     const bool post = p.postdiv != 1.0f;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      const int64_t t0 = t * kTileElems;
-      const int64_t t1 = min(t0 + (int64_t)kTileElems, len);
-      for (int64_t i = t0 + threadIdx.x; i < t1; i += kCommThreads) {
-        float acc = 0.0f;
-        for (int j = 0; j < g.size; ++j) acc = __fadd_rn(acc, to_f<Tin>(ldcg_elem(stage + (int64_t)j * c + i)));
-        const float r = post ? __fdiv_rn(acc, p.postdiv) : acc;
+      V8F acc[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[u].v[k] = 0.0f;
+      for (int j = 0; j < g.size; ++j) {
+        const Tin* s = (j == g.pos) ? mine : stage + (int64_t)j * c;
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int64_t i = vec_index(t, u);
+          if (vec && i + kVec <= len) {
+            const V8F x = unpack8<Tin>(j == g.pos ? ldg8<Tin>(s + i) : ldcg8<Tin>(s + i));
+#pragma unroll
+            for (int k = 0; k < 8; ++k) acc[u].v[k] = __fadd_rn(acc[u].v[k], x.v[k]);
+          } else {
+            for (int k = 0; k < 8 && i + k < len; ++k)
+              acc[u].v[k] = __fadd_rn(acc[u].v[k], to_f<Tin>(j == g.pos ? s[i + k] : ldcg_elem(s + i + k)));
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int64_t i = vec_index(t, u);
+        if (i >= len) continue;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[u].v[k] = post ? __fdiv_rn(acc[u].v[k], p.postdiv) : acc[u].v[k];
+        const Packed8<float> pk = pack8<float>(acc[u]);
         for (int jj = 0; jj < g.size; ++jj) {
           const int j = (g.pos + 1 + jj) % g.size;
-          ((float*)(p.bases[g.member(j)] + p.off_b))[(int64_t)g.pos * c + i] = r;
+          float* d = (float*)(p.bases[g.member(j)] + p.off_b) + (int64_t)g.pos * c;
+          if (vec && i + kVec <= len) st8<float>(d + i, pk);
+          else for (int k = 0; k < 8 && i + k < len; ++k) d[i + k] = acc[u].v[k];
         }
       }
     }
   }
   cta_barrier(p, g, 2, true);
-  // epilogue: out = (accumulate ? out : 0) + gathered, for my tiles of every chunk
+  // phase C: out = (accumulate ? out : 0) + gathered, for my tiles of every chunk
   const float* gath = (const float*)(p.bases[g.rank] + p.off_b);
   for (int j = 0; j < g.size; ++j) {
     const int64_t len = clen(j);
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      const int64_t t0 = t * kTileElems;
-      const int64_t t1 = min(t0 + (int64_t)kTileElems, len);
-      for (int64_t i = t0 + threadIdx.x; i < t1; i += kCommThreads) {
-        const int64_t k = (int64_t)j * c + i;
-        out[k] = __fadd_rn(p.accumulate ? out[k] : 0.0f, __ldcg(gath + k));
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int64_t i = vec_index(t, u);
+        const int64_t k0 = (int64_t)j * c + i;
+        if (vec && i + kVec <= len) {
+          V8F x = unpack8<float>(ldcg8<float>(gath + k0));
+          V8F b;
+          if (p.accumulate) b = unpack8<float>(ldcg8<float>(out + k0));
+#pragma unroll
+          for (int k = 0; k < 8; ++k) x.v[k] = __fadd_rn(p.accumulate ? b.v[k] : 0.0f, x.v[k]);
+          st8<float>(out + k0, pack8<float>(x));
+        } else {
+          for (int k = 0; k < 8 && i + k < len; ++k)
+            out[k0 + k] = __fadd_rn(p.accumulate ? out[k0 + k] : 0.0f, __ldcg(gath + k0 + k));
+        }
       }
     }
   }

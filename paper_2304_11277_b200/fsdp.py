@@ -48,7 +48,7 @@ from .comm import DeviceComm
 from .layout import SharedParameterError, build_unit_layouts
 from .plan import build_plan
 from .runtime import (ACCUM_OFF, NRAF, PREFETCH_POST, PREFETCH_PRE, RAF, FSDPRuntime,
-                      RuntimeConfig)
+                      PreBackward, RuntimeConfig, UnitViews)
 
 
 class ShardingStrategy(enum.Enum):
@@ -103,33 +103,6 @@ def _policy_fn(policy) -> Callable[[nn.Module], bool] | None:
     return lambda m: bool(policy(module=m, recurse=False, nonwrapped_numel=0))
 
 
-class _UnitViews(torch.autograd.Function):
-    """forward: the unit's original parameters as views of its unsharded flat
-    buffer; backward: the post-backward hook (write-back + reduce-scatter)."""
-
-    @staticmethod
-    def forward(ctx, anchor, flat, rt, uid):
-        ctx.rt, ctx.uid = rt, uid
-        ctx.set_materialize_grads(False)
-        return tuple(flat.narrow(0, o.offset, o.numel).view(o.shape)
-                     for o in rt.units[uid].layout.originals)
-
-    @staticmethod
-    def backward(ctx, *grads):
-        ctx.rt.post_backward(ctx.uid, grads)
-        return None, None, None, None
-
-
-class _PreBackward(torch.autograd.Function):
-    @staticmethod
-    def forward(ctx, wrapper, uid, *outs):
-        ctx.wrapper, ctx.uid = wrapper, uid
-        return tuple(o.view_as(o) for o in outs)
-
-    @staticmethod
-    def backward(ctx, *grads):
-        ctx.wrapper._pre_backward(ctx.uid)
-        return (None, None) + grads
 
 
 def _map_tensors(fn, obj):
@@ -294,15 +267,15 @@ class FullyShardedDataParallel(nn.Module):
             self._handles.append(um.register_forward_pre_hook(functools.partial(self._pre_fwd, uid)))
             self._handles.append(um.register_forward_hook(functools.partial(self._post_fwd, uid)))
         self._defer = False
-        self._bwd_started = False
         self._new_micro = True
+        self.rt.on_end_backward = self._end_backward
         self.mixed = mixed
 
     # ------------------------------------------------------------ hooks ---
     def _install(self, uid: int, flat: torch.Tensor) -> None:
         if flat.numel() == 0 or not self._refs[uid]:
             return
-        views = _UnitViews.apply(self._anchors[uid], flat, self.rt, uid)
+        views = UnitViews.apply(self._anchors[uid], flat, self.rt, uid)
         for (m, pname), a in zip(self._refs[uid], self._alias[uid]):
             setattr(m, pname, views[a])
 
@@ -313,7 +286,6 @@ class FullyShardedDataParallel(nn.Module):
                 self._new_micro = False
                 rt.begin_micro(final=not self._defer)
                 rt.defer_reduce = self._defer
-                self._bwd_started = False
             rt.begin_forward_pass()
         pos = rt.record_forward(uid)
         flat = rt.ensure_unsharded(uid)
@@ -326,25 +298,11 @@ class FullyShardedDataParallel(nn.Module):
         rt.post_order.append(uid)
         rt.close_window(uid)
         if torch.is_grad_enabled():
-            output = _map_tensors(lambda ts: _PreBackward.apply(self, uid, *ts), output)
+            output = _map_tensors(lambda ts: PreBackward.apply(rt, uid, *ts), output)
         rt.release_use(uid, "forward", 0)
         return output
 
-    def _pre_backward(self, uid: int) -> None:
-        rt = self.rt
-        if not self._bwd_started:
-            self._bwd_started = True
-            rt.start_backward()
-            torch.autograd.Variable._execution_engine.queue_callback(self._end_backward)
-        if uid in rt.bwd_pos and not getattr(rt.units[uid], "_pre_done", False):
-            rt.units[uid]._pre_done = True
-            rt.pre_backward(uid)
-
     def _end_backward(self) -> None:
-        for u in self.rt.units:
-            u._pre_done = False
-        self.rt.end_backward()
-        self._bwd_started = False
         self._new_micro = True
 
     # -------------------------------------------------------------- api ---

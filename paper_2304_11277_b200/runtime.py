@@ -169,9 +169,61 @@ class _SlotRef:
         self.uid, self.off, self.size, self.stride = uid, off, size, stride
 
 
+class UnitViews(torch.autograd.Function):
+    """forward: the unit's original parameters as views of its unsharded flat
+    buffer (flatparam.py:159-164); backward: the post-backward hook
+    (write-back + reduce-scatter, engine.py:527-556)."""
+
+    @staticmethod
+    def forward(ctx, anchor, flat, rt, uid):
+        ctx.rt, ctx.uid = rt, uid
+        ctx.set_materialize_grads(False)
+        return tuple(flat.narrow(0, o.offset, o.numel).view(o.shape)
+                     for o in rt.units[uid].layout.originals)
+
+    @staticmethod
+    def backward(ctx, *grads):
+        ctx.rt.post_backward(ctx.uid, grads)
+        return None, None, None, None
+
+
+class PreBackward(torch.autograd.Function):
+    """Identity on a unit's outputs; its backward is the unit's pre-backward
+    hook (unshard before the unit's gradient computation)."""
+
+    @staticmethod
+    def forward(ctx, rt, uid, *outs):
+        ctx.rt, ctx.uid = rt, uid
+        return tuple(o.view_as(o) for o in outs)
+
+    @staticmethod
+    def backward(ctx, *grads):
+        ctx.rt.autograd_pre_backward(ctx.uid)
+        return (None, None) + grads
+
+
 class FSDPRuntime:
     """The per-rank engine.  `comm` is a DeviceComm (or None at world 1 /
     NCCL backend)."""
+
+    on_end_backward: Callable[[], None] | None = None
+    _bwd_started = False
+
+    def autograd_pre_backward(self, uid: int) -> None:
+        """First call of a backward pass: fix the backward order and queue the
+        end-of-backward callback; then unshard `uid`."""
+        if not self._bwd_started:
+            self._bwd_started = True
+            self.start_backward()
+            torch.autograd.Variable._execution_engine.queue_callback(self._autograd_end_backward)
+        if uid in self.bwd_pos:
+            self.pre_backward(uid)
+
+    def _autograd_end_backward(self) -> None:
+        self._bwd_started = False
+        self.end_backward()
+        if self.on_end_backward is not None:
+            self.on_end_backward()
 
     def __init__(self, layouts: Sequence[UnitLayout], plan: ShardingPlan, rank: int,
                  config: RuntimeConfig, comm=None, process_groups=None,
@@ -212,6 +264,7 @@ class FSDPRuntime:
         self.found_inf_world = torch.zeros(1, dtype=torch.float32, device=self.device)
         self.opt_done: torch.cuda.Event | None = None
         self.adam_steps = 0
+        self.max_live_slots = 0
         self.fwd_visits: dict[int, int] = {}
         self.bytes_ag = 0
         self.bytes_rs = 0
@@ -364,6 +417,7 @@ class FSDPRuntime:
         u = self.units[uid]
         lay = u.layout
         slot, free_ev = self.slots.acquire(uid)
+        self.max_live_slots = max(self.max_live_slots, len(self.slots.owner))
         u.slot = slot
         views = self.slots.views[slot]
         u.unsharded = views[0][: lay.psi]
@@ -547,6 +601,7 @@ class FSDPRuntime:
         nested root first)."""
         if not self.in_backward:
             self.in_backward = True
+            self.trace.append(("backward_begin", None))
             seen, order = set(), []
             for uid in reversed(self.post_order):
                 if uid not in seen:
@@ -559,7 +614,6 @@ class FSDPRuntime:
 
     def pre_backward(self, uid: int) -> None:
         self.ensure_unsharded(uid)
-        self.close_window(uid)
         if self.cfg.backward_prefetch == PREFETCH_PRE:
             pos = self.bwd_pos.get(uid)
             if pos is not None and pos + 1 < len(self.bwd_order):
@@ -569,6 +623,7 @@ class FSDPRuntime:
         """Gradient write-back (flatten) + finalisation + reduction."""
         u = self.units[uid]
         lay = u.layout
+        self.close_window(uid)     # the unit's backward compute has been issued
         missing = [o.name for o, g in zip(lay.originals, grads) if g is None]
         if missing and len(missing) < len(lay.originals):
             warnings.warn(f"unit {uid}: no gradient for {missing}, zero-filled")
@@ -672,15 +727,17 @@ class FSDPRuntime:
                                              [u.grad], prediv=pre, postdiv=post,
                                              accumulate=accumulate, stream=self.rs_stream)
             elif F == 1:
-                self.comm.all_reduce(self.plan.replicated_desc, [payload], self.ar_stage_off,
-                                     self.ar_gather_off, [u.grad], postdiv=post,
-                                     accumulate=accumulate, stream=self.rs_stream)
+                with self.timed("allreduce", self.rs_stream, payload.numel() * payload.element_size()):
+                    self.comm.all_reduce(self.plan.replicated_desc, [payload], self.ar_stage_off,
+                                         self.ar_gather_off, [u.grad], postdiv=post,
+                                         accumulate=accumulate, stream=self.rs_stream)
             else:
                 tmp = torch.empty(n, dtype=torch.float32, device=self.device)
                 self.comm.reduce_scatter(self.plan.sharded_desc, [payload], self.rs_stage_off,
                                          [tmp], prediv=pre, postdiv=1.0, accumulate=False,
                                          stream=self.rs_stream)
                 self.events.append((self.step_count, "reduce_stage2", uid))
+                self.trace.append(("AR_issue", uid))
                 self.comm.all_reduce(self.plan.replicated_desc, [tmp], self.ar_stage_off,
                                      self.ar_gather_off, [u.grad], postdiv=post,
                                      accumulate=accumulate, stream=self.rs_stream)

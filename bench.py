@@ -368,9 +368,12 @@ def run_sweep(args):
         for c, cm in comms.items():
             stage, dst = offs[c]
             r[f"ag_ours_c{c}"] = bus / (timeit(lambda: cm.all_gather((world, 1), [shard], dst, torch.bfloat16)) * 1e-3) / 1e9
-            r[f"rs_ours_c{c}"] = bus / (timeit(lambda: cm.reduce_scatter((world, 1), [flat], stage, [out], postdiv=float(world))) * 1e-3) / 1e9
+            r[f"rs_push_c{c}"] = bus / (timeit(lambda: cm.reduce_scatter((world, 1), [flat], stage, [out], postdiv=float(world))) * 1e-3) / 1e9
+            cm.view(stage, n * world, torch.bfloat16).copy_(flat)
+            r[f"rs_pull_c{c}"] = bus / (timeit(lambda: cm.reduce_scatter_pull((world, 1), stage, torch.bfloat16, [out], postdiv=float(world), tma=False)) * 1e-3) / 1e9
+            r[f"rs_tma_c{c}"] = bus / (timeit(lambda: cm.reduce_scatter_pull((world, 1), stage, torch.bfloat16, [out], postdiv=float(world), tma=True)) * 1e-3) / 1e9
         r["ag_ours_gbs"] = max(r[f"ag_ours_c{c}"] for c in comms)
-        r["rs_ours_gbs"] = max(r[f"rs_ours_c{c}"] for c in comms)
+        r["rs_ours_gbs"] = max(max(r[f"rs_push_c{c}"], r[f"rs_pull_c{c}"], r[f"rs_tma_c{c}"]) for c in comms)
         r["ag_nccl_gbs"] = bus / (timeit(lambda: dist.all_gather_into_tensor(full, shard)) * 1e-3) / 1e9
         r["rs_nccl_gbs"] = bus / (timeit(lambda: dist.reduce_scatter_tensor(out_bf, flat)) * 1e-3) / 1e9
         res.append({k: (round(v, 1) if isinstance(v, float) else v) for k, v in r.items()})

@@ -161,6 +161,24 @@ int fsdp_reduce_scatter(fsdp_comm_t* c, int channel, int gsize, int gstride,
                         float* const* outs, float prediv, float postdiv, int accumulate,
                         void* stream);
 
+/* Reduce-scatter, PULL variant (same semantics as fsdp_reduce_scatter): every
+ * member's flat payload lives in its own pool at src_off (gsize*n elements);
+ * the member at group position k loads chunk k of every member's buffer over
+ * NVLink in ascending rank order and reduces in fp32 registers; no staging.
+ * The caller must not rewrite its src_off region until this call completes
+ * on its stream (the kernel's exit barrier guarantees peers are done). */
+int fsdp_reduce_scatter_pull(fsdp_comm_t* c, int channel, int gsize, int gstride, int64_t src_off,
+                             int src_dtype, int64_t n, float* const* outs, float prediv,
+                             float postdiv, int accumulate, void* stream);
+
+/* Same contract as fsdp_reduce_scatter_pull; the NVLink reads are 1-D TMA
+ * bulk copies (cp.async.bulk, mbarrier-tracked, 4-stage shared-memory ring)
+ * so a few CTAs keep the link busy.  Falls back to the register-pull kernel
+ * when n % 8 != 0 or buffers are not 16-byte aligned. */
+int fsdp_reduce_scatter_tma(fsdp_comm_t* c, int channel, int gsize, int gstride, int64_t src_off,
+                            int src_dtype, int64_t n, float* const* outs, float prediv,
+                            float postdiv, int accumulate, void* stream);
+
 /* All-reduce (collectives.py:298-301; hybrid stage 2, engine.py:804-816):
  * two-shot push (reduce-scatter to owners, ascending-rank fp32 sum, then
  * all-gather of the owners' results), so every member holds bit-identical

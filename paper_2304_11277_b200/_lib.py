@@ -69,6 +69,10 @@ _SIGS = {
     "fsdp_allgather": (_i32, [_vp, _i32, _i32, _i32, _vpp, _i32, _i64, _i64, _i32, _vp]),
     "fsdp_reduce_scatter": (_i32, [_vp, _i32, _i32, _i32, _vpp, _i32, _i64, _i64, _vpp, _f32,
                                    _f32, _i32, _vp]),
+    "fsdp_reduce_scatter_pull": (_i32, [_vp, _i32, _i32, _i32, _i64, _i32, _i64, _vpp, _f32, _f32,
+                                        _i32, _vp]),
+    "fsdp_reduce_scatter_tma": (_i32, [_vp, _i32, _i32, _i32, _i64, _i32, _i64, _vpp, _f32, _f32,
+                                       _i32, _vp]),
     "fsdp_allreduce": (_i32, [_vp, _i32, _i32, _i32, _vpp, _i32, _i64, _i64, _i64, _vpp, _f32,
                               _i32, _vp]),
     "fsdp_allreduce_scalar": (_i32, [_vp, _vpp, _vpp, _vp]),

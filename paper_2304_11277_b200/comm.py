@@ -161,6 +161,18 @@ class DeviceComm:
                                       float(prediv), float(postdiv), int(accumulate),
                                       stream_ptr(stream)), "reduce_scatter")
 
+    def reduce_scatter_pull(self, gdesc, src_off: int, src_dtype: torch.dtype,
+                            outs: Sequence[torch.Tensor], prediv: float = 1.0, postdiv: float = 1.0,
+                            accumulate: bool = False, stream=None, channel: int = _lib.CH_RS,
+                            tma: bool = True) -> None:
+        """Payload already in every member's pool at `src_off` (gsize*n elems)."""
+        n = outs[0].numel()
+        fn = lib.fsdp_reduce_scatter_tma if tma else lib.fsdp_reduce_scatter_pull
+        check(fn(self._h, channel, gdesc[0], gdesc[1], src_off,
+                                           dtype_code(src_dtype), n, self._ptrs(outs), float(prediv),
+                                           float(postdiv), int(accumulate), stream_ptr(stream)),
+              "reduce_scatter_pull")
+
     def all_reduce(self, gdesc, ins: Sequence[torch.Tensor], stage_off: int, gather_off: int,
                    outs: Sequence[torch.Tensor], postdiv: float = 1.0, accumulate: bool = False,
                    stream=None, channel: int = _lib.CH_AR) -> None:

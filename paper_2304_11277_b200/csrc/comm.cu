@@ -325,6 +325,197 @@ reduce_scatter_kernel(const __grid_constant__ CollParams p) {
   }
 }
 
+// --------------------------------------------------- reduce-scatter (pull) --
+// Member at position k reads chunk k of every member's symmetric flat buffer
+// (pool offset off_a) over NVLink in ascending rank order and sums in fp32
+// registers: no staging round trip, no mid-kernel phase barrier.  Loads of
+// all MAXW members x U vectors are issued before the adds (MLP ~16 x 16 B per
+// thread), masked to the runtime group size.  Entry barrier: every member's
+// buffer is written; exit barrier: every member finished reading mine.
+template <typename Tin, int MAXW>
+__global__ void __launch_bounds__(kCommThreads)
+reduce_scatter_pull_kernel(const __grid_constant__ CollParams p) {
+  constexpr int U = (16 / MAXW) / (int)(sizeof(Tin) / 2) > 0 ? (16 / MAXW) / (int)(sizeof(Tin) / 2) : 1;
+  constexpr int64_t TILE = (int64_t)kCommThreads * kVec * U;
+  const Group g = make_group(p);
+  const int e = p.rank0 >= 0 ? 0 : blockIdx.y;
+  float* __restrict__ out = p.out[e];
+  const int64_t n = p.n;
+  const int64_t chunk_off = p.off_a + (int64_t)g.pos * n * (int64_t)sizeof(Tin);
+  const Tin* src[MAXW];
+#pragma unroll
+  for (int j = 0; j < MAXW; ++j)
+    src[j] = j < g.size ? (const Tin*)(p.bases[g.member(j)] + chunk_off) : nullptr;
+  cta_barrier(p, g, 0, false);   // every member's payload is in place
+  const bool vec = (n % kVec == 0) && (chunk_off % 16 == 0) && aligned16(out);
+  const bool pre = p.prediv != 1.0f, post = p.postdiv != 1.0f;
+  const int64_t ntiles = (n + TILE - 1) / TILE;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    if (vec) {
+      Packed8<Tin> r[MAXW][U];
+#pragma unroll
+      for (int j = 0; j < MAXW; ++j)
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t i = t * TILE + ((int64_t)u * kCommThreads + threadIdx.x) * kVec;
+          if (j < g.size && i < n) r[j][u] = ldcg8<Tin>(src[j] + i);
+        }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = t * TILE + ((int64_t)u * kCommThreads + threadIdx.x) * kVec;
+        if (i >= n) continue;
+        V8F acc;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc.v[k] = 0.0f;
+#pragma unroll
+        for (int j = 0; j < MAXW; ++j) {
+          if (j >= g.size) break;
+          const V8F x = unpack8<Tin>(r[j][u]);
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            acc.v[k] = __fadd_rn(acc.v[k], pre ? __fdiv_rn(x.v[k], p.prediv) : x.v[k]);
+        }
+        V8F base;
+        if (p.accumulate) base = unpack8<float>(ldcg8<float>(out + i));
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float rr = post ? __fdiv_rn(acc.v[k], p.postdiv) : acc.v[k];
+          acc.v[k] = __fadd_rn(p.accumulate ? base.v[k] : 0.0f, rr);
+        }
+        st8<float>(out + i, pack8<float>(acc));
+      }
+    } else {
+      const int64_t t0 = t * TILE, t1 = min(t0 + TILE, n);
+      for (int64_t i = t0 + threadIdx.x; i < t1; i += kCommThreads) {
+        float acc = 0.0f;
+        for (int j = 0; j < g.size; ++j) {
+          const float x = to_f<Tin>(ldcg_elem(src[j] + i));
+          acc = __fadd_rn(acc, pre ? __fdiv_rn(x, p.prediv) : x);
+        }
+        const float rr = post ? __fdiv_rn(acc, p.postdiv) : acc;
+        out[i] = __fadd_rn(p.accumulate ? out[i] : 0.0f, rr);
+      }
+    }
+  }
+  cta_barrier(p, g, 1, false);   // every member is done reading my buffer
+}
+
+// ------------------------------------------- reduce-scatter (TMA pull) -----
+// Same contract as reduce_scatter_pull_kernel, but the NVLink reads are 1-D
+// TMA bulk copies (cp.async.bulk -> UBLKCP) issued by one thread into a
+// kStages-deep shared-memory ring, completion tracked by mbarrier
+// transaction counts: the bytes in flight are no longer bounded by the SM's
+// load queue, so a handful of CTAs saturates the link.  Every stage holds one
+// tile of each member's chunk; all threads reduce a landed stage in
+// ascending rank order (fp32, from +0) while later stages are in flight.
+constexpr int kTmaThreads = 256;
+constexpr int kTmaStages = 4;
+constexpr int kTmaStageBytes = 32 * 1024;   // summed over the group's members
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+               :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra WAIT_%=;\n}"
+      :: "r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* smem_dst, const void* gsrc, uint32_t bytes,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      :: "r"(smem_u32(smem_dst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+template <typename Tin>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+reduce_scatter_tma_kernel(const __grid_constant__ CollParams p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t full[kTmaStages];
+  const Group g = make_group(p);
+  const int e = p.rank0 >= 0 ? 0 : blockIdx.y;
+  float* __restrict__ out = p.out[e];
+  const int64_t n = p.n;
+  const int W = g.size;
+  // elements per member tile: a multiple of 8 (16-byte bulk-copy granule)
+  const int64_t T = (kTmaStageBytes / (W * (int)sizeof(Tin))) / kVec * kVec;
+  const int64_t chunk_off = p.off_a + (int64_t)g.pos * n * (int64_t)sizeof(Tin);
+  const int64_t ntiles = (n + T - 1) / T;
+  const int64_t my_tiles = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTmaStages; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  cta_barrier(p, g, 0, false);   // every member's payload is in place (+ mbarrier init visible)
+
+  auto issue = [&](int64_t k) {   // tile iteration k -> stage k % kTmaStages
+    const int s = (int)(k % kTmaStages);
+    const int64_t t = blockIdx.x + k * gridDim.x;
+    const int64_t i0 = t * T;
+    const uint32_t bytes = (uint32_t)((min(T, n - i0)) * (int64_t)sizeof(Tin));
+    mbar_expect_tx(&full[s], bytes * W);
+    for (int j = 0; j < W; ++j) {
+      const Tin* src = (const Tin*)(p.bases[g.member(j)] + chunk_off) + i0;
+      tma_load_1d(smem + (size_t)s * kTmaStageBytes + (size_t)j * T * sizeof(Tin), src, bytes, &full[s]);
+    }
+  };
+  if (threadIdx.x == 0)
+    for (int64_t k = 0; k < my_tiles && k < kTmaStages; ++k) issue(k);
+
+  const bool pre = p.prediv != 1.0f, post = p.postdiv != 1.0f;
+  for (int64_t k = 0; k < my_tiles; ++k) {
+    const int s = (int)(k % kTmaStages);
+    mbar_wait(&full[s], (uint32_t)((k / kTmaStages) & 1));
+    const int64_t i0 = (blockIdx.x + k * gridDim.x) * T;
+    const int64_t len = min(T, n - i0);
+    const Tin* st = (const Tin*)(smem + (size_t)s * kTmaStageBytes);
+    for (int64_t v = threadIdx.x; v * kVec < len; v += kTmaThreads) {
+      V8F acc;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc.v[q] = 0.0f;
+      for (int j = 0; j < W; ++j) {
+        Packed8<Tin> r;
+        if constexpr (sizeof(Tin) == 2) {
+          r.a = *reinterpret_cast<const uint4*>(st + (size_t)j * T + v * kVec);
+        } else {
+          r.a = *reinterpret_cast<const uint4*>(st + (size_t)j * T + v * kVec);
+          r.b = *(reinterpret_cast<const uint4*>(st + (size_t)j * T + v * kVec) + 1);
+        }
+        const V8F x = unpack8<Tin>(r);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          acc.v[q] = __fadd_rn(acc.v[q], pre ? __fdiv_rn(x.v[q], p.prediv) : x.v[q]);
+      }
+      float* o = out + i0 + v * kVec;
+      V8F base;
+      if (p.accumulate) base = unpack8<float>(ldcg8<float>(o));
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float rr = post ? __fdiv_rn(acc.v[q], p.postdiv) : acc.v[q];
+        acc.v[q] = __fadd_rn(p.accumulate ? base.v[q] : 0.0f, rr);
+      }
+      st8<float>(o, pack8<float>(acc));
+    }
+    __syncthreads();   // stage s fully consumed
+    if (threadIdx.x == 0 && k + kTmaStages < my_tiles) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(k + kTmaStages);
+    }
+  }
+  cta_barrier(p, g, 1, false);   // every member is done reading my buffer
+}
+
 // ------------------------------------------------------------ all-reduce ----
 // Two-shot: RS-push to chunk owners, ascending fp32 sum, AG-push of results.
 // Chunk stride c is a multiple of 8; the last chunk may be short (tail
@@ -696,6 +887,77 @@ extern "C" int fsdp_reduce_scatter(fsdp_comm_t* c, int channel, int gsize, int g
   if (src_dtype == FSDP_BF16)
     return launch(c, reduce_scatter_kernel<__nv_bfloat16>, p, grid, kCommThreads, s);
   return launch(c, reduce_scatter_kernel<float>, p, grid, kCommThreads, s);
+}
+
+extern "C" int fsdp_reduce_scatter_pull(fsdp_comm_t* c, int channel, int gsize, int gstride,
+                                        int64_t src_off, int src_dtype, int64_t n,
+                                        float* const* outs, float prediv, float postdiv,
+                                        int accumulate, void* stream) {
+  if (int rc = validate_group(c, channel, gsize, gstride)) return rc;
+  if (n < 0 || !outs) return fail(FSDP_E_INVALID, "fsdp_reduce_scatter_pull: bad args");
+  const int is = elem_size(src_dtype);
+  if (!is) return fail(FSDP_E_INVALID, "fsdp_reduce_scatter_pull: bad dtype");
+  if (!(prediv > 0.f) || !(postdiv > 0.f)) return fail(FSDP_E_INVALID, "divisors must be > 0");
+  if (int rc = check_range(c, src_off, n * gsize * is, "fsdp_reduce_scatter_pull")) return rc;
+  CollParams p;
+  fill_common(c, p, channel, gsize, gstride, n);
+  for (int e = 0; e < nranks_args(c); ++e) p.out[e] = outs[e];
+  p.off_a = src_off;
+  p.prediv = prediv; p.postdiv = postdiv; p.accumulate = accumulate ? 1 : 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int mw = gsize <= 2 ? 2 : (gsize <= 4 ? 4 : 8);
+  const int u = std::max(1, (16 / mw) / (is / 2));
+  const int grid = std::max(1, std::min<int>(grid_for(c, n * 4 / u), c->max_ctas));
+#define RSP(T, W) launch(c, reduce_scatter_pull_kernel<T, W>, p, grid, kCommThreads, s)
+  if (src_dtype == FSDP_BF16) {
+    if (mw == 2) return RSP(__nv_bfloat16, 2);
+    if (mw == 4) return RSP(__nv_bfloat16, 4);
+    return RSP(__nv_bfloat16, 8);
+  }
+  if (mw == 2) return RSP(float, 2);
+  if (mw == 4) return RSP(float, 4);
+  return RSP(float, 8);
+#undef RSP
+}
+
+extern "C" int fsdp_reduce_scatter_tma(fsdp_comm_t* c, int channel, int gsize, int gstride,
+                                       int64_t src_off, int src_dtype, int64_t n,
+                                       float* const* outs, float prediv, float postdiv,
+                                       int accumulate, void* stream) {
+  if (int rc = validate_group(c, channel, gsize, gstride)) return rc;
+  if (n < 0 || !outs) return fail(FSDP_E_INVALID, "fsdp_reduce_scatter_tma: bad args");
+  const int is = elem_size(src_dtype);
+  if (!is) return fail(FSDP_E_INVALID, "fsdp_reduce_scatter_tma: bad dtype");
+  if (!(prediv > 0.f) || !(postdiv > 0.f)) return fail(FSDP_E_INVALID, "divisors must be > 0");
+  if (int rc = check_range(c, src_off, n * gsize * is, "fsdp_reduce_scatter_tma")) return rc;
+  bool aligned = (n % kVec == 0) && (src_off % 16 == 0);
+  for (int e = 0; e < nranks_args(c); ++e)
+    aligned = aligned && outs[e] && ((uintptr_t)outs[e] % 16 == 0);
+  if (!aligned)   // bulk copies need 16-byte granules: take the register-pull path
+    return fsdp_reduce_scatter_pull(c, channel, gsize, gstride, src_off, src_dtype, n, outs, prediv,
+                                    postdiv, accumulate, stream);
+  CollParams p;
+  fill_common(c, p, channel, gsize, gstride, n);
+  for (int e = 0; e < nranks_args(c); ++e) p.out[e] = outs[e];
+  p.off_a = src_off;
+  p.prediv = prediv; p.postdiv = postdiv; p.accumulate = accumulate ? 1 : 0;
+  const int64_t T = (kTmaStageBytes / (gsize * is)) / kVec * kVec;
+  const int64_t ntiles = (n + T - 1) / T;
+  int grid = (int)std::min<int64_t>(std::max<int64_t>(ntiles, 1), c->max_ctas);
+  if (c->emulated) grid = std::min(grid, std::max(1, 128 / c->world));
+  const size_t smem = (size_t)kTmaStages * kTmaStageBytes;
+  cudaStream_t s = (cudaStream_t)stream;
+  void* fn = src_dtype == FSDP_BF16 ? (void*)reduce_scatter_tma_kernel<__nv_bfloat16>
+                                    : (void*)reduce_scatter_tma_kernel<float>;
+  FSDP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  void* args[] = {(void*)&p};
+  if (c->emulated) {
+    FSDP_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid, c->world), dim3(kTmaThreads), args, smem, s));
+  } else {
+    FSDP_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(kTmaThreads), args, smem, s));
+  }
+  FSDP_LAUNCHED();
+  return 0;
 }
 
 extern "C" int fsdp_allreduce(fsdp_comm_t* c, int channel, int gsize, int gstride,

@@ -132,6 +132,7 @@ class UnitState:
         # gradients
         self.grad_pending = 0
         self.flat_grad: torch.Tensor | None = None
+        self.gslot: int | None = None         # symmetric gradient slot holding flat_grad
         self.accum_unsharded: torch.Tensor | None = None
         self.reduces_this_step = 0
         self.bwd_done = False
@@ -323,10 +324,19 @@ class FSDPRuntime:
             bufs = [[torch.empty(psi_max, dtype=self.compute_dtype, device=self.device)]
                     for _ in range(nslots)]
             self.slots = SlotPool(bufs, [0] * nslots, psi_max)
+        self.gslot_offs: list[int] = []
+        self.gslot_views: list[torch.Tensor] = []
+        self.gslot_free: list[torch.cuda.Event | None] = []
+        self._gslot_next = 0
         if W > 1 and self.cfg.comm_backend == "ipc":
             c = self.comm
             if F > 1:
-                self.rs_stage_off = c.alloc(psi_max * ps)
+                # two symmetric gradient slots: the write-back of unit u lands in
+                # one while the pull reduce-scatter of the previous unit reads
+                # the other (peers read them over NVLink)
+                self.gslot_offs = [c.alloc(psi_max * ps) for _ in range(2)]
+                self.gslot_views = [c.view(o, psi_max, self.payload_dtype) for o in self.gslot_offs]
+                self.gslot_free = [None, None]
             if F < W:
                 n_ar = n_max if F > 1 else psi_max
                 gsz = W // F
@@ -352,7 +362,7 @@ class FSDPRuntime:
         total = reserved
         pad = lambda b: -(-b // 256) * 256 + 256  # noqa: E731
         if F > 1:
-            total += nslots * pad(psi_max * es) + pad(psi_max * ps)
+            total += nslots * pad(psi_max * es) + 2 * pad(psi_max * ps)
         if W > 1 and F < W:
             n_ar = n_max if F > 1 else psi_max
             g = W // F
@@ -651,7 +661,12 @@ class FSDPRuntime:
             self.events.append((self.step_count, "reduce_issue", uid))
             self.release_use(uid, "backward", None)
             return
-        if first:
+        if first and self.gslot_offs and u.grad_pending == 1 and not self.defer_reduce \
+                and u.accum_unsharded is None:
+            # write-back straight into a symmetric gradient slot: the pull
+            # reduce-scatter reads it from every peer, no copy in between
+            u.gslot, u.flat_grad = self._acquire_gslot(lay.psi)
+        elif first:
             u.flat_grad = torch.empty(lay.psi, dtype=gdt, device=self.device)
         with self.timed("flatten_grad", self.compute_stream,
                         sum(g.numel() for g in srcs if g is not None) * 2 * u.flat_grad.element_size()):
@@ -693,6 +708,16 @@ class FSDPRuntime:
         kernels.flatten([u.flat_grad], [0], u.accum_unsharded, accumulate=not first,
                         stream=self.compute_stream)
 
+    def _acquire_gslot(self, psi: int) -> tuple[int, torch.Tensor]:
+        """Next symmetric gradient slot (alternating); compute waits until the
+        reduce-scatter that last read it has finished on every peer."""
+        idx = self._gslot_next
+        self._gslot_next = 1 - idx
+        ev = self.gslot_free[idx]
+        if ev is not None:
+            self.compute_stream.wait_event(ev)
+        return idx, self.gslot_views[idx][:psi]
+
     def _reduce_unit(self, uid: int, grad: torch.Tensor) -> None:
         """engine.py:771-820 on the reduce-scatter stream."""
         u = self.units[uid]
@@ -702,6 +727,13 @@ class FSDPRuntime:
         pre = self.cfg.gradient_predivide
         if pre != 1.0:
             post = post / pre
+        gslot = getattr(u, "gslot", None)
+        if self.gslot_offs and gslot is None:
+            # payload not yet in a slot (accumulated / multi-forward / zero-filled)
+            gslot, view = self._acquire_gslot(u.layout.psi)
+            kernels.cast(grad, view, stream=self.compute_stream)
+            grad = view
+        u.gslot = None
         ready = torch.cuda.Event()
         ready.record(self.compute_stream)
         self.events.append((self.step_count, "reduce_issue", uid))
@@ -723,9 +755,10 @@ class FSDPRuntime:
                 self._reduce_nccl(u, payload, accumulate, pre, post)
             elif F == W:
                 with self.timed("reduce_scatter", self.rs_stream, payload.numel() * payload.element_size()):
-                    self.comm.reduce_scatter(self.plan.sharded_desc, [payload], self.rs_stage_off,
-                                             [u.grad], prediv=pre, postdiv=post,
-                                             accumulate=accumulate, stream=self.rs_stream)
+                    self.comm.reduce_scatter_pull(self.plan.sharded_desc, self.gslot_offs[gslot],
+                                                  payload.dtype, [u.grad], prediv=pre, postdiv=post,
+                                                  accumulate=accumulate, stream=self.rs_stream,
+                                                  tma=False)
             elif F == 1:
                 with self.timed("allreduce", self.rs_stream, payload.numel() * payload.element_size()):
                     self.comm.all_reduce(self.plan.replicated_desc, [payload], self.ar_stage_off,
@@ -733,15 +766,21 @@ class FSDPRuntime:
                                          accumulate=accumulate, stream=self.rs_stream)
             else:
                 tmp = torch.empty(n, dtype=torch.float32, device=self.device)
-                self.comm.reduce_scatter(self.plan.sharded_desc, [payload], self.rs_stage_off,
-                                         [tmp], prediv=pre, postdiv=1.0, accumulate=False,
-                                         stream=self.rs_stream)
+                with self.timed("reduce_scatter", self.rs_stream, payload.numel() * payload.element_size()):
+                    self.comm.reduce_scatter_pull(self.plan.sharded_desc, self.gslot_offs[gslot],
+                                                  payload.dtype, [tmp], prediv=pre, postdiv=1.0,
+                                                  accumulate=False, stream=self.rs_stream, tma=False)
                 self.events.append((self.step_count, "reduce_stage2", uid))
                 self.trace.append(("AR_issue", uid))
-                self.comm.all_reduce(self.plan.replicated_desc, [tmp], self.ar_stage_off,
-                                     self.ar_gather_off, [u.grad], postdiv=post,
-                                     accumulate=accumulate, stream=self.rs_stream)
+                with self.timed("allreduce", self.rs_stream, n * 4):
+                    self.comm.all_reduce(self.plan.replicated_desc, [tmp], self.ar_stage_off,
+                                         self.ar_gather_off, [u.grad], postdiv=post,
+                                         accumulate=accumulate, stream=self.rs_stream)
             payload.record_stream(self.rs_stream)
+            if gslot is not None:
+                ev = torch.cuda.Event()
+                ev.record(self.rs_stream)
+                self.gslot_free[gslot] = ev
         self.bytes_rs += grad.numel() * (2 if self.payload_dtype == torch.bfloat16 else 4)
         u.reduces_this_step += 1
 

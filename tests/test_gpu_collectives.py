@@ -121,6 +121,53 @@ def test_reduce_scatter_bf16_fp32_accumulate_divide(w, n):
         c.close()
 
 
+@pytest.mark.parametrize("tma", [False, True])
+@pytest.mark.parametrize("w", [1, 2, 3, 4, 8])
+def test_reduce_scatter_pull_matches_golden(golden, w, tma):
+    arrays, _ = golden
+    inputs = [arrays[f"coll/in/w{w}/r{r}"] for r in range(w)]
+    n = inputs[0].size
+    c = make_comm(w)
+    try:
+        off = c.alloc(1 << 20)
+        for r in range(w):
+            c.view(off, n, torch.float32, r).copy_(cu(inputs[r]))
+        outs = [torch.empty(n // w, device="cuda") for _ in range(w)]
+        c.reduce_scatter_pull((w, 1), off, torch.float32, outs, tma=tma)
+        for r in range(w):
+            assert outs[r].cpu().numpy().tobytes() == arrays[f"coll/rs/w{w}/out{r}"].tobytes()
+    finally:
+        c.close()
+
+
+@pytest.mark.parametrize("w,f", [(2, 2), (4, 4), (8, 8), (8, 4), (6, 3), (4, 2)])
+@pytest.mark.parametrize("n", [16, 1000, 65536 + 8, 1 << 20])
+@pytest.mark.parametrize("dt", ["bf16", "f32"])
+@pytest.mark.parametrize("tma", [False, True])
+def test_reduce_scatter_pull_bf16_divide_accumulate(w, f, n, dt, tma):
+    rng = np.random.default_rng(w * 100 + f * 10 + n)
+    tdt = torch.bfloat16 if dt == "bf16" else torch.float32
+    grads = [rng.standard_normal(n * f).astype(np.float32) for _ in range(w)]
+    if dt == "bf16":
+        grads = [round_to_bf16(g) for g in grads]
+    acc0 = [rng.standard_normal(n).astype(np.float32) for _ in range(w)]
+    c = make_comm(w)
+    try:
+        off = c.alloc(n * f * 4 + 256)
+        for r in range(w):
+            c.view(off, n * f, tdt, r).copy_(cu(grads[r], tdt))
+        outs = [cu(a) for a in acc0]
+        c.reduce_scatter_pull((f, 1), off, tdt, outs, postdiv=float(w), accumulate=True, tma=tma)
+        for g0 in range(0, w, f):
+            grp = list(range(g0, g0 + f))
+            res = sp.reduce_scatter([grads[r] for r in grp], acc_dtype=np.float32)
+            for pos, r in enumerate(grp):
+                exp = acc0[r] + res[pos] / np.float32(w)
+                assert outs[r].cpu().numpy().tobytes() == exp.tobytes(), (r, pos)
+    finally:
+        c.close()
+
+
 @pytest.mark.parametrize("w,f", [(8, 4), (8, 2), (4, 2)])
 def test_hybrid_bf16_reduce_unit(w, f):
     """Full hybrid reduction of bf16 grads incl. / W and accumulation."""

@@ -139,6 +139,15 @@ int64_t fsdp_comm_reserved_bytes(void);
  * Synchronous read; call after synchronising the streams. */
 int fsdp_comm_device_error(fsdp_comm_t* c);
 int fsdp_comm_set_timeout_ms(fsdp_comm_t* c, int64_t ms);
+/* split != 0 (default): collectives run as [1-CTA enter barrier] [data kernel
+ * that only signals] [1-CTA exit barrier], so a late peer never parks the
+ * data kernel's CTAs on SMs.  timing != 0: CUDA events around every data
+ * kernel, read back (and recycled) by fsdp_comm_timing_drain. */
+enum { FSDP_KIND_AG = 0, FSDP_KIND_RS = 1, FSDP_KIND_AR = 2, FSDP_NUM_KINDS = 3 };
+int fsdp_comm_set_mode(fsdp_comm_t* c, int split, int timing);
+/* Synchronises on the recorded events of `kind`; writes up to max_n
+ * durations (ms) and the total count. */
+int fsdp_comm_timing_drain(fsdp_comm_t* c, int kind, float* ms_out, int max_n, int* count);
 int fsdp_comm_destroy(fsdp_comm_t* c);
 
 /* All-gather with fused cast (collectives.py:288-291 + engine.py:661-671):

@@ -110,6 +110,20 @@ class DeviceComm:
     def set_timeout_ms(self, ms: int) -> None:
         check(lib.fsdp_comm_set_timeout_ms(self._h, int(ms)))
 
+    KIND_AG, KIND_RS, KIND_AR = 0, 1, 2
+
+    def set_mode(self, split: bool = True, timing: bool = False) -> None:
+        """split: 1-CTA enter/exit barrier kernels around signal-only data
+        kernels (default); timing: CUDA events around every data kernel."""
+        check(lib.fsdp_comm_set_mode(self._h, int(split), int(timing)))
+
+    def timing_drain(self, kind: int) -> list[float]:
+        """Durations (ms) of the data kernels of `kind` since the last drain."""
+        buf = (C.c_float * 65536)()
+        cnt = C.c_int(0)
+        check(lib.fsdp_comm_timing_drain(self._h, kind, buf, 65536, C.byref(cnt)))
+        return [buf[i] for i in range(min(cnt.value, 65536))]
+
     # -------------------------------------------------------------- memory --
     @property
     def nranks_local(self) -> int:

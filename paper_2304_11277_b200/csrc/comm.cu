@@ -56,7 +56,12 @@ struct CollParams {
   float prediv, postdiv;
   int accumulate;
   int64_t timeout_ns;
+  int split;        // 1: waits live in 1-CTA enter/exit kernels, data kernels only signal
+  int data_ctas;    // exit kernel: grid of the data kernel it waits for
 };
+
+// flag slot (CTA index) reserved for the whole-collective enter barrier
+constexpr int kEnterSlot = FSDP_MAX_CTAS - 1;
 
 // ------------------------------------------------------------ primitives ----
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
@@ -187,6 +192,55 @@ __device__ __forceinline__ int64_t vec_index(int64_t t, int u) {
   return t * kTileElems + ((int64_t)u * kCommThreads + threadIdx.x) * kVec;
 }
 
+// Bounded spin on one flag (timeout -> device error word, never a hang).
+__device__ __forceinline__ void wait_flag(const CollParams& p, const Group& g, const uint32_t* f) {
+  uint32_t* err = reinterpret_cast<uint32_t*>(p.bases[g.rank] + kErrOff);
+  const uint64_t t0 = globaltimer();
+  uint32_t spins = 0;
+  while ((int32_t)(ld_acquire_sys(f) - p.epoch) < 0) {
+    if ((++spins & 1023u) == 0) {
+      if (*(volatile uint32_t*)err != 0) break;
+      if (globaltimer() - t0 > (uint64_t)p.timeout_ns) {
+        atomicExch(err, (uint32_t)FSDP_E_TIMEOUT);
+        break;
+      }
+    }
+    __nanosleep(128);
+  }
+}
+
+// Data kernels in split mode: signal this CTA's completion, never wait.
+__device__ __forceinline__ void cta_signal(const CollParams& p, const Group& g, int phase,
+                                           bool release) {
+  __syncthreads();
+  if ((int)threadIdx.x < g.size) {
+    if (release) __threadfence_system();
+    st_release_sys(flag_ptr(p.bases[g.member(threadIdx.x)], p.channel, phase, g.rank, blockIdx.x),
+                   p.epoch);
+  }
+}
+
+// Whole-collective enter barrier: one CTA per rank, one flag per peer.  Only
+// this CTA spins while a late peer catches up; the data kernel behind it in
+// stream order never occupies SMs waiting.
+__global__ void __launch_bounds__(32) coll_enter_kernel(const __grid_constant__ CollParams p) {
+  const Group g = make_group(p);
+  if ((int)threadIdx.x < g.size) {
+    const int peer = g.member(threadIdx.x);
+    st_release_sys(flag_ptr(p.bases[peer], p.channel, 0, g.rank, kEnterSlot), p.epoch);
+    wait_flag(p, g, flag_ptr(p.bases[g.rank], p.channel, 0, peer, kEnterSlot));
+  }
+}
+
+// Exit barrier: wait for every (member, data-CTA) completion flag.
+__global__ void __launch_bounds__(256) coll_exit_kernel(const __grid_constant__ CollParams p) {
+  const Group g = make_group(p);
+  for (int t = threadIdx.x; t < g.size * p.data_ctas; t += blockDim.x) {
+    const int peer = g.member(t / p.data_ctas);
+    wait_flag(p, g, flag_ptr(p.bases[g.rank], p.channel, 1, peer, t % p.data_ctas));
+  }
+}
+
 // ------------------------------------------------------------ all-gather ----
 template <typename Tin, typename Tout>
 __global__ void __launch_bounds__(kCommThreads)
@@ -196,7 +250,7 @@ allgather_kernel(const __grid_constant__ CollParams p) {
   const Tin* __restrict__ src = (const Tin*)p.in[e];
   const int64_t n = p.n;
   const int64_t my_off = p.off_a + (int64_t)g.pos * n * (int64_t)sizeof(Tout);
-  cta_barrier(p, g, 0, false);   // every member's destination slot is free
+  if (!p.split) cta_barrier(p, g, 0, false);   // every member's destination slot is free
 
   const bool vec = (n % kVec == 0) && aligned16(src) && (my_off % 16 == 0);
   const int64_t ntiles = (n + kTileElems - 1) / kTileElems;
@@ -228,7 +282,8 @@ allgather_kernel(const __grid_constant__ CollParams p) {
       }
     }
   }
-  cta_barrier(p, g, 1, true);    // all members' pieces have landed here
+  if (p.split) cta_signal(p, g, 1, true);     // my pieces have landed everywhere
+  else cta_barrier(p, g, 1, true);            // all members' pieces have landed here
 }
 
 // -------------------------------------------------------- reduce-scatter ----
@@ -346,7 +401,7 @@ reduce_scatter_pull_kernel(const __grid_constant__ CollParams p) {
 #pragma unroll
   for (int j = 0; j < MAXW; ++j)
     src[j] = j < g.size ? (const Tin*)(p.bases[g.member(j)] + chunk_off) : nullptr;
-  cta_barrier(p, g, 0, false);   // every member's payload is in place
+  if (!p.split) cta_barrier(p, g, 0, false);   // every member's payload is in place
   const bool vec = (n % kVec == 0) && (chunk_off % 16 == 0) && aligned16(out);
   const bool pre = p.prediv != 1.0f, post = p.postdiv != 1.0f;
   const int64_t ntiles = (n + TILE - 1) / TILE;
@@ -397,7 +452,8 @@ reduce_scatter_pull_kernel(const __grid_constant__ CollParams p) {
       }
     }
   }
-  cta_barrier(p, g, 1, false);   // every member is done reading my buffer
+  if (p.split) cta_signal(p, g, 1, false);   // I am done reading my tiles of everyone
+  else cta_barrier(p, g, 1, false);          // every member is done reading my buffer
 }
 
 // ------------------------------------------- reduce-scatter (TMA pull) -----
@@ -662,6 +718,10 @@ struct fsdp_comm {
   bool opened[FSDP_MAX_RANKS] = {};
   uint32_t epoch[FSDP_NUM_CH] = {};
   int64_t timeout_ns = 20LL * 1000 * 1000 * 1000;
+  bool split = true;                          // 1-CTA enter/exit kernels around data kernels
+  bool timing = false;                        // record events around every data kernel
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed[FSDP_NUM_KINDS];
+  std::vector<cudaEvent_t> spare;
 };
 
 namespace {
@@ -717,7 +777,72 @@ int launch(fsdp_comm_t* c, K kernel, const CollParams& p, int grid, int threads,
 
 int nranks_args(fsdp_comm_t* c) { return c->emulated ? c->world : 1; }
 
+cudaEvent_t take_event(fsdp_comm_t* c) {
+  if (!c->spare.empty()) {
+    cudaEvent_t e = c->spare.back();
+    c->spare.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// enter barrier -> data kernel (signal-only) -> exit barrier, one epoch.
+// Only the 1-CTA barrier kernels ever spin.
+template <typename K>
+int launch_split(fsdp_comm_t* c, int kind, K kernel, CollParams& p, int grid, int threads,
+                 size_t smem, cudaStream_t s) {
+  p.split = 1;
+  p.data_ctas = grid;
+  if (int rc = launch(c, coll_enter_kernel, p, 1, 32, s)) return rc;
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (c->timing) {
+    a = take_event(c);
+    b = take_event(c);
+    FSDP_CUDA(cudaEventRecord(a, s));
+  }
+  void* args[] = {(void*)&p};
+  if (c->emulated) {
+    FSDP_CUDA(cudaLaunchCooperativeKernel((void*)kernel, dim3(grid, c->world), dim3(threads), args, smem, s));
+  } else {
+    FSDP_CUDA(cudaLaunchKernel((void*)kernel, dim3(grid), dim3(threads), args, smem, s));
+  }
+  FSDP_LAUNCHED();
+  if (c->timing) {
+    FSDP_CUDA(cudaEventRecord(b, s));
+    c->timed[kind].emplace_back(a, b);
+  }
+  return launch(c, coll_exit_kernel, p, 1, 256, s);
+}
+
 }  // namespace
+
+extern "C" int fsdp_comm_set_mode(fsdp_comm_t* c, int split, int timing) {
+  if (!c) return fail(FSDP_E_INVALID, "null communicator");
+  c->split = split != 0;
+  c->timing = timing != 0;
+  return 0;
+}
+
+extern "C" int fsdp_comm_timing_drain(fsdp_comm_t* c, int kind, float* ms_out, int max_n,
+                                      int* count) {
+  if (!c || kind < 0 || kind >= FSDP_NUM_KINDS || !count) return fail(FSDP_E_INVALID, "bad args");
+  auto& v = c->timed[kind];
+  int k = 0;
+  for (auto& pr : v) {
+    float ms = 0.f;
+    FSDP_CUDA(cudaEventSynchronize(pr.second));
+    FSDP_CUDA(cudaEventElapsedTime(&ms, pr.first, pr.second));
+    if (ms_out && k < max_n) ms_out[k] = ms;
+    ++k;
+    c->spare.push_back(pr.first);
+    c->spare.push_back(pr.second);
+  }
+  v.clear();
+  *count = k;
+  return 0;
+}
 
 extern "C" int64_t fsdp_comm_reserved_bytes(void) { return kReserved; }
 
@@ -726,7 +851,7 @@ extern "C" int fsdp_comm_create(int rank, int world, int64_t pool_bytes, int max
   if (!out) return fail(FSDP_E_INVALID, "null out");
   if (world < 1 || world > FSDP_MAX_RANKS || rank < 0 || rank >= world)
     return fail(FSDP_E_INVALID, "rank/world out of range (world <= 8)");
-  if (max_ctas < 1 || max_ctas > FSDP_MAX_CTAS) return fail(FSDP_E_INVALID, "max_ctas out of range");
+  if (max_ctas < 1 || max_ctas > FSDP_MAX_CTAS - 1) return fail(FSDP_E_INVALID, "max_ctas out of range (1..159)");
   if (pool_bytes < kReserved) pool_bytes = kReserved;
   pool_bytes = (pool_bytes + 4095) / 4096 * 4096;
   fsdp_comm_t* c = new fsdp_comm_t();
@@ -747,7 +872,7 @@ extern "C" int fsdp_comm_create_emulated(int world, int64_t pool_bytes, int max_
                                          fsdp_comm_t** out) {
   if (!out) return fail(FSDP_E_INVALID, "null out");
   if (world < 1 || world > FSDP_MAX_RANKS) return fail(FSDP_E_INVALID, "world out of range");
-  if (max_ctas < 1 || max_ctas > FSDP_MAX_CTAS) return fail(FSDP_E_INVALID, "max_ctas out of range");
+  if (max_ctas < 1 || max_ctas > FSDP_MAX_CTAS - 1) return fail(FSDP_E_INVALID, "max_ctas out of range (1..159)");
   if (pool_bytes < kReserved) pool_bytes = kReserved;
   pool_bytes = (pool_bytes + 4095) / 4096 * 4096;
   fsdp_comm_t* c = new fsdp_comm_t();
@@ -831,6 +956,9 @@ extern "C" int fsdp_comm_destroy(fsdp_comm_t* c) {
   if (!c->emulated)
     for (int r = 0; r < c->world; ++r)
       if (r != c->rank && c->bases[r]) cudaIpcCloseMemHandle(c->bases[r]);
+  for (auto& v : c->timed)
+    for (auto& pr : v) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
+  for (auto e : c->spare) cudaEventDestroy(e);
   cudaFree(c->pool);
   delete c;
   return 0;
@@ -858,6 +986,14 @@ extern "C" int fsdp_allgather(fsdp_comm_t* c, int channel, int gsize, int gstrid
   p.off_a = dst_off;
   const int grid = grid_for(c, n);
   cudaStream_t s = (cudaStream_t)stream;
+  if (c->split) {
+    void* k = src_dtype == FSDP_F32
+                  ? (dst_dtype == FSDP_BF16 ? (void*)allgather_kernel<float, __nv_bfloat16>
+                                            : (void*)allgather_kernel<float, float>)
+                  : (dst_dtype == FSDP_BF16 ? (void*)allgather_kernel<__nv_bfloat16, __nv_bfloat16>
+                                            : (void*)allgather_kernel<__nv_bfloat16, float>);
+    return launch_split(c, FSDP_KIND_AG, k, p, grid, kCommThreads, 0, s);
+  }
   if (src_dtype == FSDP_F32 && dst_dtype == FSDP_BF16)
     return launch(c, allgather_kernel<float, __nv_bfloat16>, p, grid, kCommThreads, s);
   if (src_dtype == FSDP_F32 && dst_dtype == FSDP_F32)
@@ -908,7 +1044,10 @@ extern "C" int fsdp_reduce_scatter_pull(fsdp_comm_t* c, int channel, int gsize, 
   const int mw = gsize <= 2 ? 2 : (gsize <= 4 ? 4 : 8);
   const int u = std::max(1, (16 / mw) / (is / 2));
   const int grid = std::max(1, std::min<int>(grid_for(c, n * 4 / u), c->max_ctas));
-#define RSP(T, W) launch(c, reduce_scatter_pull_kernel<T, W>, p, grid, kCommThreads, s)
+#define RSP(T, W)                                                                        \
+  (c->split ? launch_split(c, FSDP_KIND_RS, (void*)reduce_scatter_pull_kernel<T, W>, p, grid, \
+                           kCommThreads, 0, s)                                           \
+            : launch(c, reduce_scatter_pull_kernel<T, W>, p, grid, kCommThreads, s))
   if (src_dtype == FSDP_BF16) {
     if (mw == 2) return RSP(__nv_bfloat16, 2);
     if (mw == 4) return RSP(__nv_bfloat16, 4);

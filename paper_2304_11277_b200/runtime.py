@@ -413,10 +413,22 @@ class FSDPRuntime:
             nb = [x for _, _, x in v]
             out[k] = {"count": len(ms), "total_ms": sum(ms), "mean_ms": sum(ms) / max(1, len(ms)),
                       "bytes_total": sum(nb)}
+        if self.comm is not None and self.profile:
+            # the data kernels alone (the 1-CTA enter/exit barrier kernels
+            # around them absorb waiting for late peers)
+            for name, kind in (("allgather", self.comm.KIND_AG), ("reduce_scatter", self.comm.KIND_RS)):
+                d = self.comm.timing_drain(kind)
+                if name in out and d:
+                    out[name]["data_mean_ms"] = sum(d) / len(d)
+                    out[name]["data_total_ms"] = sum(d)
         return out
 
     def reset_timers(self) -> None:
         self.timers = {}
+        if self.comm is not None:
+            self.comm.set_mode(split=True, timing=self.profile)
+            for kind in (self.comm.KIND_AG, self.comm.KIND_RS, self.comm.KIND_AR):
+                self.comm.timing_drain(kind)
 
     # --------------------------------------------------- materialisation ---
     def _group_ag(self):

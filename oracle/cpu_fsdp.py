@@ -77,9 +77,15 @@ class CPUFSDP:
                 m._parameters[pname] = torch.nn.Parameter(t)
 
     def step(self, batches_per_rank) -> float:
-        """One optimizer step; batches_per_rank[r] = (x, y) torch CPU tensors."""
-        W = self.plan.world_size
-        flat_grads = [[None] * len(self.layouts) for _ in range(W)]
+        """One optimizer step; batches_per_rank[r] = (x, y) torch CPU tensors.
+
+        The W-rank reduction is accumulated while the simulated ranks run, in
+        exactly the fabric's order (collectives.py:273-297 ascending within
+        each sharded group, engine.py:899-917 ascending across groups), so
+        only one partial sum per group is resident instead of W gradients."""
+        W, F = self.plan.world_size, self.plan.shard_factor
+        nu = len(self.layouts)
+        partial = {}                       # (group index, unit) -> running fp32 sum
         losses = []
         for r in range(W):
             self._install(r)
@@ -88,16 +94,23 @@ class CPUFSDP:
             loss = self.model(x, y)
             loss.backward()
             losses.append(float(loss.detach()))
-            grads = {n: (p.grad.numpy() if p.grad is not None else None)
-                     for n, p in self.model.named_parameters()}
+            grads = {n: p.grad.numpy() for n, p in self.model.named_parameters()
+                     if p.grad is not None}
+            gi = r // F
             for u, lay in enumerate(self.layouts):
-                flat_grads[r][u] = sp.writeback_grad(lay, {k: v for k, v in grads.items()
-                                                           if v is not None}, np.float32)[0]
+                flat = sp.writeback_grad(lay, grads, np.float32)[0]
+                key = (gi, u)
+                partial[key] = (np.zeros_like(flat) if key not in partial else partial[key]) + flat
         for u, lay in enumerate(self.layouts):
-            acc = sp.reduce_unit([flat_grads[r][u] for r in range(W)], self.plan,
-                                 reduce_dtype=np.float32, full_dtype=np.float32, mean=True)
+            total = None
+            for gi in range(W // F):                       # ascending across groups
+                p = partial.pop((gi, u))
+                total = (np.zeros_like(p) + p) if total is None else total + p
+            red = total / np.float32(W)
             for r in range(W):
-                sp.adam_step(self.shards[r][u], acc[r], self.states[r][u], lr=self.lr)
+                k = sp.shard_index(self.plan, r)
+                g = red[k * lay.shard_numel:(k + 1) * lay.shard_numel]
+                sp.adam_step(self.shards[r][u], np.zeros_like(g) + g, self.states[r][u], lr=self.lr)
         return float(np.mean(losses))
 
 

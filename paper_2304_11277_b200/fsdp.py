@@ -137,7 +137,8 @@ class FullyShardedDataParallel(nn.Module):
                  limit_all_gathers: bool = True, use_orig_params: bool = False,
                  ignored_states=None, device_mesh=None, *, hybrid_shard_size: int | None = None,
                  comm_backend: str = "ipc", num_slots: int | None = None, ag_ctas: int = 32,
-                 optimizer: str = "adam", lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-8):
+                 optimizer: str = "adam", lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-8,
+                 optimizer_in_backward: bool = False):
         super().__init__()
         if cpu_offload is not None and cpu_offload.offload_params:
             raise NotImplementedError("CPU offload is out of scope for the B200 runtime")
@@ -169,7 +170,8 @@ class FullyShardedDataParallel(nn.Module):
                             rate_limit=2 if limit_all_gathers else None,
                             keep_outermost_unsharded=True, accumulation=ACCUM_OFF,
                             comm_backend=comm_backend, num_slots=num_slots, ag_ctas=ag_ctas,
-                            optimizer=optimizer, lr=lr, betas=tuple(betas), eps=eps)
+                            optimizer=optimizer, lr=lr, betas=tuple(betas), eps=eps,
+                            optimizer_in_backward=optimizer_in_backward)
         self.module = module
         self.plan = plan
         self.rank = rank

@@ -87,6 +87,11 @@ class RuntimeConfig:
     lr: float = 1e-3
     betas: tuple = (0.9, 0.999)
     eps: float = 1e-8
+    # step each unit's shard as soon as its final reduction is issued (on the
+    # reduce stream, overlapping the rest of backward).  Only valid when every
+    # backward is followed by an optimizer step and no loss scaler needs a
+    # global verdict first; identical arithmetic to the end-of-step launch.
+    optimizer_in_backward: bool = False
 
     def __post_init__(self):
         if self.reshard_after_forward not in (RAF, NRAF):
@@ -136,6 +141,7 @@ class UnitState:
         self.accum_unsharded: torch.Tensor | None = None
         self.reduces_this_step = 0
         self.bwd_done = False
+        self.stepped = False           # optimizer already applied this step (in backward)
 
 
 class SlotPool:
@@ -581,7 +587,27 @@ class FSDPRuntime:
     def begin_step(self) -> None:
         for u in self.units:
             u.reduces_this_step = 0
+            u.stepped = False
         self.micro_index = 0
+
+    def _step_in_backward(self) -> bool:
+        return (self.cfg.optimizer_in_backward and self.final_micro and not self.defer_reduce)
+
+    def _step_unit(self, uid: int, stream: torch.cuda.Stream) -> None:
+        """Optimizer on one unit's shard slice (same arithmetic as the arena
+        launch, t = the step about to be taken)."""
+        u = self.units[uid]
+        cfg = self.cfg
+        n = u.layout.shard_numel
+        with self.timed(cfg.optimizer + "_step", stream, n * (28 if cfg.optimizer == "adam" else 12)
+                        + (2 * n if u.low is not None else 0)):
+            if cfg.optimizer == "adam":
+                kernels.adam_step(u.master, u.grad, u.exp_avg, u.exp_avg_sq, lr=cfg.lr,
+                                  betas=cfg.betas, eps=cfg.eps, t=self.adam_steps + 1,
+                                  p_lowp=u.low, stream=stream)
+            else:
+                kernels.sgd_step(u.master, u.grad, lr=cfg.lr, p_lowp=u.low, stream=stream)
+        u.stepped = True
 
     def begin_micro(self, final: bool) -> None:
         self.final_micro = final
@@ -671,6 +697,11 @@ class FSDPRuntime:
             u.grad_pending -= 1
             self._finalize(uid, reduced=True)
             self.events.append((self.step_count, "reduce_issue", uid))
+            if self._step_in_backward():
+                ready = torch.cuda.Event()
+                ready.record(self.compute_stream)
+                self.rs_stream.wait_event(ready)
+                self._step_unit(uid, self.rs_stream)
             self.release_use(uid, "backward", None)
             return
         if first and self.gslot_offs and u.grad_pending == 1 and not self.defer_reduce \
@@ -793,6 +824,8 @@ class FSDPRuntime:
                 ev = torch.cuda.Event()
                 ev.record(self.rs_stream)
                 self.gslot_free[gslot] = ev
+            if self._step_in_backward():
+                self._step_unit(uid, self.rs_stream)   # right behind its reduction
         self.bytes_rs += grad.numel() * (2 if self.payload_dtype == torch.bfloat16 else 4)
         u.reduces_this_step += 1
 
@@ -859,6 +892,19 @@ class FSDPRuntime:
             skip = self.found_inf_world
         self.step_count += 1
         cfg = self.cfg
+        if skip is None and self.units and all(u.stepped for u in self.units):
+            # every shard was already stepped in backward, right behind its
+            # reduction on the reduce stream
+            self.adam_steps += 1
+            ev = torch.cuda.Event()
+            ev.record(self.rs_stream)
+            self.compute_stream.wait_event(ev)
+            self.opt_done = ev
+            self.events.append((self.step_count - 1, "opt_step", None))
+            return
+        if any(u.stepped for u in self.units):
+            raise EngineError("optimizer_in_backward stepped only part of the units; "
+                              "every backward must be followed by an optimizer step")
         n = self.master.numel()
         if cfg.optimizer == "adam":
             nb = n * (28 + (2 if self.low is not None else 0))

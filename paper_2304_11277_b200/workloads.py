@@ -41,9 +41,11 @@ class GPTConfig:
     def n_params(self) -> int:
         return self.layers * self.block_params + self.root_params
 
-    def flops_per_token(self) -> float:
-        """6·N_nonembed + 12·L·d·S + 6·V·d (fwd+bwd)."""
-        return (6.0 * self.layers * self.block_params + 12.0 * self.layers * self.d * self.seq
+    def flops_per_token(self, seq: int | None = None) -> float:
+        """6·N_nonembed + 12·L·d·S + 6·V·d (fwd+bwd); `seq`
+        overrides S for samples run at a shorter sequence length."""
+        s = self.seq if seq is None else seq
+        return (6.0 * self.layers * self.block_params + 12.0 * self.layers * self.d * s
                 + 6.0 * self.vocab * self.d)
 
 

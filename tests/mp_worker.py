@@ -89,7 +89,7 @@ def raw_collectives(rank, world, results):
     results["raw_collectives"] = "bit-exact"
 
 
-def fsdp_step_parity(rank, world, strategy, hybrid, results, backend="ipc"):
+def fsdp_step_parity(rank, world, strategy, hybrid, results, backend="ipc", opt_in_bwd=False):
     from paper_2304_11277_b200 import kernels  # noqa: F401
     from paper_2304_11277_b200.fsdp import (FullyShardedDataParallel, MixedPrecision,
                                             ModuleWrapPolicy, ShardingStrategy)
@@ -99,7 +99,8 @@ def fsdp_step_parity(rank, world, strategy, hybrid, results, backend="ipc"):
                                     sharding_strategy=ShardingStrategy[strategy],
                                     auto_wrap_policy=ModuleWrapPolicy({Block}),
                                     mixed_precision=MixedPrecision(param_dtype=torch.bfloat16),
-                                    hybrid_shard_size=hybrid, comm_backend=backend, lr=1e-3)
+                                    hybrid_shard_size=hybrid, comm_backend=backend, lr=1e-3,
+                                    optimizer_in_backward=opt_in_bwd)
     plan = fsdp.plan
     ref = init_gpt_(GPT(cfg), seed=0).cuda().to(torch.bfloat16)
     x, y = synthetic_batch(cfg, 2, seed=100 + rank, device="cuda")
@@ -107,9 +108,12 @@ def fsdp_step_parity(rank, world, strategy, hybrid, results, backend="ipc"):
     loss.backward()
     lref = ref(x, y)
     lref.backward()
-    key = f"{strategy}{'' if hybrid is None else hybrid}/{backend}"
-    before = [u.master.clone() for u in fsdp.rt.units]
+    key = f"{strategy}{'' if hybrid is None else hybrid}/{backend}{'/opt-in-bwd' if opt_in_bwd else ''}"
     torch.cuda.synchronize()
+    # initial shards from the oracle (flatten + shard of the same init)
+    vals = {k: v.detach().float().cpu().numpy() for k, v in init_gpt_(GPT(cfg), seed=0).named_parameters()}
+    k_idx = plan.shard_index(rank)
+    before = [sp.shard(sp.flatten(vals, lay, np.float32), lay, k_idx) for lay in fsdp.layouts]
     if backend == "ipc":
         check(loss.item() == lref.item(), f"{key}: loss differs from the unwrapped model")
         g = {n: p.grad.float().cpu().numpy() for n, p in ref.named_parameters()}
@@ -123,7 +127,7 @@ def fsdp_step_parity(rank, world, strategy, hybrid, results, backend="ipc"):
     fsdp.optimizer().step()
     torch.cuda.synchronize()
     for b, u in zip(before, fsdp.rt.units):
-        p = b.cpu().numpy().copy()
+        p = b.copy()
         sp.adam_step(p, u.grad.cpu().numpy(), sp.adam_init(p.size, np.float32), lr=1e-3)
         check(u.master.cpu().numpy().tobytes() == p.tobytes(), f"{key}: Adam shard")
     # step 2: re-gather the updated shards, compare against an unwrapped copy
@@ -301,6 +305,9 @@ def main():
             cases.append(("HYBRID_SHARD", 2))
         for strat, hyb in cases:
             fsdp_step_parity(rank, world, strat, hyb, results)
+        fsdp_step_parity(rank, world, "FULL_SHARD", None, results, opt_in_bwd=True)
+        if world == 4:
+            fsdp_step_parity(rank, world, "HYBRID_SHARD", 2, results, opt_in_bwd=True)
         fsdp_step_parity(rank, world, "FULL_SHARD", None, results, backend="nccl")
     except Exception:
         ok = False

@@ -83,3 +83,21 @@ def test_fp32_no_mixed_precision_step():
     m.optimizer().step()
     torch.cuda.synchronize()
     assert np.isfinite(l.item())
+
+
+def test_optimizer_in_backward_identical():
+    """Per-unit Adam on the reduce stream during backward == end-of-step launch."""
+    from paper_2304_11277_b200.workloads import synthetic_batch
+    cfg, a, _ = build()
+    _, b, _ = build(optimizer_in_backward=True)
+    for s in range(2):
+        x, y = synthetic_batch(cfg, 2, seed=40 + s, device="cuda")
+        for m in (a, b):
+            l = m(x, y)
+            l.backward()
+            m.optimizer(lr=1e-3).step()
+    torch.cuda.synchronize()
+    for ua, ub in zip(a.rt.units, b.rt.units):
+        assert torch.equal(ua.master, ub.master)
+        assert torch.equal(ua.exp_avg_sq, ub.exp_avg_sq)
+        assert torch.equal(ua.low, ub.low)

@@ -50,6 +50,12 @@ def parse():
     ap.add_argument("--strategy", default="FULL_SHARD")
     ap.add_argument("--hybrid-shard-size", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-limiter", action="store_true", help="limit_all_gathers=False")
+    ap.add_argument("--forward-prefetch", action="store_true")
+    ap.add_argument("--ctas", type=int, default=32, help="CTAs of the all-gather data kernel")
+    ap.add_argument("--rs-ctas", type=int, default=64, help="CTAs of the reduce-scatter data kernel")
+    ap.add_argument("--exposed", action="store_true",
+                    help="also time the step with collectives replaced by no-ops")
     ap.add_argument("--opt-in-bwd", action="store_true",
                     help="step each unit's shard in backward (measured: slower at N=1, "
                          "Adam contends for HBM with the backward kernels)")
@@ -139,33 +145,49 @@ def run_ours(args):
     from paper_2304_11277_b200 import _lib
     from paper_2304_11277_b200.fsdp import (BackwardPrefetch, FullyShardedDataParallel,
                                             MixedPrecision, ModuleWrapPolicy, ShardingStrategy)
-    from paper_2304_11277_b200.workloads import CONFIGS, GPT, Block, param_init_fn
+    from paper_2304_11277_b200.workloads import (CONFIGS, GPT, T5, T5_CONFIGS, Block,
+                                                 T5DecoderBlock, T5EncoderBlock, param_init_fn)
 
     torch.backends.cuda.matmul.allow_tf32 = True
-    cfg = CONFIGS[args.config]
     dev = torch.device("cuda", local)
     torch.manual_seed(1234)
-    with torch.device("meta"):
-        model = GPT(cfg)
-    strategy = ShardingStrategy[args.strategy]
-    fsdp = FullyShardedDataParallel(
-        model, sharding_strategy=strategy, auto_wrap_policy=ModuleWrapPolicy({Block}),
-        backward_prefetch=BackwardPrefetch.BACKWARD_PRE,
-        mixed_precision=MixedPrecision(param_dtype=torch.bfloat16, reduce_dtype=torch.bfloat16),
-        limit_all_gathers=True, param_init_fn=param_init_fn, comm_backend=args.backend,
-        hybrid_shard_size=args.hybrid_shard_size, lr=1e-4,
-        optimizer_in_backward=args.opt_in_bwd)
-    opt = fsdp.optimizer()
-    rt = fsdp.rt
     B = args.micro
     g = torch.Generator(device="cpu").manual_seed(1 + rank)
-    x_host = torch.randint(0, cfg.vocab, (B, cfg.seq), generator=g).pin_memory()
-    y_host = torch.randint(0, cfg.vocab, (B, cfg.seq), generator=g).pin_memory()
-    x, y = x_host.to(dev), y_host.to(dev)
+    if args.config in T5_CONFIGS:
+        cfg = T5_CONFIGS[args.config]
+        with torch.device("meta"):
+            model = T5(cfg)
+        wrap = {T5EncoderBlock, T5DecoderBlock}
+        host = (torch.randint(0, cfg.vocab, (B, cfg.enc_seq), generator=g).pin_memory(),
+                torch.randint(0, cfg.vocab, (B, cfg.dec_seq), generator=g).pin_memory(),
+                torch.randint(0, cfg.vocab, (B, cfg.dec_seq), generator=g).pin_memory())
+        flops_step = cfg.flops_per_sample() * B          # per GPU
+        seq_len = cfg.enc_seq
+    else:
+        cfg = CONFIGS[args.config]
+        with torch.device("meta"):
+            model = GPT(cfg)
+        wrap = {Block}
+        host = (torch.randint(0, cfg.vocab, (B, cfg.seq), generator=g).pin_memory(),
+                torch.randint(0, cfg.vocab, (B, cfg.seq), generator=g).pin_memory())
+        flops_step = cfg.flops_per_token() * B * cfg.seq  # per GPU
+        seq_len = cfg.seq
+    strategy = ShardingStrategy[args.strategy]
+    fsdp = FullyShardedDataParallel(
+        model, sharding_strategy=strategy, auto_wrap_policy=ModuleWrapPolicy(wrap),
+        backward_prefetch=BackwardPrefetch.BACKWARD_PRE,
+        mixed_precision=MixedPrecision(param_dtype=torch.bfloat16, reduce_dtype=torch.bfloat16),
+        limit_all_gathers=not args.no_limiter, param_init_fn=param_init_fn,
+        comm_backend=args.backend, hybrid_shard_size=args.hybrid_shard_size, lr=1e-4,
+        optimizer_in_backward=args.opt_in_bwd, forward_prefetch=args.forward_prefetch,
+        ag_ctas=args.ctas, rs_ctas=args.rs_ctas)
+    opt = fsdp.optimizer()
+    rt = fsdp.rt
+    dev_inputs = tuple(h.to(dev) for h in host)
     compute = torch.cuda.current_stream()
 
-    def step(xx, yy):
-        loss = fsdp(xx, yy)
+    def step(*inputs):
+        loss = fsdp(*inputs)
         loss.backward()
         opt.step()
         return loss
@@ -177,7 +199,7 @@ def run_ours(args):
         torch.cuda.synchronize()
 
     for _ in range(args.warmup):
-        step(x, y)
+        step(*dev_inputs)
     barrier()
     sampler = ClockSampler(local)
     if rank == 0:
@@ -189,7 +211,7 @@ def run_ours(args):
     barrier()
     t0.record(compute)
     for _ in range(args.steps):
-        loss = step(x, y)
+        loss = step(*dev_inputs)
     t1.record(compute)
     barrier()
     launches = _lib.launch_count() - n_launch0
@@ -203,20 +225,33 @@ def run_ours(args):
     te0.record(compute)
     losses = []
     for _ in range(args.steps):
-        xx = x_host.to(dev, non_blocking=True)
-        yy = y_host.to(dev, non_blocking=True)
-        l = step(xx, yy)
+        inputs = tuple(h.to(dev, non_blocking=True) for h in host)
+        l = step(*inputs)
         losses.append(l.item())
     te1.record(compute)
     barrier()
     ms_e2e = te0.elapsed_time(te1) / args.steps
     clocks = sampler.stop() if rank == 0 else None
-    tmax = torch.tensor([ms, ms_e2e], device=dev)
+    ms_nocomm = 0.0
+    if args.exposed and world > 1:
+        # same step with every collective replaced by a no-op (values become
+        # garbage; timing only): exposed comm = step - step_without_comm
+        rt.cfg.fake_comm = True
+        for _ in range(2):
+            step(*dev_inputs)
+        barrier()
+        tf0, tf1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        tf0.record(compute)
+        for _ in range(args.steps):
+            step(*dev_inputs)
+        tf1.record(compute)
+        barrier()
+        ms_nocomm = tf0.elapsed_time(tf1) / args.steps
+        rt.cfg.fake_comm = False
+    tmax = torch.tensor([ms, ms_e2e, ms_nocomm], device=dev)
     if world > 1:
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-    ms, ms_e2e = tmax.tolist()
-    tokens = B * cfg.seq
-    flops_step = cfg.flops_per_token() * tokens          # per GPU
+    ms, ms_e2e, ms_nocomm = tmax.tolist()
     tflops_gpu = flops_step / (ms * 1e-3) / 1e12
     value = tflops_gpu * world
     e2e_value = flops_step / (ms_e2e * 1e-3) / 1e12 * world
@@ -265,21 +300,27 @@ def run_ours(args):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform token ids, meta-init weights)",
-            "config": {"workload": f"{cfg.name} {args.strategy} bf16 MixedPrecision, block auto-wrap, "
-                                   f"BACKWARD_PRE, limit_all_gathers",
-                       "model": cfg.name, "global_batch": B * world, "seq_len": cfg.seq,
+            "config": {"workload": f"{cfg.name} {args.strategy}"
+                                   f"{'' if args.hybrid_shard_size is None else ' F=%d' % args.hybrid_shard_size}"
+                                   f" bf16 MixedPrecision, block auto-wrap, BACKWARD_PRE"
+                                   f"{'' if args.no_limiter else ', limit_all_gathers'}",
+                       "model": cfg.name, "global_batch": B * world, "seq_len": seq_len,
                        "parallelism": f"fsdp{world}" if world > 1 else "fsdp1 (NO_SHARD-equivalent)",
                        "comm_backend": args.backend, "l2": "inputs > L2 (weights+state >20 GB)"},
             "tflops_per_gpu": round(tflops_gpu, 2),
             "roofline": roof, "roofline_step": step_roof, "kernels": kern_share,
             "e2e": {"value": round(e2e_value, 2), "unit": "TFLOP/s (model, whole job)",
-                    "h2d_bytes_per_step": int(x_host.numel() * 8 * 2),
+                    "h2d_bytes_per_step": int(sum(h.numel() * h.element_size() for h in host)),
                     "d2h_bytes_per_step": 4, "ms_per_step": round(ms_e2e, 3)},
             "gpu_launches": int(launches), "clocks": clocks, "loss": round(losses[-1], 4),
             "peak_mem_gb": round(torch.cuda.max_memory_allocated() / 1e9, 2),
+            **({"exposed_comm": {"ms_per_step_without_comm": round(ms_nocomm, 3),
+                                 "exposed_ms": round(ms - ms_nocomm, 3),
+                                 "frac_of_step": round((ms - ms_nocomm) / ms, 4)}}
+               if ms_nocomm > 0 else {}),
         }
         out.update(comm_bw)
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config in CONFIGS:
         out["cpu_baseline"] = cpu_baseline(cfg, args.cpu_tokens, world=1)
     if world > 1:
         dist.barrier()

@@ -145,6 +145,9 @@ int fsdp_comm_set_timeout_ms(fsdp_comm_t* c, int64_t ms);
  * kernel, read back (and recycled) by fsdp_comm_timing_drain. */
 enum { FSDP_KIND_AG = 0, FSDP_KIND_RS = 1, FSDP_KIND_AR = 2, FSDP_NUM_KINDS = 3 };
 int fsdp_comm_set_mode(fsdp_comm_t* c, int split, int timing);
+/* Grid cap for the data kernels of one collective kind (0 = max_ctas).  Every
+ * member of a group must use the same value (per-CTA flags pair by index). */
+int fsdp_comm_set_ctas(fsdp_comm_t* c, int kind, int ctas);
 /* Synchronises on the recorded events of `kind`; writes up to max_n
  * durations (ms) and the total count. */
 int fsdp_comm_timing_drain(fsdp_comm_t* c, int kind, float* ms_out, int max_n, int* count);

@@ -117,6 +117,10 @@ class DeviceComm:
         kernels (default); timing: CUDA events around every data kernel."""
         check(lib.fsdp_comm_set_mode(self._h, int(split), int(timing)))
 
+    def set_ctas(self, kind: int, ctas: int) -> None:
+        """Grid cap of one collective kind's data kernel (same on every rank)."""
+        check(lib.fsdp_comm_set_ctas(self._h, kind, int(ctas)))
+
     def timing_drain(self, kind: int) -> list[float]:
         """Durations (ms) of the data kernels of `kind` since the last drain."""
         buf = (C.c_float * 65536)()

@@ -718,6 +718,7 @@ struct fsdp_comm {
   bool opened[FSDP_MAX_RANKS] = {};
   uint32_t epoch[FSDP_NUM_CH] = {};
   int64_t timeout_ns = 20LL * 1000 * 1000 * 1000;
+  int kind_ctas[FSDP_NUM_KINDS] = {};         // per-kind grid caps (0: max_ctas)
   bool split = true;                          // 1-CTA enter/exit kernels around data kernels
   bool timing = false;                        // record events around every data kernel
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed[FSDP_NUM_KINDS];
@@ -755,9 +756,10 @@ void fill_common(fsdp_comm_t* c, CollParams& p, int channel, int gsize, int gstr
   p.timeout_ns = c->timeout_ns;
 }
 
-int grid_for(fsdp_comm_t* c, int64_t elems) {
+int grid_for(fsdp_comm_t* c, int64_t elems, int kind = -1) {
   int64_t tiles = (elems + kTileElems - 1) / kTileElems;
-  int g = (int)std::min<int64_t>(std::max<int64_t>(tiles, 1), c->max_ctas);
+  const int cap = (kind >= 0 && c->kind_ctas[kind] > 0) ? c->kind_ctas[kind] : c->max_ctas;
+  int g = (int)std::min<int64_t>(std::max<int64_t>(tiles, 1), cap);
   if (c->emulated) g = std::min(g, std::max(1, 128 / c->world));
   return g;
 }
@@ -817,6 +819,13 @@ int launch_split(fsdp_comm_t* c, int kind, K kernel, CollParams& p, int grid, in
 }
 
 }  // namespace
+
+extern "C" int fsdp_comm_set_ctas(fsdp_comm_t* c, int kind, int ctas) {
+  if (!c || kind < 0 || kind >= FSDP_NUM_KINDS || ctas < 0 || ctas > FSDP_MAX_CTAS - 1)
+    return fail(FSDP_E_INVALID, "fsdp_comm_set_ctas: bad args");
+  c->kind_ctas[kind] = ctas;
+  return 0;
+}
 
 extern "C" int fsdp_comm_set_mode(fsdp_comm_t* c, int split, int timing) {
   if (!c) return fail(FSDP_E_INVALID, "null communicator");
@@ -984,7 +993,7 @@ extern "C" int fsdp_allgather(fsdp_comm_t* c, int channel, int gsize, int gstrid
   fill_common(c, p, channel, gsize, gstride, n);
   for (int e = 0; e < nranks_args(c); ++e) p.in[e] = shards[e];
   p.off_a = dst_off;
-  const int grid = grid_for(c, n);
+  const int grid = grid_for(c, n, FSDP_KIND_AG);
   cudaStream_t s = (cudaStream_t)stream;
   if (c->split) {
     void* k = src_dtype == FSDP_F32
@@ -1043,7 +1052,7 @@ extern "C" int fsdp_reduce_scatter_pull(fsdp_comm_t* c, int channel, int gsize, 
   cudaStream_t s = (cudaStream_t)stream;
   const int mw = gsize <= 2 ? 2 : (gsize <= 4 ? 4 : 8);
   const int u = std::max(1, (16 / mw) / (is / 2));
-  const int grid = std::max(1, std::min<int>(grid_for(c, n * 4 / u), c->max_ctas));
+  const int grid = std::max(1, grid_for(c, n * 4 / u, FSDP_KIND_RS));
 #define RSP(T, W)                                                                        \
   (c->split ? launch_split(c, FSDP_KIND_RS, (void*)reduce_scatter_pull_kernel<T, W>, p, grid, \
                            kCommThreads, 0, s)                                           \

@@ -136,7 +136,7 @@ class FullyShardedDataParallel(nn.Module):
                  sync_module_states: bool = False, forward_prefetch: bool = False,
                  limit_all_gathers: bool = True, use_orig_params: bool = False,
                  ignored_states=None, device_mesh=None, *, hybrid_shard_size: int | None = None,
-                 comm_backend: str = "ipc", num_slots: int | None = None, ag_ctas: int = 32,
+                 comm_backend: str = "ipc", num_slots: int | None = None, ag_ctas: int = 32, rs_ctas: int = 64,
                  optimizer: str = "adam", lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-8,
                  optimizer_in_backward: bool = False):
         super().__init__()
@@ -169,7 +169,7 @@ class FullyShardedDataParallel(nn.Module):
                             backward_prefetch=bp, forward_prefetch=forward_prefetch,
                             rate_limit=2 if limit_all_gathers else None,
                             keep_outermost_unsharded=True, accumulation=ACCUM_OFF,
-                            comm_backend=comm_backend, num_slots=num_slots, ag_ctas=ag_ctas,
+                            comm_backend=comm_backend, num_slots=num_slots, ag_ctas=ag_ctas, rs_ctas=rs_ctas,
                             optimizer=optimizer, lr=lr, betas=tuple(betas), eps=eps,
                             optimizer_in_backward=optimizer_in_backward)
         self.module = module
@@ -224,7 +224,7 @@ class FullyShardedDataParallel(nn.Module):
         comm = None
         pgs = {}
         if world > 1 and comm_backend == "ipc":
-            comm = DeviceComm.create(FSDPRuntime.pool_bytes_for(layouts, plan, cfg), max_ctas=ag_ctas,
+            comm = DeviceComm.create(FSDPRuntime.pool_bytes_for(layouts, plan, cfg), max_ctas=max(ag_ctas, rs_ctas),
                                      group=process_group)
         elif world > 1:
             pgs = _nccl_groups(plan, rank)

@@ -82,7 +82,8 @@ class RuntimeConfig:
     gradient_predivide: float = 1.0
     comm_backend: str = "ipc"            # "ipc" (this library) | "nccl" (comparison path)
     num_slots: int | None = None
-    ag_ctas: int = 32
+    ag_ctas: int = 32                    # grid cap of the all-gather data kernel
+    rs_ctas: int = 64                    # grid cap of the reduce-scatter data kernel
     optimizer: str = "adam"
     lr: float = 1e-3
     betas: tuple = (0.9, 0.999)
@@ -92,6 +93,9 @@ class RuntimeConfig:
     # backward is followed by an optimizer step and no loss scaler needs a
     # global verdict first; identical arithmetic to the end-of-step launch.
     optimizer_in_backward: bool = False
+    # measurement only (bench.py --exposed): skip every collective, keep all
+    # stream/event plumbing — the step time without communication
+    fake_comm: bool = False
 
     def __post_init__(self):
         if self.reshard_after_forward not in (RAF, NRAF):
@@ -241,6 +245,9 @@ class FSDPRuntime:
         self.device = device or torch.device("cuda", torch.cuda.current_device())
         self.units = [UnitState(l) for l in layouts]
         self.comm = comm
+        if comm is not None:
+            comm.set_ctas(comm.KIND_AG, config.ag_ctas)
+            comm.set_ctas(comm.KIND_RS, config.rs_ctas)
         self.pgs = process_groups or {}
         W, F = plan.world_size, plan.shard_factor
         if W > 1 and config.comm_backend == "ipc" and comm is None:
@@ -455,7 +462,9 @@ class FSDPRuntime:
                 self.ag_stream.wait_event(free_ev)
             if self.opt_done is not None:
                 self.ag_stream.wait_event(self.opt_done)
-            if self.cfg.comm_backend == "ipc":
+            if self.cfg.fake_comm:
+                pass
+            elif self.cfg.comm_backend == "ipc":
                 with self.timed("allgather", self.ag_stream,
                                 lay.psi * (2 if self.cfg.mixed else 4)):
                     self.comm.all_gather(self._group_ag(), [src], self.slots.offsets[slot],
@@ -789,7 +798,9 @@ class FSDPRuntime:
                 payload = torch.empty(grad.numel(), dtype=self.payload_dtype, device=self.device)
                 kernels.cast(grad, payload, stream=self.rs_stream)
             grad.record_stream(self.rs_stream)
-            if W == 1:
+            if self.cfg.fake_comm and W > 1:
+                pass
+            elif W == 1:
                 # world of one: the "reduction" is the fp32 cast (+ accumulate)
                 with self.timed("reduce_w1", self.rs_stream, n * (payload.element_size() + 4)):
                     kernels.flatten([payload], [0], u.grad, accumulate=accumulate,

@@ -121,6 +121,141 @@ class GPT(nn.Module):
         return F.cross_entropy(logits.float().view(-1, logits.size(-1)), targets.view(-1))
 
 
+@dataclass(frozen=True)
+class T5Config:
+    """T5-style encoder-decoder (T5-11B, d=1024, d_ff=65536,
+    128 heads x 128, 24+24 layers, V=32128).  Units: root (shared embedding
+    + final norms), every encoder block, every decoder block (SURVEY §8:
+    encoder psi 201,328,640, decoder psi 268,438,528)."""
+    name: str
+    d: int
+    d_ff: int
+    heads: int
+    d_kv: int
+    enc_layers: int
+    dec_layers: int
+    vocab: int
+    enc_seq: int
+    dec_seq: int
+
+    @property
+    def inner(self) -> int:
+        return self.heads * self.d_kv
+
+    @property
+    def enc_block_params(self) -> int:
+        return 4 * self.d * self.inner + 2 * self.d * self.d_ff + 2 * self.d
+
+    @property
+    def dec_block_params(self) -> int:
+        return 8 * self.d * self.inner + 2 * self.d * self.d_ff + 3 * self.d
+
+    @property
+    def n_params(self) -> int:
+        return (self.enc_layers * self.enc_block_params + self.dec_layers * self.dec_block_params
+                + self.vocab * self.d + 2 * self.d)
+
+    def flops_per_sample(self) -> float:
+        """fwd+bwd model flops of one (enc_seq, dec_seq) pair: 6 x params x tokens
+        for the blocks, 12 x layers x inner x S per token for self/cross
+        attention scores, 6 x V x d per decoder token for the tied head."""
+        se, sd, inn = self.enc_seq, self.dec_seq, self.inner
+        enc = se * (6.0 * self.enc_layers * self.enc_block_params + 12.0 * self.enc_layers * inn * se)
+        dec = sd * (6.0 * self.dec_layers * self.dec_block_params + 12.0 * self.dec_layers * inn * sd
+                    + 12.0 * self.dec_layers * inn * se + 6.0 * self.vocab * self.d)
+        return enc + dec
+
+
+T5_CONFIGS = {
+    "t5-11b": T5Config("t5-11b", 1024, 65536, 128, 128, 24, 24, 32128, 512, 512),
+    "t5-tiny": T5Config("t5-tiny", 64, 256, 4, 16, 2, 2, 128, 32, 32),
+}
+
+
+class T5Attention(nn.Module):
+    def __init__(self, d: int, heads: int, d_kv: int):
+        super().__init__()
+        inner = heads * d_kv
+        self.q = nn.Linear(d, inner, bias=False)
+        self.k = nn.Linear(d, inner, bias=False)
+        self.v = nn.Linear(d, inner, bias=False)
+        self.o = nn.Linear(inner, d, bias=False)
+        self.heads, self.d_kv = heads, d_kv
+
+    def forward(self, x, kv=None, causal=False):
+        b, s, _ = x.shape
+        kv = x if kv is None else kv
+        t = kv.shape[1]
+        h, dk = self.heads, self.d_kv
+        q = self.q(x).view(b, s, h, dk).transpose(1, 2)
+        k = self.k(kv).view(b, t, h, dk).transpose(1, 2)
+        v = self.v(kv).view(b, t, h, dk).transpose(1, 2)
+        y = F.scaled_dot_product_attention(q, k, v, is_causal=causal)
+        return self.o(y.transpose(1, 2).reshape(b, s, h * dk))
+
+
+class T5FFN(nn.Module):
+    def __init__(self, d: int, d_ff: int):
+        super().__init__()
+        self.wi = nn.Linear(d, d_ff, bias=False)
+        self.wo = nn.Linear(d_ff, d, bias=False)
+
+    def forward(self, x):
+        return self.wo(F.relu(self.wi(x)))
+
+
+class T5EncoderBlock(nn.Module):
+    def __init__(self, c: T5Config):
+        super().__init__()
+        self.ln_1 = nn.RMSNorm(c.d)
+        self.attn = T5Attention(c.d, c.heads, c.d_kv)
+        self.ln_2 = nn.RMSNorm(c.d)
+        self.ffn = T5FFN(c.d, c.d_ff)
+
+    def forward(self, x):
+        x = x + self.attn(self.ln_1(x))
+        return x + self.ffn(self.ln_2(x))
+
+
+class T5DecoderBlock(nn.Module):
+    def __init__(self, c: T5Config):
+        super().__init__()
+        self.ln_1 = nn.RMSNorm(c.d)
+        self.self_attn = T5Attention(c.d, c.heads, c.d_kv)
+        self.ln_2 = nn.RMSNorm(c.d)
+        self.cross_attn = T5Attention(c.d, c.heads, c.d_kv)
+        self.ln_3 = nn.RMSNorm(c.d)
+        self.ffn = T5FFN(c.d, c.d_ff)
+
+    def forward(self, x, enc):
+        x = x + self.self_attn(self.ln_1(x), causal=True)
+        x = x + self.cross_attn(self.ln_2(x), kv=enc)
+        return x + self.ffn(self.ln_3(x))
+
+
+class T5(nn.Module):
+    def __init__(self, c: T5Config):
+        super().__init__()
+        self.cfg = c
+        self.shared = nn.Embedding(c.vocab, c.d)
+        self.encoder = nn.ModuleList([T5EncoderBlock(c) for _ in range(c.enc_layers)])
+        self.enc_norm = nn.RMSNorm(c.d)
+        self.decoder = nn.ModuleList([T5DecoderBlock(c) for _ in range(c.dec_layers)])
+        self.dec_norm = nn.RMSNorm(c.d)
+
+    def forward(self, src, tgt_in, tgt_out):
+        e = self.shared(src)
+        for blk in self.encoder:
+            e = blk(e)
+        e = self.enc_norm(e)
+        x = self.shared(tgt_in)
+        for blk in self.decoder:
+            x = blk(x, e)
+        x = self.dec_norm(x) * (self.cfg.d ** -0.5)
+        logits = F.linear(x, self.shared.weight)            # tied head
+        return F.cross_entropy(logits.float().view(-1, logits.size(-1)), tgt_out.view(-1))
+
+
 def init_gpt_(model: GPT, seed: int = 0) -> GPT:
     """GPT-2 style init (normal 0.02, scaled residual projections)."""
     g = torch.Generator(device="cpu").manual_seed(seed)
@@ -144,7 +279,7 @@ def param_init_fn(module: nn.Module) -> None:
         for name, p in module.named_parameters(recurse=False):
             if name == "bias":
                 p.zero_()
-            elif isinstance(module, nn.LayerNorm):
+            elif isinstance(module, (nn.LayerNorm, nn.RMSNorm)):
                 p.fill_(1.0)
             else:
                 p.normal_(0.0, 0.02)

@@ -301,7 +301,12 @@ class FullyShardedDataParallel(nn.Module):
         rt.close_window(uid)
         if torch.is_grad_enabled():
             output = _map_tensors(lambda ts: PreBackward.apply(rt, uid, *ts), output)
-        rt.release_use(uid, "forward", 0)
+            rt.release_use(uid, "forward", 0)
+        else:
+            # no backward will follow (eval / no_grad): nothing is kept unsharded
+            rt.release_use(uid, "backward", None)
+            if uid == 0:
+                self._new_micro = True
         return output
 
     def _end_backward(self) -> None:
@@ -366,6 +371,52 @@ class FullyShardedDataParallel(nn.Module):
             for o, t in zip(lay.originals, tensors):
                 out[o.name] = t
         return out
+
+
+    def load_full_state_dict(self, sd: dict[str, torch.Tensor]) -> None:
+        """Inverse of full_state_dict: flatten each unit's original tensors and
+        keep this rank's shard (the init path, deferred_init.py:156-176);
+        the bf16 copy is refreshed.  Optimizer state is left unchanged."""
+        for uid, lay in enumerate(self.layouts):
+            if lay.psi:
+                self.rt.load_unit_values(uid, [sd[o.name] for o in lay.originals])
+        torch.cuda.synchronize()
+
+    def sharded_state_dict(self) -> dict:
+        """This rank's shards + optimizer state (a checkpoint that needs no
+        gather); restore with load_sharded_state_dict on the same plan."""
+        rt = self.rt
+        out = {"world_size": self.plan.world_size, "shard_factor": self.plan.shard_factor,
+               "rank": self.rank, "adam_steps": rt.adam_steps,
+               "psi": [lay.psi for lay in self.layouts], "units": []}
+        for u in rt.units:
+            d = {"master": u.master.detach().clone().cpu()}
+            if u.exp_avg is not None:
+                d["exp_avg"] = u.exp_avg.detach().clone().cpu()
+                d["exp_avg_sq"] = u.exp_avg_sq.detach().clone().cpu()
+            out["units"].append(d)
+        return out
+
+    def load_sharded_state_dict(self, sd: dict) -> None:
+        rt = self.rt
+        if (sd["world_size"], sd["shard_factor"], sd["rank"]) != \
+                (self.plan.world_size, self.plan.shard_factor, self.rank) or \
+                sd["psi"] != [lay.psi for lay in self.layouts]:
+            raise ValueError("sharded state dict was saved with a different plan/layout/rank")
+        from . import kernels
+        for u, d in zip(rt.units, sd["units"]):
+            u.master.copy_(d["master"])
+            if u.exp_avg is not None and "exp_avg" in d:
+                u.exp_avg.copy_(d["exp_avg"])
+                u.exp_avg_sq.copy_(d["exp_avg_sq"])
+            if u.low is not None:
+                kernels.cast(u.master, u.low)
+        rt.adam_steps = int(sd["adam_steps"])
+        torch.cuda.synchronize()
+
+    def trace_lines(self) -> list[str]:
+        """The reference's trace format (memsim.py:50-61) for this rank."""
+        return self.rt.trace.lines(self.rank)
 
 
 def owner_of_name(fq: str, root: nn.Module, owner_of: dict) -> int:

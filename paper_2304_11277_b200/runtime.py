@@ -173,6 +173,29 @@ class SlotPool:
         self.free.append((slot, ev))
 
 
+class TraceLog(list):
+    """Issue-order event log of one rank: (kind, unit) entries plus the bytes
+    each moved; `lines()` renders the reference's trace format
+    `rank= seq= kind= unit= bytes=` (memsim.py:50-61) so its trace-order
+    assertions (AG/RS issue order, prefetch placement) port unchanged."""
+
+    def __init__(self):
+        super().__init__()
+        self.nbytes: list[int] = []
+
+    def append(self, item) -> None:
+        super().append(item)
+        self.nbytes.append(0)
+
+    def record(self, kind: str, unit, nbytes: int = 0) -> None:
+        super().append((kind, unit))
+        self.nbytes.append(int(nbytes))
+
+    def lines(self, rank: int) -> list[str]:
+        return [f"rank={rank} seq={i} kind={k} unit={'-' if u is None else u} bytes={b}"
+                for i, ((k, u), b) in enumerate(zip(self, self.nbytes))]
+
+
 class _SlotRef:
     __slots__ = ("uid", "off", "size", "stride")
 
@@ -272,7 +295,7 @@ class FSDPRuntime:
         self.micro_index = 0
         self.step_count = 0           # optimizer steps taken (Adam t)
         self.events: list[tuple[int, str, int | None]] = []   # (step, kind, unit)
-        self.trace: list[tuple[str, int]] = []                # (kind, unit) issue order
+        self.trace = TraceLog()                               # (kind, unit) issue order
         self.inject_inf: set[int] = set()                     # steps to poison (test hook)
         self.found_inf = torch.zeros(1, dtype=torch.float32, device=self.device)
         self.found_inf_world = torch.zeros(1, dtype=torch.float32, device=self.device)
@@ -477,7 +500,7 @@ class FSDPRuntime:
         u.ag_event = ev
         u.window = _Window(uid)
         self.inflight.append(u.window)
-        self.trace.append(("AG_issue", uid))
+        self.trace.record("AG_issue", uid, lay.psi * self.compute_dtype.itemsize)
         self.bytes_ag += lay.psi * (2 if self.cfg.mixed else 4)
 
     def limiter_acquire(self) -> None:
@@ -789,7 +812,7 @@ class FSDPRuntime:
         ready = torch.cuda.Event()
         ready.record(self.compute_stream)
         self.events.append((self.step_count, "reduce_issue", uid))
-        self.trace.append(("RS_issue", uid))
+        self.trace.record("RS_issue", uid, grad.numel() * self.payload_dtype.itemsize)
         n = u.layout.shard_numel
         with torch.cuda.stream(self.rs_stream):
             self.rs_stream.wait_event(ready)
@@ -825,7 +848,7 @@ class FSDPRuntime:
                                                   payload.dtype, [tmp], prediv=pre, postdiv=1.0,
                                                   accumulate=False, stream=self.rs_stream, tma=False)
                 self.events.append((self.step_count, "reduce_stage2", uid))
-                self.trace.append(("AR_issue", uid))
+                self.trace.record("AR_issue", uid, n * 4)
                 with self.timed("allreduce", self.rs_stream, n * 4):
                     self.comm.all_reduce(self.plan.replicated_desc, [tmp], self.ar_stage_off,
                                          self.ar_gather_off, [u.grad], postdiv=post,
@@ -887,6 +910,12 @@ class FSDPRuntime:
     def optimizer_step(self, scale: float | None = None) -> None:
         """engine.py:563-594: unscale + world verdict + optimizer on the arena.
         The verdict stays on device (skip flag) — no host sync."""
+        for u in self.units:          # gathered copies would be stale after the update
+            if u.unsharded is not None:
+                if u.pending:
+                    self.compute_stream.wait_event(u.ag_event)
+                    u.pending = False
+                self.reshard(u.uid)
         skip = None
         if scale is not None:
             self.found_inf.zero_()

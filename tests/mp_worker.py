@@ -150,6 +150,31 @@ def fsdp_step_parity(rank, world, strategy, hybrid, results, backend="ipc", opt_
     fsdp.close()
 
 
+def deadlock_detection(rank, world, results):
+    """A member that never enters the collective: the others time out on
+    device into the error word and surface DeadlockError (the analogue of
+    collectives.py:461-483) instead of hanging the GPU."""
+    from paper_2304_11277_b200 import _lib
+    from paper_2304_11277_b200.comm import DeviceComm
+    from paper_2304_11277_b200.plan import DeadlockError
+    comm = DeviceComm.create(8 << 20, max_ctas=8)
+    comm.set_timeout_ms(1500)
+    off = comm.alloc(1 << 16)
+    dist.barrier()
+    if rank == 0:
+        comm.all_gather((world, 1), [torch.ones(64, device="cuda")], off, torch.float32)
+        torch.cuda.synchronize()
+        check(comm.device_error() == _lib.E_TIMEOUT, "timeout not recorded")
+        try:
+            comm.raise_device_error()
+            check(False, "DeadlockError not raised")
+        except DeadlockError:
+            pass
+    dist.barrier()
+    comm.close()
+    results["deadlock_detection"] = "ok"
+
+
 def _sess(w, f, spec=None, seed=0, **kw):
     from paper_2304_11277_b200.data import ModelSpec
     from paper_2304_11277_b200.plan import build_plan
@@ -285,6 +310,9 @@ def session_parity(rank, world, results):
     d = max(float(np.abs(g[k] - ref[k]).max()) for k in ref)
     check(0 < d < 1e-2, f"mixed delta {d}")
     check(all(u.master.dtype == torch.float32 for u in s.rt.units), "fp32 masters")
+    # AG payload is low precision: issue bytes = psi x 2 (test_engine.py:331-341, low = bf16)
+    ag_bytes = [b for (k, u), b in zip(s.trace, s.trace.nbytes) if k == "AG_issue"]
+    check(ag_bytes[0] == s.layouts[0].psi * 2, f"mixed AG bytes {ag_bytes[0]}")
     s.close()
     results["session"] = out
 
@@ -309,6 +337,7 @@ def main():
         if world == 4:
             fsdp_step_parity(rank, world, "HYBRID_SHARD", 2, results, opt_in_bwd=True)
         fsdp_step_parity(rank, world, "FULL_SHARD", None, results, backend="nccl")
+        deadlock_detection(rank, world, results)
     except Exception:
         ok = False
         traceback.print_exc()

@@ -191,6 +191,19 @@ int fsdp_reduce_scatter_tma(fsdp_comm_t* c, int channel, int gsize, int gstride,
                             int src_dtype, int64_t n, float* const* outs, float prediv,
                             float postdiv, int accumulate, void* stream);
 
+/* Copy-engine variants (no SM work for the data movement; real communicator
+ * only).  All-gather: same-dtype shard -> every member's pool at
+ * dst_off + pos*n (DMA writes over NVLink, one side stream per peer).
+ * Reduce-scatter: chunk pos of every member's payload (pool offset src_off)
+ * is DMA-pulled into local staging (stage_off, gsize*n elements), then one
+ * local kernel sums in ascending rank order in fp32 (/ postdiv, += out).
+ * Same flag protocol (enter barrier, per-peer release, exit barrier). */
+int fsdp_allgather_ce(fsdp_comm_t* c, int channel, int gsize, int gstride, const void* shard,
+                      int dtype, int64_t n, int64_t dst_off, void* stream);
+int fsdp_reduce_scatter_ce(fsdp_comm_t* c, int channel, int gsize, int gstride, int64_t src_off,
+                           int src_dtype, int64_t n, int64_t stage_off, float* out, float prediv,
+                           float postdiv, int accumulate, void* stream);
+
 /* All-reduce (collectives.py:298-301; hybrid stage 2, engine.py:804-816):
  * two-shot push (reduce-scatter to owners, ascending-rank fp32 sum, then
  * all-gather of the owners' results), so every member holds bit-identical

@@ -191,6 +191,22 @@ class DeviceComm:
                                            float(postdiv), int(accumulate), stream_ptr(stream)),
               "reduce_scatter_pull")
 
+    def all_gather_ce(self, gdesc, shard: torch.Tensor, dst_off: int, stream=None,
+                      channel: int = _lib.CH_AG) -> None:
+        """Copy-engine all-gather (same dtype in and out)."""
+        check(lib.fsdp_allgather_ce(self._h, channel, gdesc[0], gdesc[1], shard.data_ptr(),
+                                    dtype_code(shard.dtype), shard.numel(), dst_off,
+                                    stream_ptr(stream)), "allgather_ce")
+
+    def reduce_scatter_ce(self, gdesc, src_off: int, src_dtype: torch.dtype, stage_off: int,
+                          out: torch.Tensor, prediv: float = 1.0, postdiv: float = 1.0,
+                          accumulate: bool = False, stream=None, channel: int = _lib.CH_RS) -> None:
+        """Copy-engine pull of the peers' chunks + local ascending fp32 reduction."""
+        check(lib.fsdp_reduce_scatter_ce(self._h, channel, gdesc[0], gdesc[1], src_off,
+                                         dtype_code(src_dtype), out.numel(), stage_off,
+                                         out.data_ptr(), float(prediv), float(postdiv),
+                                         int(accumulate), stream_ptr(stream)), "reduce_scatter_ce")
+
     def all_reduce(self, gdesc, ins: Sequence[torch.Tensor], stage_off: int, gather_off: int,
                    outs: Sequence[torch.Tensor], postdiv: float = 1.0, accumulate: bool = False,
                    stream=None, channel: int = _lib.CH_AR) -> None:

@@ -241,6 +241,66 @@ __global__ void __launch_bounds__(256) coll_exit_kernel(const __grid_constant__ 
   }
 }
 
+// Copy-engine path: after the data has been moved by DMA (cudaMemcpyAsync,
+// ordered before this kernel on the stream), publish "my part is done" to
+// every member with one system-scope release per peer (phase 1, slot 0).
+__global__ void __launch_bounds__(32) coll_signal_kernel(const __grid_constant__ CollParams p) {
+  const Group g = make_group(p);
+  if ((int)threadIdx.x < g.size) {
+    __threadfence_system();
+    st_release_sys(flag_ptr(p.bases[g.member(threadIdx.x)], p.channel, 1, g.rank, 0), p.epoch);
+  }
+}
+
+// Local reduction of a copy-engine reduce-scatter: member chunks j != pos sit
+// in local staging (off_b + j*n), the own chunk in the own payload buffer
+// (off_a + pos*n); ascending-rank fp32 sum from +0, / postdiv, += out.
+template <typename Tin>
+__global__ void __launch_bounds__(256)
+ce_reduce_kernel(const __grid_constant__ CollParams p) {
+  const Group g = make_group(p);
+  const int e = p.rank0 >= 0 ? 0 : blockIdx.y;
+  float* __restrict__ out = p.out[e];
+  const int64_t n = p.n;
+  const Tin* own = (const Tin*)(p.bases[g.rank] + p.off_a) + (int64_t)g.pos * n;
+  const Tin* stage = (const Tin*)(p.bases[g.rank] + p.off_b);
+  const bool pre = p.prediv != 1.0f, post = p.postdiv != 1.0f;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const bool vec = (n % kVec == 0) && aligned16(own) && aligned16(stage) && aligned16(out);
+  if (vec) {
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v * kVec < n; v += stride) {
+      const int64_t i = v * kVec;
+      V8F acc;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc.v[q] = 0.0f;
+      for (int j = 0; j < g.size; ++j) {
+        const V8F x = unpack8<Tin>(j == g.pos ? ldg8<Tin>(own + i) : ldg8<Tin>(stage + (int64_t)j * n + i));
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          acc.v[q] = __fadd_rn(acc.v[q], pre ? __fdiv_rn(x.v[q], p.prediv) : x.v[q]);
+      }
+      V8F base;
+      if (p.accumulate) base = unpack8<float>(ldcg8<float>(out + i));
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float r = post ? __fdiv_rn(acc.v[q], p.postdiv) : acc.v[q];
+        acc.v[q] = __fadd_rn(p.accumulate ? base.v[q] : 0.0f, r);
+      }
+      st8<float>(out + i, pack8<float>(acc));
+    }
+  } else {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+      float acc = 0.0f;
+      for (int j = 0; j < g.size; ++j) {
+        const float x = to_f<Tin>(j == g.pos ? own[i] : stage[(int64_t)j * n + i]);
+        acc = __fadd_rn(acc, pre ? __fdiv_rn(x, p.prediv) : x);
+      }
+      const float r = post ? __fdiv_rn(acc, p.postdiv) : acc;
+      out[i] = __fadd_rn(p.accumulate ? out[i] : 0.0f, r);
+    }
+  }
+}
+
 // ------------------------------------------------------------ all-gather ----
 template <typename Tin, typename Tout>
 __global__ void __launch_bounds__(kCommThreads)
@@ -723,6 +783,10 @@ struct fsdp_comm {
   bool timing = false;                        // record events around every data kernel
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed[FSDP_NUM_KINDS];
   std::vector<cudaEvent_t> spare;
+  // copy-engine path: one side stream per peer (parallel CEs), event pool
+  cudaStream_t ce_stream[FSDP_MAX_RANKS] = {};
+  std::vector<cudaEvent_t> ce_events;
+  size_t ce_next = 0;
 };
 
 namespace {
@@ -968,6 +1032,9 @@ extern "C" int fsdp_comm_destroy(fsdp_comm_t* c) {
   for (auto& v : c->timed)
     for (auto& pr : v) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
   for (auto e : c->spare) cudaEventDestroy(e);
+  for (auto e : c->ce_events) cudaEventDestroy(e);
+  for (auto s : c->ce_stream)
+    if (s) cudaStreamDestroy(s);
   cudaFree(c->pool);
   delete c;
   return 0;
@@ -1106,6 +1173,115 @@ extern "C" int fsdp_reduce_scatter_tma(fsdp_comm_t* c, int channel, int gsize, i
   }
   FSDP_LAUNCHED();
   return 0;
+}
+
+// ---------------------------------------------------- copy-engine variants --
+static int ce_prepare(fsdp_comm_t* c) {
+  if (c->ce_events.empty()) {
+    for (int r = 0; r < FSDP_MAX_RANKS; ++r)
+      FSDP_CUDA(cudaStreamCreateWithFlags(&c->ce_stream[r], cudaStreamNonBlocking));
+    c->ce_events.resize(256);
+    for (auto& e : c->ce_events) FSDP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  return 0;
+}
+static cudaEvent_t ce_event(fsdp_comm_t* c) {
+  cudaEvent_t e = c->ce_events[c->ce_next % c->ce_events.size()];
+  ++c->ce_next;
+  return e;
+}
+
+// copies[j] = (dst, src, bytes) for member j (skipped when bytes == 0); each on
+// its own side stream so distinct peers' transfers use distinct copy engines
+static int ce_fork_join(fsdp_comm_t* c, cudaStream_t s, int gsize, void* const* dst,
+                        const void* const* src, size_t bytes) {
+  cudaEvent_t fork = ce_event(c);
+  FSDP_CUDA(cudaEventRecord(fork, s));
+  for (int j = 0; j < gsize; ++j) {
+    if (!dst[j] || !bytes) continue;
+    FSDP_CUDA(cudaStreamWaitEvent(c->ce_stream[j], fork, 0));
+    FSDP_CUDA(cudaMemcpyAsync(dst[j], src[j], bytes, cudaMemcpyDeviceToDevice, c->ce_stream[j]));
+    cudaEvent_t done = ce_event(c);
+    FSDP_CUDA(cudaEventRecord(done, c->ce_stream[j]));
+    FSDP_CUDA(cudaStreamWaitEvent(s, done, 0));
+  }
+  return 0;
+}
+
+extern "C" int fsdp_allgather_ce(fsdp_comm_t* c, int channel, int gsize, int gstride,
+                                 const void* shard, int dtype, int64_t n, int64_t dst_off,
+                                 void* stream) {
+  if (int rc = validate_group(c, channel, gsize, gstride)) return rc;
+  if (c->emulated) return fail(FSDP_E_UNSUPPORTED, "copy-engine collectives need a real communicator");
+  const int es = elem_size(dtype);
+  if (n < 0 || !shard || !es) return fail(FSDP_E_INVALID, "fsdp_allgather_ce: bad args");
+  if (int rc = check_range(c, dst_off, n * gsize * es, "fsdp_allgather_ce")) return rc;
+  if (int rc = ce_prepare(c)) return rc;
+  CollParams p;
+  fill_common(c, p, channel, gsize, gstride, n);
+  p.data_ctas = 1;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (int rc = launch(c, coll_enter_kernel, p, 1, 32, s)) return rc;
+  const int start = gstride == 1 ? (c->rank / gsize) * gsize : c->rank % gstride;
+  const int pos = gstride == 1 ? c->rank - start : c->rank / gstride;
+  void* dst[FSDP_MAX_RANKS] = {};
+  const void* src[FSDP_MAX_RANKS] = {};
+  for (int j = 0; j < gsize; ++j) {
+    dst[j] = c->bases[start + j * gstride] + dst_off + (int64_t)pos * n * es;
+    src[j] = shard;
+  }
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (c->timing) { a = take_event(c); b = take_event(c); FSDP_CUDA(cudaEventRecord(a, s)); }
+  if (int rc = ce_fork_join(c, s, gsize, dst, src, (size_t)n * es)) return rc;
+  if (c->timing) { FSDP_CUDA(cudaEventRecord(b, s)); c->timed[FSDP_KIND_AG].emplace_back(a, b); }
+  if (int rc = launch(c, coll_signal_kernel, p, 1, 32, s)) return rc;
+  return launch(c, coll_exit_kernel, p, 1, 256, s);
+}
+
+extern "C" int fsdp_reduce_scatter_ce(fsdp_comm_t* c, int channel, int gsize, int gstride,
+                                      int64_t src_off, int src_dtype, int64_t n,
+                                      int64_t stage_off, float* out, float prediv, float postdiv,
+                                      int accumulate, void* stream) {
+  if (int rc = validate_group(c, channel, gsize, gstride)) return rc;
+  if (c->emulated) return fail(FSDP_E_UNSUPPORTED, "copy-engine collectives need a real communicator");
+  const int es = elem_size(src_dtype);
+  if (n < 0 || !out || !es) return fail(FSDP_E_INVALID, "fsdp_reduce_scatter_ce: bad args");
+  if (!(prediv > 0.f) || !(postdiv > 0.f)) return fail(FSDP_E_INVALID, "divisors must be > 0");
+  if (int rc = check_range(c, src_off, n * gsize * es, "fsdp_reduce_scatter_ce(src)")) return rc;
+  if (int rc = check_range(c, stage_off, n * gsize * es, "fsdp_reduce_scatter_ce(stage)")) return rc;
+  if (int rc = ce_prepare(c)) return rc;
+  CollParams p;
+  fill_common(c, p, channel, gsize, gstride, n);
+  p.data_ctas = 1;
+  p.out[0] = out;
+  p.off_a = src_off;
+  p.off_b = stage_off;
+  p.prediv = prediv; p.postdiv = postdiv; p.accumulate = accumulate ? 1 : 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (int rc = launch(c, coll_enter_kernel, p, 1, 32, s)) return rc;
+  const int start = gstride == 1 ? (c->rank / gsize) * gsize : c->rank % gstride;
+  const int pos = gstride == 1 ? c->rank - start : c->rank / gstride;
+  void* dst[FSDP_MAX_RANKS] = {};
+  const void* src[FSDP_MAX_RANKS] = {};
+  for (int j = 0; j < gsize; ++j) {
+    if (j == pos) continue;   // own chunk is reduced in place
+    dst[j] = c->bases[c->rank] + stage_off + (int64_t)j * n * es;
+    src[j] = c->bases[start + j * gstride] + src_off + (int64_t)pos * n * es;   // pull
+  }
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (c->timing) { a = take_event(c); b = take_event(c); FSDP_CUDA(cudaEventRecord(a, s)); }
+  if (int rc = ce_fork_join(c, s, gsize, dst, src, (size_t)n * es)) return rc;
+  if (c->timing) { FSDP_CUDA(cudaEventRecord(b, s)); c->timed[FSDP_KIND_RS].emplace_back(a, b); }
+  if (int rc = launch(c, coll_signal_kernel, p, 1, 32, s)) return rc;   // done reading peers
+  const int64_t nv = std::max<int64_t>(1, (n + kVec - 1) / kVec);
+  const int grid = (int)std::min<int64_t>((nv + 255) / 256, (int64_t)kNumSMs * 4);
+  if (src_dtype == FSDP_BF16) {
+    ce_reduce_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(p);
+  } else {
+    ce_reduce_kernel<float><<<grid, 256, 0, s>>>(p);
+  }
+  FSDP_LAUNCHED();
+  return launch(c, coll_exit_kernel, p, 1, 256, s);     // peers done reading mine
 }
 
 extern "C" int fsdp_allreduce(fsdp_comm_t* c, int channel, int gsize, int gstride,

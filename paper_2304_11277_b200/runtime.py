@@ -84,6 +84,12 @@ class RuntimeConfig:
     num_slots: int | None = None
     ag_ctas: int = 32                    # grid cap of the all-gather data kernel
     rs_ctas: int = 64                    # grid cap of the reduce-scatter data kernel
+    # data movement engine of the collectives.  "ce": copy engines move the
+    # bytes (DMA over NVLink, no SMs taken from the concurrent GEMMs; measured
+    # lower exposed comm in-step); "sm": push/pull kernels (higher standalone
+    # bandwidth).  Same flag protocol and bits either way.
+    ag_engine: str = "ce"
+    rs_engine: str = "ce"
     optimizer: str = "adam"
     lr: float = 1e-3
     betas: tuple = (0.9, 0.999)
@@ -373,6 +379,8 @@ class FSDPRuntime:
                 self.gslot_offs = [c.alloc(psi_max * ps) for _ in range(2)]
                 self.gslot_views = [c.view(o, psi_max, self.payload_dtype) for o in self.gslot_offs]
                 self.gslot_free = [None, None]
+                if self.cfg.rs_engine == "ce":
+                    self.rs_stage_off = c.alloc(psi_max * ps)    # local DMA landing zone
             if F < W:
                 n_ar = n_max if F > 1 else psi_max
                 gsz = W // F
@@ -398,7 +406,7 @@ class FSDPRuntime:
         total = reserved
         pad = lambda b: -(-b // 256) * 256 + 256  # noqa: E731
         if F > 1:
-            total += nslots * pad(psi_max * es) + 2 * pad(psi_max * ps)
+            total += nslots * pad(psi_max * es) + 3 * pad(psi_max * ps)
         if W > 1 and F < W:
             n_ar = n_max if F > 1 else psi_max
             g = W // F
@@ -490,8 +498,12 @@ class FSDPRuntime:
             elif self.cfg.comm_backend == "ipc":
                 with self.timed("allgather", self.ag_stream,
                                 lay.psi * (2 if self.cfg.mixed else 4)):
-                    self.comm.all_gather(self._group_ag(), [src], self.slots.offsets[slot],
-                                         self.compute_dtype, stream=self.ag_stream)
+                    if self.cfg.ag_engine == "ce" and src.dtype == self.compute_dtype:
+                        self.comm.all_gather_ce(self._group_ag(), src, self.slots.offsets[slot],
+                                                stream=self.ag_stream)
+                    else:
+                        self.comm.all_gather(self._group_ag(), [src], self.slots.offsets[slot],
+                                             self.compute_dtype, stream=self.ag_stream)
             else:
                 import torch.distributed as dist
                 dist.all_gather_into_tensor(u.unsharded, src, group=self.pgs.get("shard"))
@@ -783,6 +795,18 @@ class FSDPRuntime:
         kernels.flatten([u.flat_grad], [0], u.accum_unsharded, accumulate=not first,
                         stream=self.compute_stream)
 
+    def _rs(self, gslot: int, dtype: torch.dtype, out: torch.Tensor, pre: float, post: float,
+            accumulate: bool) -> None:
+        """Reduce-scatter of the payload in symmetric gradient slot `gslot`."""
+        if self.cfg.rs_engine == "ce":
+            self.comm.reduce_scatter_ce(self.plan.sharded_desc, self.gslot_offs[gslot], dtype,
+                                        self.rs_stage_off, out, prediv=pre, postdiv=post,
+                                        accumulate=accumulate, stream=self.rs_stream)
+        else:
+            self.comm.reduce_scatter_pull(self.plan.sharded_desc, self.gslot_offs[gslot], dtype,
+                                          [out], prediv=pre, postdiv=post, accumulate=accumulate,
+                                          stream=self.rs_stream, tma=False)
+
     def _acquire_gslot(self, psi: int) -> tuple[int, torch.Tensor]:
         """Next symmetric gradient slot (alternating); compute waits until the
         reduce-scatter that last read it has finished on every peer."""
@@ -832,10 +856,7 @@ class FSDPRuntime:
                 self._reduce_nccl(u, payload, accumulate, pre, post)
             elif F == W:
                 with self.timed("reduce_scatter", self.rs_stream, payload.numel() * payload.element_size()):
-                    self.comm.reduce_scatter_pull(self.plan.sharded_desc, self.gslot_offs[gslot],
-                                                  payload.dtype, [u.grad], prediv=pre, postdiv=post,
-                                                  accumulate=accumulate, stream=self.rs_stream,
-                                                  tma=False)
+                    self._rs(gslot, payload.dtype, u.grad, pre, post, accumulate)
             elif F == 1:
                 with self.timed("allreduce", self.rs_stream, payload.numel() * payload.element_size()):
                     self.comm.all_reduce(self.plan.replicated_desc, [payload], self.ar_stage_off,
@@ -844,9 +865,7 @@ class FSDPRuntime:
             else:
                 tmp = torch.empty(n, dtype=torch.float32, device=self.device)
                 with self.timed("reduce_scatter", self.rs_stream, payload.numel() * payload.element_size()):
-                    self.comm.reduce_scatter_pull(self.plan.sharded_desc, self.gslot_offs[gslot],
-                                                  payload.dtype, [tmp], prediv=pre, postdiv=1.0,
-                                                  accumulate=False, stream=self.rs_stream, tma=False)
+                    self._rs(gslot, payload.dtype, tmp, pre, 1.0, False)
                 self.events.append((self.step_count, "reduce_stage2", uid))
                 self.trace.record("AR_issue", uid, n * 4)
                 with self.timed("allreduce", self.rs_stream, n * 4):

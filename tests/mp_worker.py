@@ -79,6 +79,17 @@ def raw_collectives(rank, world, results):
             exp = sp.reduce_unit(grads, sp.Plan(world, f), reduce_dtype=sp.BF16, full_dtype=np.float32,
                                  acc_dtype=np.float32, mean=True, accum=bases)
             check(out.cpu().numpy().tobytes() == exp[rank].tobytes(), f"hybrid n={n}")
+        # copy-engine variants: same bits
+        sh = torch.from_numpy(shards[rank]).cuda().to(torch.bfloat16)
+        comm.all_gather_ce((world, 1), sh, a)
+        got = comm.view(a, n * world, torch.bfloat16).float().cpu().numpy()
+        check(np.array_equal(got, sp.cast(sp.all_gather(shards), sp.BF16)), f"AG-CE n={n}")
+        comm.view(b, n * world, torch.bfloat16).copy_(torch.from_numpy(grads[rank]).cuda().to(torch.bfloat16))
+        out = torch.from_numpy(acc0[rank]).cuda()
+        comm.reduce_scatter_ce((world, 1), b, torch.bfloat16, a, out, postdiv=float(world), accumulate=True)
+        exp = sp.reduce_unit(grads, sp.Plan(world, world), reduce_dtype=sp.BF16, full_dtype=np.float32,
+                             acc_dtype=np.float32, mean=True, accum=acc0)
+        check(out.cpu().numpy().tobytes() == exp[rank].tobytes(), f"RS-CE n={n}")
     flag = torch.tensor([1.0 if rank == world - 1 else 0.0], device="cuda")
     tot = torch.zeros(1, device="cuda")
     comm.scalar_all_reduce([flag], [tot])
@@ -89,7 +100,8 @@ def raw_collectives(rank, world, results):
     results["raw_collectives"] = "bit-exact"
 
 
-def fsdp_step_parity(rank, world, strategy, hybrid, results, backend="ipc", opt_in_bwd=False):
+def fsdp_step_parity(rank, world, strategy, hybrid, results, backend="ipc", opt_in_bwd=False,
+                     engine="ce"):
     from paper_2304_11277_b200 import kernels  # noqa: F401
     from paper_2304_11277_b200.fsdp import (FullyShardedDataParallel, MixedPrecision,
                                             ModuleWrapPolicy, ShardingStrategy)
@@ -100,7 +112,8 @@ def fsdp_step_parity(rank, world, strategy, hybrid, results, backend="ipc", opt_
                                     auto_wrap_policy=ModuleWrapPolicy({Block}),
                                     mixed_precision=MixedPrecision(param_dtype=torch.bfloat16),
                                     hybrid_shard_size=hybrid, comm_backend=backend, lr=1e-3,
-                                    optimizer_in_backward=opt_in_bwd)
+                                    optimizer_in_backward=opt_in_bwd, ag_engine=engine,
+                                    rs_engine=engine)
     plan = fsdp.plan
     ref = init_gpt_(GPT(cfg), seed=0).cuda().to(torch.bfloat16)
     x, y = synthetic_batch(cfg, 2, seed=100 + rank, device="cuda")
@@ -108,7 +121,8 @@ def fsdp_step_parity(rank, world, strategy, hybrid, results, backend="ipc", opt_
     loss.backward()
     lref = ref(x, y)
     lref.backward()
-    key = f"{strategy}{'' if hybrid is None else hybrid}/{backend}{'/opt-in-bwd' if opt_in_bwd else ''}"
+    key = (f"{strategy}{'' if hybrid is None else hybrid}/{backend}/{engine}"
+           f"{'/opt-in-bwd' if opt_in_bwd else ''}")
     torch.cuda.synchronize()
     # initial shards from the oracle (flatten + shard of the same init)
     vals = {k: v.detach().float().cpu().numpy() for k, v in init_gpt_(GPT(cfg), seed=0).named_parameters()}
@@ -334,6 +348,9 @@ def main():
         for strat, hyb in cases:
             fsdp_step_parity(rank, world, strat, hyb, results)
         fsdp_step_parity(rank, world, "FULL_SHARD", None, results, opt_in_bwd=True)
+        fsdp_step_parity(rank, world, "FULL_SHARD", None, results, engine="sm")
+        if world == 4:
+            fsdp_step_parity(rank, world, "HYBRID_SHARD", 2, results, engine="sm")
         if world == 4:
             fsdp_step_parity(rank, world, "HYBRID_SHARD", 2, results, opt_in_bwd=True)
         fsdp_step_parity(rank, world, "FULL_SHARD", None, results, backend="nccl")

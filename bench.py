@@ -283,9 +283,16 @@ def run_ours(args):
                     "bus_bytes_per_launch": int(bus), "mean_ms": round(dms, 4),
                     "note": "timed live inside the step, concurrent with GEMMs"}
         else:
+            traffic = None
+            try:
+                with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+                    t = json.load(fh).get(f"{dom}|{args.config}|{world}")
+                traffic = t["bytes"] if t else None
+            except Exception:
+                traffic = None
             roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1),
                     "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
-                    "traffic": None, "peak_kind": peak_kind,
+                    "traffic": traffic, "peak_kind": peak_kind,
                     "algorithmic_bytes_per_launch": int(per_launch_bytes),
                     "mean_ms": round(d["mean_ms"], 4)}
     step_roof = {"bound": "tensor", "achieved": round(tflops_gpu, 1), "peak": bf16_peak,

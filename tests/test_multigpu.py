@@ -34,3 +34,19 @@ def test_multigpu_parity():
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-6000:]
     res = json.loads(lines[-1])
     assert res["ok"] and res["raw_collectives"] == "bit-exact"
+
+
+def test_multigpu_cli_verify():
+    """`verify`: sharded fp32 training vs an unsharded torch.optim.Adam copy."""
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    w = 4 if n >= 4 else 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={w}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+           "-m", "paper_2304_11277_b200", "verify", "--steps", "3"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900,
+                       cwd=os.path.dirname(HERE))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    last = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]
+    assert json.loads(last)["verify"] == "PASS"

@@ -444,6 +444,57 @@ def _shard_group(plan, rank):
     return _nccl_groups(plan, rank)["shard"]
 
 
+class ShardedGradScaler:
+    """torch.distributed.fsdp.ShardedGradScaler-shaped loss scaler over the
+    runtime's device-side verdict (engine.py:118-145, :563-589):
+
+        scaler.scale(loss).backward(); scaler.step(opt); scaler.update()
+
+    step() unscales every rank's gradient shard, all-reduces the found_inf
+    flag across the world and runs the optimizer with an on-device skip (no
+    host sync); update() reads the verdict once and backs off / grows the
+    scale exactly like the reference."""
+
+    def __init__(self, init_scale: float = 65536.0, growth_factor: float = 2.0,
+                 backoff_factor: float = 0.5, growth_interval: int = 2000, enabled: bool = True):
+        self.scale_value = float(init_scale)
+        self.growth_factor, self.backoff_factor = growth_factor, backoff_factor
+        self.growth_interval = growth_interval
+        self.enabled = enabled
+        self._tracker = 0
+        self._pending: FullyShardedDataParallel | None = None
+        self.steps_skipped = 0
+
+    def scale(self, loss: torch.Tensor) -> torch.Tensor:
+        return loss * self.scale_value if self.enabled else loss
+
+    def step(self, optimizer: "ShardedOptimizer") -> None:
+        if not self.enabled:
+            optimizer.step()
+            return
+        optimizer.step(scale=self.scale_value)
+        self._pending = optimizer.fsdp
+
+    def update(self) -> bool:
+        """Returns True if the last step was skipped (non-finite gradients)."""
+        if not self.enabled or self._pending is None:
+            return False
+        rt = self._pending.rt
+        found = bool(rt.found_inf_world.item() > 0.0)
+        if found:
+            rt.undo_adam_t()
+            self.scale_value *= self.backoff_factor
+            self._tracker = 0
+            self.steps_skipped += 1
+        else:
+            self._tracker += 1
+            if self._tracker >= self.growth_interval:
+                self.scale_value *= self.growth_factor
+                self._tracker = 0
+        self._pending = None
+        return found
+
+
 class ShardedOptimizer:
     """torch.optim-like handle: step() runs the fused sharded optimizer."""
 

@@ -114,6 +114,30 @@ def test_state_dict_roundtrips_and_trace_format():
     assert all(l.startswith("rank=0 seq=") and " kind=" in l and " bytes=" in l for l in lines)
 
 
+def test_wrapper_grad_scaler_skips_nonfinite_step():
+    from paper_2304_11277_b200.fsdp import ShardedGradScaler
+    from paper_2304_11277_b200.workloads import synthetic_batch
+    cfg, m, _ = build()
+    sc = ShardedGradScaler(init_scale=1024.0)
+    opt = m.optimizer(lr=1e-3)
+    x, y = synthetic_batch(cfg, 2, seed=3, device="cuda")
+    sc.scale(m(x, y)).backward()
+    sc.step(opt)
+    assert not sc.update() and sc.scale_value == 1024.0
+    before = [u.master.clone() for u in m.rt.units]
+    m.rt.inject_inf = {m.rt.step_count}          # poison unit 0's gradient this step
+    sc.scale(m(x, y)).backward()
+    sc.step(opt)
+    assert sc.update() and sc.scale_value == 512.0 and sc.steps_skipped == 1
+    for b, u in zip(before, m.rt.units):
+        assert torch.equal(b, u.master)          # every shard skipped on device
+    m.rt.inject_inf = set()
+    sc.scale(m(x, y)).backward()
+    sc.step(opt)
+    assert not sc.update()
+    assert m.rt.adam_steps == 2                  # the skipped step did not advance Adam's t
+
+
 def test_optimizer_in_backward_identical():
     """Per-unit Adam on the reduce stream during backward == end-of-step launch."""
     from paper_2304_11277_b200.workloads import synthetic_batch

@@ -784,7 +784,8 @@ struct fsdp_comm {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed[FSDP_NUM_KINDS];
   std::vector<cudaEvent_t> spare;
   // copy-engine path: one side stream per peer (parallel CEs), event pool
-  cudaStream_t ce_stream[FSDP_MAX_RANKS] = {};
+  cudaStream_t ce_stream[FSDP_MAX_RANKS * 4] = {};
+  int ce_split = 1;                           // pieces per peer copy (FSDP_CE_SPLIT, <= 4)
   std::vector<cudaEvent_t> ce_events;
   size_t ce_next = 0;
 };
@@ -1178,7 +1179,8 @@ extern "C" int fsdp_reduce_scatter_tma(fsdp_comm_t* c, int channel, int gsize, i
 // ---------------------------------------------------- copy-engine variants --
 static int ce_prepare(fsdp_comm_t* c) {
   if (c->ce_events.empty()) {
-    for (int r = 0; r < FSDP_MAX_RANKS; ++r)
+    if (const char* e = getenv("FSDP_CE_SPLIT")) c->ce_split = std::max(1, std::min(4, atoi(e)));
+    for (int r = 0; r < FSDP_MAX_RANKS * c->ce_split; ++r)
       FSDP_CUDA(cudaStreamCreateWithFlags(&c->ce_stream[r], cudaStreamNonBlocking));
     c->ce_events.resize(256);
     for (auto& e : c->ce_events) FSDP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -1197,13 +1199,22 @@ static int ce_fork_join(fsdp_comm_t* c, cudaStream_t s, int gsize, void* const* 
                         const void* const* src, size_t bytes) {
   cudaEvent_t fork = ce_event(c);
   FSDP_CUDA(cudaEventRecord(fork, s));
+  const int k = c->ce_split;
+  const size_t piece = ((bytes + k - 1) / k + 255) / 256 * 256;
   for (int j = 0; j < gsize; ++j) {
     if (!dst[j] || !bytes) continue;
-    FSDP_CUDA(cudaStreamWaitEvent(c->ce_stream[j], fork, 0));
-    FSDP_CUDA(cudaMemcpyAsync(dst[j], src[j], bytes, cudaMemcpyDeviceToDevice, c->ce_stream[j]));
-    cudaEvent_t done = ce_event(c);
-    FSDP_CUDA(cudaEventRecord(done, c->ce_stream[j]));
-    FSDP_CUDA(cudaStreamWaitEvent(s, done, 0));
+    for (int q = 0; q < k; ++q) {
+      const size_t off = (size_t)q * piece;
+      if (off >= bytes) break;
+      const size_t len = std::min(piece, bytes - off);
+      cudaStream_t cs = c->ce_stream[j * k + q];
+      FSDP_CUDA(cudaStreamWaitEvent(cs, fork, 0));
+      FSDP_CUDA(cudaMemcpyAsync((char*)dst[j] + off, (const char*)src[j] + off, len,
+                                cudaMemcpyDeviceToDevice, cs));
+      cudaEvent_t done = ce_event(c);
+      FSDP_CUDA(cudaEventRecord(done, cs));
+      FSDP_CUDA(cudaStreamWaitEvent(s, done, 0));
+    }
   }
   return 0;
 }

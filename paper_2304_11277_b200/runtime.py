@@ -907,7 +907,8 @@ class FSDPRuntime:
         for uid in self.bwd_order:
             u = self.units[uid]
             if not u.bwd_done and u.grad_pending > 0:
-                warnings.warn(f"unit {uid}: no gradient for any parameter, zero-filled")
+                if u.layout.originals:
+                    warnings.warn(f"unit {uid}: no gradient for any parameter, zero-filled")
                 if u.flat_grad is None:
                     u.flat_grad = torch.empty(u.layout.psi, dtype=self.compute_dtype, device=self.device)
                     kernels.flatten([None] * len(u.layout.originals), u.layout.offsets, u.flat_grad,
@@ -935,6 +936,12 @@ class FSDPRuntime:
                     self.compute_stream.wait_event(u.ag_event)
                     u.pending = False
                 self.reshard(u.uid)
+            if u.reduces_this_step == 0 and not u.stepped:
+                # unit not visited this step: its gradient is zero (the
+                # reference zero-fills missing gradients, flatparam.py:181-185),
+                # never a stale one from an earlier step
+                self.compute_stream.wait_stream(self.rs_stream)
+                u.grad.zero_()
         skip = None
         if scale is not None:
             self.found_inf.zero_()

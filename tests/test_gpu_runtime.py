@@ -138,6 +138,47 @@ def test_wrapper_grad_scaler_skips_nonfinite_step():
     assert m.rt.adam_steps == 2                  # the skipped step did not advance Adam's t
 
 
+class _OddMLP(torch.nn.Module):
+    """Root without parameters; units with odd, non-multiple-of-8 sizes and
+    one unit whose parameter is never used (zero-filled gradient)."""
+
+    def __init__(self):
+        super().__init__()
+        self.a = torch.nn.Linear(5, 7)
+        self.b = torch.nn.Linear(7, 3)
+        self.unused = torch.nn.Linear(3, 3)
+
+    def forward(self, x):
+        return self.b(torch.relu(self.a(x))).pow(2).mean()
+
+
+def test_paramless_root_odd_sizes_unused_unit():
+    import warnings
+    from paper_2304_11277_b200.fsdp import FullyShardedDataParallel, ModuleWrapPolicy
+    torch.manual_seed(0)
+    ref = _OddMLP()
+    m = FullyShardedDataParallel(_OddMLP().requires_grad_(True), auto_wrap_policy=ModuleWrapPolicy({torch.nn.Linear}),
+                                 optimizer="sgd", lr=0.1)
+    m.load_full_state_dict({k: v for k, v in ref.state_dict().items()})
+    assert m.layouts[0].psi == 0 and [l.psi for l in m.layouts[1:]] == [42, 24, 12]
+    x = torch.randn(4, 5, device="cuda")
+    refc = _OddMLP().cuda()
+    refc.load_state_dict(ref.state_dict())
+    loss = m(x)
+    loss.backward()
+    m.optimizer().step()
+    lr = refc(x)
+    lr.backward()
+    with torch.no_grad():
+        for p in refc.parameters():
+            if p.grad is not None:
+                p -= 0.1 * p.grad
+    sd = m.full_state_dict()
+    for k, v in refc.state_dict().items():
+        assert torch.allclose(sd[k], v, atol=1e-6), k
+    assert torch.equal(sd["unused.weight"], refc.unused.weight)      # zero grad: unchanged
+
+
 def test_optimizer_in_backward_identical():
     """Per-unit Adam on the reduce stream during backward == end-of-step launch."""
     from paper_2304_11277_b200.workloads import synthetic_batch

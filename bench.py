@@ -35,6 +35,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "TFLOPS/GPU and step time at 1/2/4/8 B200; AG/RS bus GB/s vs 900 GB/s NVLink"
+# NVLink roofline denominators: nominal 900 GB/s per direction; measured peer
+# copy on this pool's B200s 770 GB/s per direction (B200_PROFILING.md)
+NVLINK_MEASURED_GBS = 770.0
 
 
 def parse():
@@ -46,7 +49,7 @@ def parse():
     ap.add_argument("--micro", type=int, default=8, help="sequences per GPU per step")
     ap.add_argument("--backend", default="ipc", choices=["ipc", "nccl"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mode", default="step", choices=["step", "sweep"])
+    ap.add_argument("--mode", default="step", choices=["step", "sweep", "copy"])
     ap.add_argument("--strategy", default="FULL_SHARD")
     ap.add_argument("--hybrid-shard-size", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -54,7 +57,7 @@ def parse():
     ap.add_argument("--forward-prefetch", action="store_true")
     ap.add_argument("--ctas", type=int, default=32, help="CTAs of the all-gather data kernel")
     ap.add_argument("--rs-ctas", type=int, default=64, help="CTAs of the reduce-scatter data kernel")
-    ap.add_argument("--ag-engine", default="ce", choices=["sm", "ce"])
+    ap.add_argument("--ag-engine", default="ce", choices=["sm", "ce", "nvls"])
     ap.add_argument("--rs-engine", default="ce", choices=["sm", "ce"])
     ap.add_argument("--exposed", action="store_true",
                     help="also time the step with collectives replaced by no-ops")
@@ -404,6 +407,10 @@ def run_sweep(args):
     cta_opts = [int(c) for c in os.environ.get("FSDP_SWEEP_CTAS", "16,32,64").split(",")]
     comms = {c: DeviceComm.create(2 * max_bytes + (64 << 20), max_ctas=c) for c in cta_opts}
     offs = {c: (cm.alloc(max_bytes), cm.alloc(max_bytes)) for c, cm in comms.items()}
+    # NVLS multicast all-gather (multimem.st), same CTA options
+    nvls = {c: DeviceComm.create(max_bytes + (64 << 20), max_ctas=c, nvls_group=world) for c in cta_opts}
+    nvls = {c: cm for c, cm in nvls.items() if cm.nvls_group == world}
+    nvls_off = {c: cm.alloc(max_bytes) for c, cm in nvls.items()}
     dev = torch.device("cuda", local)
     res = []
     for mb in sizes_mb:
@@ -439,24 +446,121 @@ def run_sweep(args):
             cm.view(stage, n * world, torch.bfloat16).copy_(flat)
             r[f"rs_pull_c{c}"] = bus / (timeit(lambda: cm.reduce_scatter_pull((world, 1), stage, torch.bfloat16, [out], postdiv=float(world), tma=False)) * 1e-3) / 1e9
             r[f"rs_tma_c{c}"] = bus / (timeit(lambda: cm.reduce_scatter_pull((world, 1), stage, torch.bfloat16, [out], postdiv=float(world), tma=True)) * 1e-3) / 1e9
+        for c, cm in nvls.items():
+            r[f"ag_nvls_c{c}"] = bus / (timeit(lambda: cm.all_gather_nvls((world, 1), shard, nvls_off[c], torch.bfloat16)) * 1e-3) / 1e9
         cm0 = next(iter(comms.values()))
         stage0, dst0 = offs[next(iter(comms))]
         cm0.view(stage0, n * world, torch.bfloat16).copy_(flat)
         r["ag_ce"] = bus / (timeit(lambda: cm0.all_gather_ce((world, 1), shard, dst0)) * 1e-3) / 1e9
         r["rs_ce"] = bus / (timeit(lambda: cm0.reduce_scatter_ce((world, 1), stage0, torch.bfloat16, dst0, out, postdiv=float(world))) * 1e-3) / 1e9
-        r["ag_ours_gbs"] = max(r[f"ag_ours_c{c}"] for c in comms)
+        r["ag_ours_gbs"] = max([r[f"ag_ours_c{c}"] for c in comms] + [r[f"ag_nvls_c{c}"] for c in nvls])
         r["rs_ours_gbs"] = max(max(r[f"rs_push_c{c}"], r[f"rs_pull_c{c}"], r[f"rs_tma_c{c}"]) for c in comms)
+        r["ag_frac_of_measured"] = r["ag_ours_gbs"] / NVLINK_MEASURED_GBS
+        r["rs_frac_of_measured"] = r["rs_ours_gbs"] / NVLINK_MEASURED_GBS
         r["ag_nccl_gbs"] = bus / (timeit(lambda: dist.all_gather_into_tensor(full, shard)) * 1e-3) / 1e9
         r["rs_nccl_gbs"] = bus / (timeit(lambda: dist.reduce_scatter_tensor(out_bf, flat)) * 1e-3) / 1e9
-        res.append({k: (round(v, 1) if isinstance(v, float) else v) for k, v in r.items()})
-    for cm in comms.values():
+        res.append({k: (round(v, 3 if "frac" in k else 1) if isinstance(v, float) else v) for k, v in r.items()})
+    for cm in list(comms.values()) + list(nvls.values()):
         cm.close()
     if rank == 0:
         best = max(res, key=lambda r: r["ag_ours_gbs"])
         return {"metric": "AG/RS bus GB/s vs 900 GB/s NVLink", "value": best["ag_ours_gbs"],
                 "unit": "GB/s (AG busbw, best size)", "n_gpus": world, "sweep": res,
+                "nvls": bool(nvls) or DeviceComm.last_nvls_error,
+                "peak": {"nominal_gbs": 900.0, "measured_peer_copy_gbs": NVLINK_MEASURED_GBS,
+                         "source": "B200_PROFILING.md: peer copy 770 GB/s per direction on this pool"},
+                "best": {"ag_gbs": best["ag_ours_gbs"], "ag_frac_of_measured": best["ag_frac_of_measured"],
+                         "ag_frac_of_nominal": round(best["ag_ours_gbs"] / 900.0, 3),
+                         "rs_gbs": max(r["rs_ours_gbs"] for r in res),
+                         "rs_frac_of_measured": round(max(r["rs_ours_gbs"] for r in res) / NVLINK_MEASURED_GBS, 3),
+                         "rs_frac_of_nominal": round(max(r["rs_ours_gbs"] for r in res) / 900.0, 3)},
                 "higher_is_better": True}
     return None
+
+
+def run_copy(args):
+    """HBM roofline of the flat-parameter layout kernels on one GPU, on the
+    real unit layouts of `--config` (one transformer block = one FSDP unit).
+
+    Each case is timed per launch with CUDA events on the launching stream,
+    L2 flushed (256 MiB memset) before every launch; bytes are algorithmic
+    (every source byte read once, every destination byte written once, plus
+    the destination read when accumulating)."""
+    import torch
+    rank, world, local = dist_env()
+    if rank != 0:
+        return None
+    torch.cuda.set_device(local)
+    from paper_2304_11277_b200 import kernels
+    from paper_2304_11277_b200.workloads import CONFIGS, T5_CONFIGS, Block, T5DecoderBlock
+    dev = torch.device("cuda", local)
+    if args.config in T5_CONFIGS:
+        c = T5_CONFIGS[args.config]
+        with torch.device("meta"):
+            unit = T5DecoderBlock(c)
+    else:
+        c = CONFIGS[args.config]
+        with torch.device("meta"):
+            unit = Block(c.d, c.heads)
+    shapes = [tuple(p.shape) for p in unit.parameters()]
+    numels = [int(torch.Size(s).numel()) for s in shapes]
+    offsets, o = [], 0
+    for n in numels:
+        offsets.append(o)
+        o += n
+    raw = o
+    F = 8
+    psi = -(-raw // F) * F
+    hbm_peak, _, peak_kind = load_peaks()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    p32 = [torch.randn(s, device=dev) for s in shapes]
+    g16 = [torch.randn(s, device=dev).to(torch.bfloat16) for s in shapes]
+    flat32 = torch.empty(psi, device=dev)
+    flat16 = torch.empty(psi, dtype=torch.bfloat16, device=dev)
+    out32 = [torch.empty(s, device=dev) for s in shapes]
+    shard32 = torch.empty(psi // F, device=dev)
+    big32 = torch.randn(psi, device=dev)
+    big16 = torch.empty(psi, dtype=torch.bfloat16, device=dev)
+
+    cases = [
+        ("flatten f32->f32 (materialise, deferred_init.py:156)",
+         lambda: kernels.flatten(p32, offsets, flat32), raw * 4 + psi * 4),
+        ("flatten bf16->bf16 (grad write-back into the gradient slot, flatparam.py:167)",
+         lambda: kernels.flatten(g16, offsets, flat16), raw * 2 + psi * 2),
+        ("flatten bf16->f32 (W=1 write-back = reduction)",
+         lambda: kernels.flatten(g16, offsets, flat32), raw * 2 + psi * 4),
+        ("flatten bf16->f32 accumulate (engine.py:534)",
+         lambda: kernels.flatten(g16, offsets, flat32, accumulate=True), raw * 2 + psi * 8),
+        ("unflatten f32->f32 (gather_full_params, engine.py:824)",
+         lambda: kernels.unflatten(flat32, out32, offsets), raw * 8),
+        ("shard_copy f32 F=8 (FlatParameter.shard, flatparam.py:139)",
+         lambda: kernels.shard_copy(big32, shard32, 3), (psi // F) * 8),
+        ("cast f32->bf16 (engine.py:661)",
+         lambda: kernels.cast(big32, big16), psi * 6),
+    ]
+    s = torch.cuda.current_stream()
+    res = []
+    for name, fn, nbytes in cases:
+        for _ in range(args.warmup):
+            fn()
+        times = []
+        for _ in range(max(args.steps, 5)):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            fn()
+            b.record(s)
+            times.append((a, b))
+        torch.cuda.synchronize()
+        ms = statistics.median(x.elapsed_time(y) for x, y in times)
+        gbs = nbytes / (ms * 1e-3) / 1e9
+        res.append({"kernel": name, "bytes": int(nbytes), "ms": round(ms, 4),
+                    "gbs": round(gbs, 1), "frac": round(gbs / hbm_peak, 4)})
+    return {"metric": "layout-kernel HBM GB/s vs measured peak", "n_gpus": 1,
+            "config": {"workload": f"{args.config} unit layout: {len(shapes)} tensors, "
+                                   f"raw {raw}, psi {psi} (F={F})", "l2": "flushed before every launch"},
+            "peak": hbm_peak, "peak_kind": peak_kind, "unit": "GB/s", "cases": res,
+            "value": round(min(r["frac"] for r in res), 4), "higher_is_better": True}
 
 
 def main():
@@ -465,6 +569,8 @@ def main():
         out = run_reference(args)
     elif args.mode == "sweep":
         out = run_sweep(args)
+    elif args.mode == "copy":
+        out = run_copy(args)
     else:
         out = run_ours(args)
     if out is not None:

@@ -219,6 +219,47 @@ int fsdp_allreduce(fsdp_comm_t* c, int channel, int gsize, int gstride, const vo
 int fsdp_allreduce_scalar(fsdp_comm_t* c, const float* const* ins, float* const* outs,
                           void* stream);
 
+
+/* ------------------------------------------------------------------------
+ * VMM pool + NVLink SHARP (NVLS) multicast                (B200 + NVSwitch)
+ *
+ * A VMM communicator's pool is one exportable cuMemCreate allocation per
+ * rank; peers map it from the exported handle (replacing cudaMalloc +
+ * cudaIpc*).  Its pool can then be bound whole to the multicast object of
+ * the rank's shard group (consecutive groups of gsize ranks), so a single
+ * multimem.st lands at the same pool offset in every member.  Setup order
+ * (every rank; the host exchanges the 64-byte handles — for
+ * FSDP_HANDLE_POSIX_FD the first int is a file descriptor that the host
+ * must pass to the peer process, e.g. SCM_RIGHTS):
+ *   create_vmm -> export_pool -> import_pool(every peer)
+ *   leader: nvls_create -> (handle) -> members: nvls_import
+ *   all: nvls_add_device -> barrier -> all: nvls_bind
+ * ---------------------------------------------------------------------- */
+enum { FSDP_HANDLE_FABRIC = 1, FSDP_HANDLE_POSIX_FD = 2 };
+#define FSDP_SHAREABLE_BYTES 64
+
+/* 1 if `device` supports multicast objects and VMM, else 0. */
+int fsdp_nvls_supported(int device);
+int fsdp_comm_create_vmm(int rank, int world, int64_t pool_bytes, int max_ctas, int handle_type,
+                         fsdp_comm_t** out);
+int fsdp_comm_export_pool(fsdp_comm_t* c, void* handle_out /* FSDP_SHAREABLE_BYTES */);
+int fsdp_comm_import_pool(fsdp_comm_t* c, int r, const void* handle);
+int fsdp_nvls_create(fsdp_comm_t* c, int gsize, void* handle_out);
+int fsdp_nvls_import(fsdp_comm_t* c, int gsize, const void* handle);
+int fsdp_nvls_add_device(fsdp_comm_t* c);
+int fsdp_nvls_bind(fsdp_comm_t* c);
+/* group size of the bound multicast object, 0 if none */
+int fsdp_nvls_group_size(fsdp_comm_t* c);
+
+/* All-gather through the multicast object (same contract as fsdp_allgather,
+ * real communicator, one shard): member k stores cast(shard) ONCE with
+ * multimem.st at dst_off + k*n*sizeof(dst) and the switch replicates it to
+ * every member.  Falls back to fsdp_allgather when the group is not the
+ * bound shard group, n % 8 != 0 or the buffers are not 16-byte aligned.
+ * Replaces: _issue_unshard cast + AG (engine.py:661-671, collectives.py:288-291). */
+int fsdp_allgather_nvls(fsdp_comm_t* c, int channel, int gsize, int gstride, const void* shard,
+                        int src_dtype, int64_t n, int64_t dst_off, int dst_dtype, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -16,6 +16,7 @@ F32, BF16 = 0, 1
 E_INVALID, E_TIMEOUT, E_IPC, E_UNSUPPORTED = 10001, 10002, 10003, 10004
 CH_AG, CH_RS, CH_AR, CH_SCALAR = 0, 1, 2, 3
 MAX_RANKS, MAX_CTAS, MAX_TENSORS, IPC_HANDLE_BYTES = 8, 160, 96, 64
+HANDLE_FABRIC, HANDLE_POSIX_FD, SHAREABLE_BYTES = 1, 2, 64
 
 
 class FsdpCudaError(RuntimeError):
@@ -82,6 +83,16 @@ _SIGS = {
     "fsdp_allreduce": (_i32, [_vp, _i32, _i32, _i32, _vpp, _i32, _i64, _i64, _i64, _vpp, _f32,
                               _i32, _vp]),
     "fsdp_allreduce_scalar": (_i32, [_vp, _vpp, _vpp, _vp]),
+    "fsdp_nvls_supported": (_i32, [_i32]),
+    "fsdp_comm_create_vmm": (_i32, [_i32, _i32, _i64, _i32, _i32, C.POINTER(_vp)]),
+    "fsdp_comm_export_pool": (_i32, [_vp, _vp]),
+    "fsdp_comm_import_pool": (_i32, [_vp, _i32, _vp]),
+    "fsdp_nvls_create": (_i32, [_vp, _i32, _vp]),
+    "fsdp_nvls_import": (_i32, [_vp, _i32, _vp]),
+    "fsdp_nvls_add_device": (_i32, [_vp]),
+    "fsdp_nvls_bind": (_i32, [_vp]),
+    "fsdp_nvls_group_size": (_i32, [_vp]),
+    "fsdp_allgather_nvls": (_i32, [_vp, _i32, _i32, _i32, _vp, _i32, _i64, _i64, _i32, _vp]),
 }
 
 EXPORTS = tuple(_SIGS)

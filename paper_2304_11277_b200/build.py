@@ -16,7 +16,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["capi.cu", "copy_kernels.cu", "optim_kernels.cu", "comm.cu"]
+SOURCES = ["capi.cu", "copy_kernels.cu", "optim_kernels.cu", "comm.cu", "vmm.cu"]
 LIB = os.path.join(HERE, "_fsdp_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -20,6 +20,8 @@ rank, a non-1-D buffer, or a length not divisible by the group).
 from __future__ import annotations
 
 import ctypes as C
+import os
+import socket
 from typing import Sequence
 
 import torch
@@ -56,6 +58,52 @@ def stream_ptr(stream: torch.cuda.Stream | None) -> int:
     return s.cuda_stream
 
 
+def _fd_passing_ok() -> bool:
+    return hasattr(socket, "send_fds") and hasattr(socket, "AF_UNIX")
+
+
+def _handle_bytes(fd: int) -> bytes:
+    return int(fd).to_bytes(4, "little", signed=True) + bytes(_lib.SHAREABLE_BYTES - 4)
+
+
+class _FdBox:
+    """File-descriptor exchange between the ranks' processes (SCM_RIGHTS over
+    abstract-namespace Unix sockets): the POSIX-fd shareable handles of
+    cuMemExportToShareableHandle are process-local numbers."""
+
+    def __init__(self, token: str, rank: int):
+        self.token, self.rank = token, rank
+        self.sock = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+        self.sock.bind(self._addr(rank))
+        self.sock.listen(64)
+        self.sock.settimeout(120.0)
+
+    def _addr(self, r: int) -> str:
+        return f"\0fsdp-b200-{self.token}-{r}"
+
+    def exchange(self, sends: dict, n_recv: int, tag: int) -> dict:
+        for peer, fd in sends.items():
+            c = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+            c.settimeout(120.0)
+            c.connect(self._addr(peer))
+            socket.send_fds(c, [bytes([tag]) + self.rank.to_bytes(4, "little")], [fd])
+            c.close()
+        got = {}
+        while len(got) < n_recv:
+            conn, _ = self.sock.accept()
+            msg, fds, _, _ = socket.recv_fds(conn, 16, 1)
+            conn.close()
+            if not fds or len(msg) < 5 or msg[0] != tag:
+                for f in fds:
+                    os.close(f)
+                raise RuntimeError("unexpected fd message")
+            got[int.from_bytes(msg[1:5], "little")] = fds[0]
+        return got
+
+    def close(self) -> None:
+        self.sock.close()
+
+
 class DeviceComm:
     def __init__(self, handle: int, rank: int, world: int, emulated: bool, device: torch.device):
         self._h = C.c_void_p(handle)
@@ -74,11 +122,22 @@ class DeviceComm:
 
     # ------------------------------------------------------------ creation --
     @classmethod
-    def create(cls, pool_bytes: int, max_ctas: int = 32, group=None) -> "DeviceComm":
+    def create(cls, pool_bytes: int, max_ctas: int = 32, group=None,
+               nvls_group: int | None = None) -> "DeviceComm":
+        """Real communicator over the ranks of `group`.
+
+        nvls_group=F (F > 1, F | world) first tries an exportable VMM pool
+        bound to the NVLink SHARP multicast object of each consecutive group
+        of F ranks (`all_gather_nvls`); every rank falls back together to the
+        cudaMalloc + CUDA-IPC pool if any step fails anywhere."""
         import torch.distributed as dist
         rank = dist.get_rank(group)
         world = dist.get_world_size(group)
         dev = torch.device("cuda", torch.cuda.current_device())
+        if nvls_group and nvls_group > 1 and world % nvls_group == 0:
+            comm = cls._create_vmm(pool_bytes, max_ctas, group, nvls_group, rank, world, dev)
+            if comm is not None:
+                return comm
         h = C.c_void_p()
         check(lib.fsdp_comm_create(rank, world, pool_bytes, max_ctas, C.byref(h)), "comm_create")
         buf = (C.c_char * _lib.IPC_HANDLE_BYTES)()
@@ -91,6 +150,98 @@ class DeviceComm:
         torch.cuda.synchronize()
         dist.barrier(group=group)          # every pool's flags are zeroed before use
         return cls(h.value, rank, world, False, dev)
+
+    @classmethod
+    def _create_vmm(cls, pool_bytes, max_ctas, group, F, rank, world, dev):
+        """VMM pool + NVLS multicast; None (everyone) if any rank fails."""
+        import torch.distributed as dist
+
+        def agree(ok: bool, what: str) -> bool:
+            st: list = [None] * world
+            dist.all_gather_object(st, (ok, what), group=group)
+            return all(x[0] for x in st)
+
+        err = ""
+        h = C.c_void_p()
+        ok = bool(lib.fsdp_nvls_supported(dev.index)) and _fd_passing_ok()
+        if ok:
+            rc = lib.fsdp_comm_create_vmm(rank, world, pool_bytes, max_ctas, _lib.HANDLE_POSIX_FD,
+                                          C.byref(h))
+            ok = rc == 0
+            err = "" if ok else _lib.last_error()
+        if not agree(ok, err):
+            if ok:
+                lib.fsdp_comm_destroy(h)
+            return None
+        tokens: list = [None] * world
+        dist.all_gather_object(tokens, os.urandom(8).hex(), group=group)
+        box = _FdBox(tokens[0], rank)
+        own_fd = -1
+        try:
+            # 1. pools: every rank's exported fd to every peer
+            buf = (C.c_char * _lib.SHAREABLE_BYTES)()
+            check(lib.fsdp_comm_export_pool(h, buf), "comm_export_pool")
+            own_fd = int.from_bytes(bytes(buf)[:4], "little", signed=True)
+            dist.barrier(group=group)                  # every box is listening
+            got = box.exchange({p: own_fd for p in range(world) if p != rank}, world - 1, tag=0)
+            ok, err = True, ""
+            for p, fd in got.items():
+                rc = lib.fsdp_comm_import_pool(h, p, _handle_bytes(fd))
+                os.close(fd)
+                if rc != 0:
+                    ok, err = False, _lib.last_error()
+            if not agree(ok, err):
+                raise RuntimeError(err or "peer pool import failed")
+            # 2. multicast object of the shard group
+            leader = rank // F * F
+            mc_fd = -1
+            if rank == leader:
+                rc = lib.fsdp_nvls_create(h, F, buf)
+                ok, err = rc == 0, ("" if rc == 0 else _lib.last_error())
+                if ok:
+                    mc_fd = int.from_bytes(bytes(buf)[:4], "little", signed=True)
+            if not agree(ok, err):
+                raise RuntimeError(err or "multicast object creation failed")
+            dist.barrier(group=group)
+            sends = {p: mc_fd for p in range(leader + 1, leader + F)} if rank == leader else {}
+            got = box.exchange(sends, 0 if rank == leader else 1, tag=1)
+            if rank != leader:
+                fd = got[leader]
+                rc = lib.fsdp_nvls_import(h, F, _handle_bytes(fd))
+                os.close(fd)
+                ok, err = rc == 0, ("" if rc == 0 else _lib.last_error())
+            if not agree(ok, err):
+                raise RuntimeError(err or "multicast import failed")
+            rc = lib.fsdp_nvls_add_device(h)
+            if not agree(rc == 0, "" if rc == 0 else _lib.last_error()):
+                raise RuntimeError("cuMulticastAddDevice failed")
+            rc = lib.fsdp_nvls_bind(h)
+            if not agree(rc == 0, "" if rc == 0 else _lib.last_error()):
+                raise RuntimeError("multicast bind failed: " + _lib.last_error())
+            if mc_fd >= 0:
+                os.close(mc_fd)
+        except Exception as exc:  # noqa: BLE001 — every rank reaches here together
+            box.close()
+            if own_fd >= 0:
+                os.close(own_fd)
+            torch.cuda.synchronize()
+            dist.barrier(group=group)
+            lib.fsdp_comm_destroy(h)
+            cls.last_nvls_error = str(exc)
+            return None
+        box.close()
+        if own_fd >= 0:
+            os.close(own_fd)
+        torch.cuda.synchronize()
+        dist.barrier(group=group)
+        return cls(h.value, rank, world, False, dev)
+
+    last_nvls_error = ""
+
+    @property
+    def nvls_group(self) -> int:
+        """Size of the shard group bound to an NVLS multicast object (0: none)."""
+        return int(lib.fsdp_nvls_group_size(self._h))
 
     @classmethod
     def create_emulated(cls, world: int, pool_bytes: int, max_ctas: int = 16) -> "DeviceComm":
@@ -197,6 +348,14 @@ class DeviceComm:
         check(lib.fsdp_allgather_ce(self._h, channel, gdesc[0], gdesc[1], shard.data_ptr(),
                                     dtype_code(shard.dtype), shard.numel(), dst_off,
                                     stream_ptr(stream)), "allgather_ce")
+
+    def all_gather_nvls(self, gdesc, shard: torch.Tensor, dst_off: int, dst_dtype: torch.dtype,
+                        stream=None, channel: int = _lib.CH_AG) -> None:
+        """NVLS multicast all-gather (fused cast); same contract as all_gather,
+        falls back to it inside the library when the group is not the bound one."""
+        check(lib.fsdp_allgather_nvls(self._h, channel, gdesc[0], gdesc[1], shard.data_ptr(),
+                                      dtype_code(shard.dtype), shard.numel(), dst_off,
+                                      dtype_code(dst_dtype), stream_ptr(stream)), "allgather_nvls")
 
     def reduce_scatter_ce(self, gdesc, src_off: int, src_dtype: torch.dtype, stage_off: int,
                           out: torch.Tensor, prediv: float = 1.0, postdiv: float = 1.0,

@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "vmm.h"
 
 namespace fsdp {
 
@@ -58,6 +59,7 @@ struct CollParams {
   int64_t timeout_ns;
   int split;        // 1: waits live in 1-CTA enter/exit kernels, data kernels only signal
   int data_ctas;    // exit kernel: grid of the data kernel it waits for
+  char* mc_base;    // NVLS multicast VA of the pool (shard group), or null
 };
 
 // flag slot (CTA index) reserved for the whole-collective enter barrier
@@ -165,21 +167,6 @@ template <> __device__ __forceinline__ void st8<float>(float* p, const Packed8<f
 }
 template <> __device__ __forceinline__ void st8<__nv_bfloat16>(__nv_bfloat16* p, const Packed8<__nv_bfloat16>& v) {
   reinterpret_cast<uint4*>(p)[0] = v.a;
-}
-template <typename T> __device__ __forceinline__ V8F unpack8(const Packed8<T>& r);
-template <> __device__ __forceinline__ V8F unpack8<float>(const Packed8<float>& r) {
-  V8F x;
-  x.v[0] = __uint_as_float(r.a.x); x.v[1] = __uint_as_float(r.a.y);
-  x.v[2] = __uint_as_float(r.a.z); x.v[3] = __uint_as_float(r.a.w);
-  x.v[4] = __uint_as_float(r.b.x); x.v[5] = __uint_as_float(r.b.y);
-  x.v[6] = __uint_as_float(r.b.z); x.v[7] = __uint_as_float(r.b.w);
-  return x;
-}
-template <> __device__ __forceinline__ V8F unpack8<__nv_bfloat16>(const Packed8<__nv_bfloat16>& r) {
-  V8F x;
-  x.v[0] = bf16lo(r.a.x); x.v[1] = bf16hi(r.a.x); x.v[2] = bf16lo(r.a.y); x.v[3] = bf16hi(r.a.y);
-  x.v[4] = bf16lo(r.a.z); x.v[5] = bf16hi(r.a.z); x.v[6] = bf16lo(r.a.w); x.v[7] = bf16hi(r.a.w);
-  return x;
 }
 template <typename Tin, typename Tout>
 __device__ __forceinline__ Packed8<Tout> convert8(const Packed8<Tin>& r) {
@@ -344,6 +331,53 @@ allgather_kernel(const __grid_constant__ CollParams p) {
   }
   if (p.split) cta_signal(p, g, 1, true);     // my pieces have landed everywhere
   else cta_barrier(p, g, 1, true);            // all members' pieces have landed here
+}
+
+// ------------------------------------------------- all-gather (NVLS) -----
+// NVLink SHARP multicast: the pool of every member of the shard group is
+// bound to one multicast object, so ONE multimem.st from the member at
+// position k writes its (cast) shard into every member's unsharded buffer at
+// dst_off + k*n: egress per GPU is the shard once (S/W) instead of W-1 copies,
+// and each vector costs one store instruction instead of W.  Bit-exact (pure
+// copy + RNE cast).  Split mode only: enter barrier (slots free everywhere),
+// this signal-only kernel, exit barrier (every member's stores landed).
+__device__ __forceinline__ void multimem_st16(void* p, const uint4& v) {
+  asm volatile("multimem.st.global.v4.f32 [%0], {%1,%2,%3,%4};"
+               :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+template <typename T> __device__ __forceinline__ void mc_st8(T* p, const Packed8<T>& v);
+template <> __device__ __forceinline__ void mc_st8<float>(float* p, const Packed8<float>& v) {
+  multimem_st16(p, v.a);
+  multimem_st16(p + 4, v.b);
+}
+template <> __device__ __forceinline__ void mc_st8<__nv_bfloat16>(__nv_bfloat16* p,
+                                                                  const Packed8<__nv_bfloat16>& v) {
+  multimem_st16(p, v.a);
+}
+
+template <typename Tin, typename Tout>
+__global__ void __launch_bounds__(kCommThreads)
+allgather_nvls_kernel(const __grid_constant__ CollParams p) {
+  const Group g = make_group(p);
+  const Tin* __restrict__ src = (const Tin*)p.in[0];
+  const int64_t n = p.n;
+  Tout* dst = (Tout*)(p.mc_base + p.off_a + (int64_t)g.pos * n * (int64_t)sizeof(Tout));
+  const int64_t ntiles = (n + kTileElems - 1) / kTileElems;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    Packed8<Tout> o[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t i = vec_index(t, u);
+      if (i < n) o[u] = convert8<Tin, Tout>(ldg8<Tin>(src + i));
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t i = vec_index(t, u);
+      if (i < n) mc_st8<Tout>(dst + i, o[u]);
+    }
+  }
+  __threadfence_system();          // each thread orders its own multicast stores
+  cta_signal(p, g, 1, true);       // ... before this CTA's completion flags
 }
 
 // -------------------------------------------------------- reduce-scatter ----
@@ -788,6 +822,16 @@ struct fsdp_comm {
   int ce_split = 1;                           // pieces per peer copy (FSDP_CE_SPLIT, <= 4)
   std::vector<cudaEvent_t> ce_events;
   size_t ce_next = 0;
+  // VMM pool (fsdp_comm_create_vmm): own allocation + peer mappings
+  bool vmm = false;
+  int handle_type = 0;
+  vmm::Mapping own_map;
+  vmm::Mapping peer_map[FSDP_MAX_RANKS];
+  // NVLS: multicast object of this rank's shard group (consecutive mc_gsize ranks)
+  CUmemGenericAllocationHandle mc_handle = 0;
+  vmm::Mapping mc_map;
+  int mc_gsize = 0;
+  bool mc_added = false;
 };
 
 namespace {
@@ -819,6 +863,7 @@ void fill_common(fsdp_comm_t* c, CollParams& p, int channel, int gsize, int gstr
   p.prediv = 1.0f;
   p.postdiv = 1.0f;
   p.timeout_ns = c->timeout_ns;
+  p.mc_base = (char*)c->mc_map.va;
 }
 
 int grid_for(fsdp_comm_t* c, int64_t elems, int kind = -1) {
@@ -1027,16 +1072,24 @@ extern "C" int fsdp_comm_device_error(fsdp_comm_t* c) {
 
 extern "C" int fsdp_comm_destroy(fsdp_comm_t* c) {
   if (!c) return 0;
-  if (!c->emulated)
+  if (c->vmm) {
+    cudaDeviceSynchronize();
+    if (c->mc_map.va) vmm::mc_unbind(c->mc_handle, c->device, &c->mc_map);
+    if (c->mc_handle) vmm::release_handle(c->mc_handle);
+    for (int r = 0; r < c->world; ++r)
+      if (r != c->rank) vmm::unmap(&c->peer_map[r]);
+  } else if (!c->emulated) {
     for (int r = 0; r < c->world; ++r)
       if (r != c->rank && c->bases[r]) cudaIpcCloseMemHandle(c->bases[r]);
+  }
   for (auto& v : c->timed)
     for (auto& pr : v) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
   for (auto e : c->spare) cudaEventDestroy(e);
   for (auto e : c->ce_events) cudaEventDestroy(e);
   for (auto s : c->ce_stream)
     if (s) cudaStreamDestroy(s);
-  cudaFree(c->pool);
+  if (c->vmm) vmm::unmap(&c->own_map);
+  else cudaFree(c->pool);
   delete c;
   return 0;
 }
@@ -1328,4 +1381,130 @@ extern "C" int fsdp_allreduce_scalar(fsdp_comm_t* c, const float* const* ins, fl
   fill_common(c, p, FSDP_CH_SCALAR, c->world, 1, 1);
   for (int e = 0; e < nranks_args(c); ++e) { p.in[e] = ins[e]; p.out[e] = outs[e]; }
   return launch(c, scalar_allreduce_kernel, p, 1, 32, (cudaStream_t)stream);
+}
+
+// ------------------------------------------------------ VMM pool + NVLS ----
+extern "C" int fsdp_nvls_supported(int device) { return vmm::multicast_supported(device); }
+
+extern "C" int fsdp_comm_create_vmm(int rank, int world, int64_t pool_bytes, int max_ctas,
+                                    int handle_type, fsdp_comm_t** out) {
+  if (!out) return fail(FSDP_E_INVALID, "null out");
+  if (world < 1 || world > FSDP_MAX_RANKS || rank < 0 || rank >= world)
+    return fail(FSDP_E_INVALID, "rank/world out of range (world <= 8)");
+  if (max_ctas < 1 || max_ctas > FSDP_MAX_CTAS - 1) return fail(FSDP_E_INVALID, "max_ctas out of range (1..159)");
+  if (handle_type != vmm::kFabric && handle_type != vmm::kPosixFd)
+    return fail(FSDP_E_INVALID, "handle_type must be FSDP_HANDLE_FABRIC or FSDP_HANDLE_POSIX_FD");
+  int device = 0;
+  FSDP_CUDA(cudaGetDevice(&device));
+  size_t gran = 0;
+  if (int rc = vmm::granularity(device, handle_type, world, &gran)) return rc;
+  if (pool_bytes < kReserved) pool_bytes = kReserved;
+  pool_bytes = (int64_t)(((size_t)pool_bytes + gran - 1) / gran * gran);
+  fsdp_comm_t* c = new fsdp_comm_t();
+  c->rank = rank; c->world = world; c->pool_bytes = pool_bytes; c->max_ctas = max_ctas;
+  c->device = device;
+  c->vmm = true;
+  c->handle_type = handle_type;
+  if (int rc = vmm::create(device, (size_t)pool_bytes, handle_type, &c->own_map)) { delete c; return rc; }
+  c->pool = (char*)c->own_map.va;
+  cudaError_t e = cudaMemset(c->pool, 0, kReserved);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) { vmm::unmap(&c->own_map); delete c; return check_cuda(e, "cudaMemset(pool)"); }
+  c->bases[rank] = c->pool;
+  c->opened[rank] = true;
+  *out = c;
+  return 0;
+}
+
+extern "C" int fsdp_comm_export_pool(fsdp_comm_t* c, void* handle_out) {
+  if (!c || !handle_out) return fail(FSDP_E_INVALID, "null argument");
+  if (!c->vmm) return fail(FSDP_E_UNSUPPORTED, "not a VMM communicator");
+  return vmm::export_handle(c->own_map.handle, c->handle_type, handle_out);
+}
+
+extern "C" int fsdp_comm_import_pool(fsdp_comm_t* c, int r, const void* handle) {
+  if (!c || !handle) return fail(FSDP_E_INVALID, "null argument");
+  if (!c->vmm) return fail(FSDP_E_UNSUPPORTED, "not a VMM communicator");
+  if (r < 0 || r >= c->world || r == c->rank) return fail(FSDP_E_INVALID, "bad peer rank");
+  if (c->opened[r]) return 0;
+  if (int rc = vmm::import_map(c->device, handle, c->handle_type, (size_t)c->pool_bytes, &c->peer_map[r]))
+    return rc;
+  c->bases[r] = (char*)c->peer_map[r].va;
+  c->opened[r] = true;
+  return 0;
+}
+
+static int nvls_check(fsdp_comm_t* c, int gsize) {
+  if (!c) return fail(FSDP_E_INVALID, "null communicator");
+  if (!c->vmm) return fail(FSDP_E_UNSUPPORTED, "NVLS needs a VMM communicator (fsdp_comm_create_vmm)");
+  if (gsize < 2 || c->world % gsize) return fail(FSDP_E_INVALID, "NVLS group size must divide the world");
+  if (c->mc_gsize && c->mc_gsize != gsize) return fail(FSDP_E_INVALID, "NVLS group already set up");
+  return 0;
+}
+
+extern "C" int fsdp_nvls_create(fsdp_comm_t* c, int gsize, void* handle_out) {
+  if (int rc = nvls_check(c, gsize)) return rc;
+  if (c->rank % gsize != 0) return fail(FSDP_E_INVALID, "fsdp_nvls_create: only the group leader creates");
+  if (!handle_out) return fail(FSDP_E_INVALID, "null handle_out");
+  if (!c->mc_handle) {
+    if (int rc = vmm::mc_create(gsize, (size_t)c->pool_bytes, c->handle_type, &c->mc_handle)) return rc;
+  }
+  c->mc_gsize = gsize;
+  return vmm::export_handle(c->mc_handle, c->handle_type, handle_out);
+}
+
+extern "C" int fsdp_nvls_import(fsdp_comm_t* c, int gsize, const void* handle) {
+  if (int rc = nvls_check(c, gsize)) return rc;
+  if (c->rank % gsize == 0) return fail(FSDP_E_INVALID, "fsdp_nvls_import: the leader creates");
+  if (!handle) return fail(FSDP_E_INVALID, "null handle");
+  if (!c->mc_handle)
+    if (int rc = vmm::mc_import(handle, c->handle_type, &c->mc_handle)) return rc;
+  c->mc_gsize = gsize;
+  return 0;
+}
+
+extern "C" int fsdp_nvls_add_device(fsdp_comm_t* c) {
+  if (!c || !c->mc_handle) return fail(FSDP_E_INVALID, "fsdp_nvls_add_device: no multicast object");
+  if (c->mc_added) return 0;
+  if (int rc = vmm::mc_add_device(c->mc_handle, c->device)) return rc;
+  c->mc_added = true;
+  return 0;
+}
+
+extern "C" int fsdp_nvls_bind(fsdp_comm_t* c) {
+  if (!c || !c->mc_added) return fail(FSDP_E_INVALID, "fsdp_nvls_bind: add the device first");
+  if (c->mc_map.va) return 0;
+  return vmm::mc_bind_map(c->mc_handle, c->device, c->own_map, &c->mc_map);
+}
+
+extern "C" int fsdp_nvls_group_size(fsdp_comm_t* c) {
+  return (c && c->mc_map.va) ? c->mc_gsize : 0;
+}
+
+extern "C" int fsdp_allgather_nvls(fsdp_comm_t* c, int channel, int gsize, int gstride,
+                                   const void* shard, int src_dtype, int64_t n, int64_t dst_off,
+                                   int dst_dtype, void* stream) {
+  if (int rc = validate_group(c, channel, gsize, gstride)) return rc;
+  const int os = elem_size(dst_dtype);
+  if (n < 0 || !shard || !os || !elem_size(src_dtype))
+    return fail(FSDP_E_INVALID, "fsdp_allgather_nvls: bad args");
+  if (int rc = check_range(c, dst_off, n * gsize * os, "fsdp_allgather_nvls")) return rc;
+  const int64_t my_off = dst_off + (int64_t)(c->rank % gsize) * n * os;
+  const bool usable = c->mc_map.va && gstride == 1 && gsize == c->mc_gsize && n % kVec == 0 &&
+                      aligned16(shard) && my_off % 16 == 0;
+  if (!usable) {   // same contract through the unicast SM kernel
+    const void* shards[1] = {shard};
+    return fsdp_allgather(c, channel, gsize, gstride, shards, src_dtype, n, dst_off, dst_dtype, stream);
+  }
+  CollParams p;
+  fill_common(c, p, channel, gsize, gstride, n);
+  p.in[0] = shard;
+  p.off_a = dst_off;
+  const int grid = grid_for(c, n, FSDP_KIND_AG);
+  void* k = src_dtype == FSDP_F32
+                ? (dst_dtype == FSDP_BF16 ? (void*)allgather_nvls_kernel<float, __nv_bfloat16>
+                                          : (void*)allgather_nvls_kernel<float, float>)
+                : (dst_dtype == FSDP_BF16 ? (void*)allgather_nvls_kernel<__nv_bfloat16, __nv_bfloat16>
+                                          : (void*)allgather_nvls_kernel<__nv_bfloat16, float>);
+  return launch_split(c, FSDP_KIND_AG, k, p, grid, kCommThreads, 0, (cudaStream_t)stream);
 }

@@ -138,6 +138,32 @@ template <> __device__ __forceinline__ void store8<__nv_bfloat16>(__nv_bfloat16*
   st_v4(p, v.a);
 }
 
+// Raw (still-packed) 8-element loads: half the registers of V8F for bf16,
+// so more vectors stay in flight per thread.
+template <typename T> __device__ __forceinline__ Packed8<T> ld_raw8(const T* p, int mode);
+template <> __device__ __forceinline__ Packed8<float> ld_raw8<float>(const float* p, int mode) {
+  Packed8<float> r; r.a = ld_mode(p, mode); r.b = ld_mode(p + 4, mode); return r;
+}
+template <> __device__ __forceinline__ Packed8<__nv_bfloat16> ld_raw8<__nv_bfloat16>(
+    const __nv_bfloat16* p, int mode) {
+  Packed8<__nv_bfloat16> r; r.a = ld_mode(p, mode); return r;
+}
+template <typename T> __device__ __forceinline__ V8F unpack8(const Packed8<T>& x);
+template <> __device__ __forceinline__ V8F unpack8<float>(const Packed8<float>& x) {
+  V8F r;
+  r.v[0] = __uint_as_float(x.a.x); r.v[1] = __uint_as_float(x.a.y);
+  r.v[2] = __uint_as_float(x.a.z); r.v[3] = __uint_as_float(x.a.w);
+  r.v[4] = __uint_as_float(x.b.x); r.v[5] = __uint_as_float(x.b.y);
+  r.v[6] = __uint_as_float(x.b.z); r.v[7] = __uint_as_float(x.b.w);
+  return r;
+}
+template <> __device__ __forceinline__ V8F unpack8<__nv_bfloat16>(const Packed8<__nv_bfloat16>& x) {
+  V8F r;
+  r.v[0] = bf16lo(x.a.x); r.v[1] = bf16hi(x.a.x); r.v[2] = bf16lo(x.a.y); r.v[3] = bf16hi(x.a.y);
+  r.v[4] = bf16lo(x.a.z); r.v[5] = bf16hi(x.a.z); r.v[6] = bf16lo(x.a.w); r.v[7] = bf16hi(x.a.w);
+  return r;
+}
+
 template <typename T> __device__ __forceinline__ float to_f(T x);
 template <> __device__ __forceinline__ float to_f<float>(float x) { return x; }
 template <> __device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 x) {
@@ -149,7 +175,7 @@ template <> __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float
   return __float2bfloat16_rn(x);
 }
 
-__device__ __forceinline__ bool aligned16(const void* p) {
+__host__ __device__ __forceinline__ bool aligned16(const void* p) {
   return (reinterpret_cast<uintptr_t>(p) & 15) == 0;
 }
 

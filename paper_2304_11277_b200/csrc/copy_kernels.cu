@@ -1,12 +1,17 @@
 // Flat-parameter layout kernels: flatten (multi-tensor gather + pad + cast,
 // optional accumulate), unflatten (multi-tensor scatter + cast), shard copy
-// and elementwise cast.  HBM-bound: 8-element (16/32-byte) vectors,
-// streaming loads, grid = a multiple of the 148 SMs.
+// and elementwise cast.  HBM-bound: warp-interleaved 8-element vectors
+// (every warp instruction moves one contiguous 256/512-byte span), streaming
+// loads, grid = one resident wave over the 148 SMs.
 //
 // Reference semantics: flatparam.py:88-93 (offsets, padding), :139-147
 // (shard), :159-164 (views), :167-191 (gradient write-back);
 // deferred_init.py:156-176 (materialise by unit), engine.py:661-662 (cast).
 #include "common.cuh"
+
+#include <cstdlib>
+#include <mutex>
+#include <type_traits>
 
 namespace fsdp {
 
@@ -33,129 +38,309 @@ __device__ __forceinline__ int find_tensor(const TensorTable& t, int64_t p, int 
   return lo;
 }
 
-// flat[p] for p in [0, psi): value of the tensor covering p, else 0.
+// ---- warp-interleaved 8-element vectors --------------------------------
+// Vector v of a kernel covers two 4-element quads: elements [a, a+4) and
+// [a+128, a+132) with a = (v/32)*256 + (v%32)*4.  A warp's 32 vectors tile
+// 256 consecutive elements, and every load or store INSTRUCTION of the warp
+// touches one contiguous span (32 x 16 B for fp32, 32 x 8 B for bf16): full
+// 32-byte sectors, no half-sector writes for the 4-byte side of a cast.
+__device__ __forceinline__ int64_t quad0(int64_t v) { return ((v >> 5) << 8) + ((v & 31) << 2); }
+constexpr int64_t kQuadGap = 128;
+constexpr int64_t kVecSpan = kQuadGap + 4;        // a .. a+132
+
+template <typename T> struct Quad;
+template <> struct Quad<float> { uint4 q; };
+template <> struct Quad<__nv_bfloat16> { uint2 q; };
+
+template <typename T> __device__ __forceinline__ Quad<T> ldq(const T* p, bool nc);
+template <> __device__ __forceinline__ Quad<float> ldq<float>(const float* p, bool nc) {
+  Quad<float> r;
+  if (nc) asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(r.q.x), "=r"(r.q.y), "=r"(r.q.z), "=r"(r.q.w) : "l"(p));
+  else asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                    : "=r"(r.q.x), "=r"(r.q.y), "=r"(r.q.z), "=r"(r.q.w) : "l"(p));
+  return r;
+}
+template <> __device__ __forceinline__ Quad<__nv_bfloat16> ldq<__nv_bfloat16>(const __nv_bfloat16* p, bool nc) {
+  Quad<__nv_bfloat16> r;
+  if (nc) asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.q.x), "=r"(r.q.y) : "l"(p));
+  else asm volatile("ld.global.v2.u32 {%0,%1}, [%2];" : "=r"(r.q.x), "=r"(r.q.y) : "l"(p));
+  return r;
+}
+template <typename T> __device__ __forceinline__ void stq(T* p, const Quad<T>& v);
+template <> __device__ __forceinline__ void stq<float>(float* p, const Quad<float>& v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};"
+               :: "l"(p), "r"(v.q.x), "r"(v.q.y), "r"(v.q.z), "r"(v.q.w) : "memory");
+}
+template <> __device__ __forceinline__ void stq<__nv_bfloat16>(__nv_bfloat16* p, const Quad<__nv_bfloat16>& v) {
+  asm volatile("st.global.v2.u32 [%0], {%1,%2};" :: "l"(p), "r"(v.q.x), "r"(v.q.y) : "memory");
+}
+template <typename T> __device__ __forceinline__ float4 q2f(const Quad<T>& x);
+template <> __device__ __forceinline__ float4 q2f<float>(const Quad<float>& x) {
+  return make_float4(__uint_as_float(x.q.x), __uint_as_float(x.q.y), __uint_as_float(x.q.z),
+                     __uint_as_float(x.q.w));
+}
+template <> __device__ __forceinline__ float4 q2f<__nv_bfloat16>(const Quad<__nv_bfloat16>& x) {
+  return make_float4(bf16lo(x.q.x), bf16hi(x.q.x), bf16lo(x.q.y), bf16hi(x.q.y));
+}
+template <typename T> __device__ __forceinline__ Quad<T> f2q(const float4& x);
+template <> __device__ __forceinline__ Quad<float> f2q<float>(const float4& x) {
+  Quad<float> r;
+  r.q = make_uint4(__float_as_uint(x.x), __float_as_uint(x.y), __float_as_uint(x.z), __float_as_uint(x.w));
+  return r;
+}
+template <> __device__ __forceinline__ Quad<__nv_bfloat16> f2q<__nv_bfloat16>(const float4& x) {
+  Quad<__nv_bfloat16> r;
+  r.q = make_uint2(pack_bf16x2(x.x, x.y), pack_bf16x2(x.z, x.w));
+  return r;
+}
 template <typename Tin, typename Tout>
+__device__ __forceinline__ Quad<Tout> convq(const Quad<Tin>& x) {
+  if constexpr (std::is_same<Tin, Tout>::value) return x;
+  else return f2q<Tout>(q2f<Tin>(x));
+}
+template <typename T> __device__ __forceinline__ bool qaligned(const T* p) {
+  return (reinterpret_cast<uintptr_t>(p) & (4 * sizeof(T) - 1)) == 0;
+}
+__device__ __forceinline__ int64_t vec_elem(int64_t a, int k) { return a + (k < 4 ? k : kQuadGap + k - 4); }
+__device__ __forceinline__ float f4get(const float4& f, int k) {
+  return k == 0 ? f.x : (k == 1 ? f.y : (k == 2 ? f.z : f.w));
+}
+__device__ __forceinline__ void f4set(float4& f, int k, float v) {
+  if (k == 0) f.x = v; else if (k == 1) f.y = v; else if (k == 2) f.z = v; else f.w = v;
+}
+
+// Element-wise slow path of flatten for one vector at quad start a: its
+// elements may span tensors / padding / unaligned sources.
+template <typename Tin>
+__device__ __noinline__ void gather_slow(const TensorTable& tab, int64_t a, int64_t psi, int ti,
+                                         float4& lo, float4& hi) {
+  lo = hi = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int k = 0; k < 8; ++k) {
+    const int64_t p = vec_elem(a, k);
+    float val = 0.f;
+    if (p < psi) {
+      int tk = find_tensor(tab, p, ti);
+      const int64_t o = tab.off[tk];
+      if (p >= o && p < o + tab.numel[tk] && tab.ptr[tk] != nullptr)
+        val = to_f<Tin>(((const Tin*)tab.ptr[tk])[p - o]);
+    }
+    if (k < 4) f4set(lo, k, val); else f4set(hi, k - 4, val);
+  }
+}
+
+// flat[p] for p in [0, psi): value of the tensor covering p, else 0 (with
+// kAcc: flat[p] += value, padding untouched).  Each thread handles U
+// grid-strided vectors per iteration and issues all their loads (kept
+// packed) before any store.
+template <typename Tin, typename Tout, bool kAcc, int U>
 __global__ void __launch_bounds__(kCopyThreads)
-flatten_kernel(const __grid_constant__ TensorTable tab, Tout* __restrict__ flat, int64_t psi,
-               int accumulate) {
-  const int64_t nvec = (psi + 7) >> 3;
+flatten_kernel(const __grid_constant__ TensorTable tab, Tout* __restrict__ flat, int64_t psi) {
+  const int64_t nvec = ((psi + 255) >> 8) << 5;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const bool flat_al = qaligned(flat);
   int hint = 0;
-  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += stride) {
-    const int64_t p0 = v << 3;
-    int ti = find_tensor(tab, p0, hint);
-    hint = ti;
-    const Tin* src = (const Tin*)tab.ptr[ti];
-    const int64_t t0 = tab.off[ti], t1 = t0 + tab.numel[ti];
-    const bool full_vec = p0 + 8 <= psi;
-    V8F x;
-    if (full_vec && p0 >= t0 && p0 + 8 <= t1 && src != nullptr && aligned16(src + (p0 - t0))) {
-      x = load8<Tin>(src + (p0 - t0), LD_NC);
-    } else {
-      // mixed vector: elements may span tensors / padding / unaligned sources
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += U * stride) {
+    Quad<Tin> x[U][2];
+    Quad<Tout> y[U][2];
+    bool fast[U];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int64_t p = p0 + k;
-        float val = 0.f;
-        if (p < psi) {
-          int tk = find_tensor(tab, p, ti);
-          const int64_t a = tab.off[tk];
-          if (p >= a && p < a + tab.numel[tk] && tab.ptr[tk] != nullptr)
-            val = to_f<Tin>(((const Tin*)tab.ptr[tk])[p - a]);
+    for (int u = 0; u < U; ++u) {
+      const int64_t vu = v + u * stride;
+      fast[u] = false;
+      if (vu >= nvec) break;
+      const int64_t a = quad0(vu);
+      if (a >= psi) continue;
+      const int ti = find_tensor(tab, a, hint);
+      hint = ti;
+      const Tin* src = (const Tin*)tab.ptr[ti];
+      const int64_t t0 = tab.off[ti], t1 = t0 + tab.numel[ti];
+      fast[u] = a + kVecSpan <= psi && a >= t0 && a + kVecSpan <= t1 && src != nullptr &&
+                qaligned(src + (a - t0)) && flat_al;
+      if (fast[u]) {
+        x[u][0] = ldq<Tin>(src + (a - t0), true);
+        x[u][1] = ldq<Tin>(src + (a - t0) + kQuadGap, true);
+        if (kAcc) {
+          y[u][0] = ldq<Tout>(flat + a, false);
+          y[u][1] = ldq<Tout>(flat + a + kQuadGap, false);
         }
-        x.v[k] = val;
       }
     }
-    Tout* dst = flat + p0;
-    if (full_vec && aligned16(dst)) {
-      if (accumulate) {
-        V8F y = load8<Tout>(dst, LD_PLAIN);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) x.v[k] = __fadd_rn(y.v[k], x.v[k]);
-      }
-      store8<Tout>(dst, pack8<Tout>(x));
-    } else {
-      for (int k = 0; k < 8 && p0 + k < psi; ++k) {
-        float val = x.v[k];
-        if (accumulate) val = __fadd_rn(to_f<Tout>(dst[k]), val);
-        dst[k] = from_f<Tout>(val);
+    for (int u = 0; u < U; ++u) {
+      const int64_t vu = v + u * stride;
+      if (vu >= nvec) break;
+      const int64_t a = quad0(vu);
+      if (a >= psi) continue;
+      if (fast[u]) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (kAcc) {
+            float4 f = q2f<Tin>(x[u][h]);
+            const float4 b = q2f<Tout>(y[u][h]);
+            f.x = __fadd_rn(b.x, f.x); f.y = __fadd_rn(b.y, f.y);
+            f.z = __fadd_rn(b.z, f.z); f.w = __fadd_rn(b.w, f.w);
+            stq<Tout>(flat + a + h * kQuadGap, f2q<Tout>(f));
+          } else {
+            stq<Tout>(flat + a + h * kQuadGap, convq<Tin, Tout>(x[u][h]));
+          }
+        }
+      } else {
+        float4 lo, hi;
+        gather_slow<Tin>(tab, a, psi, find_tensor(tab, a, hint), lo, hi);
+        for (int k = 0; k < 8; ++k) {
+          const int64_t p = vec_elem(a, k);
+          if (p >= psi) continue;
+          float val = k < 4 ? f4get(lo, k) : f4get(hi, k - 4);
+          if (kAcc) val = __fadd_rn(to_f<Tout>(flat[p]), val);
+          flat[p] = from_f<Tout>(val);
+        }
       }
     }
   }
 }
 
-// dst_i[j] = flat[off_i + j]
-template <typename Tin, typename Tout>
+// dst_i[j] = flat[off_i + j]; U vectors per thread per iteration, loads
+// issued before stores.  Vectors cover [off[0], off[n]) from the
+// 256-element block containing off[0].
+template <typename Tin, typename Tout, int U>
 __global__ void __launch_bounds__(kCopyThreads)
 unflatten_kernel(const Tin* __restrict__ flat, const __grid_constant__ TensorTable tab) {
-  const int64_t end = tab.off[tab.n];
-  const int64_t v0 = tab.off[0] >> 3;
-  const int64_t nvec = ((end + 7) >> 3) - v0;
+  const int64_t begin = tab.off[0], end = tab.off[tab.n];
+  const int64_t b0 = begin >> 8;
+  const int64_t nvec = (((end + 255) >> 8) - b0) << 5;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int hint = 0;
-  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += stride) {
-    const int64_t p0 = (v0 + v) << 3;
-    int ti = find_tensor(tab, p0 < tab.off[0] ? tab.off[0] : p0, hint);
-    hint = ti;
-    const int64_t t0 = tab.off[ti], t1 = t0 + tab.numel[ti];
-    Tout* dst = (Tout*)tab.ptr[ti];
-    if (p0 >= t0 && p0 + 8 <= t1 && aligned16(flat + p0) && aligned16(dst + (p0 - t0))) {
-      store8<Tout>(dst + (p0 - t0), pack8<Tout>(load8<Tin>(flat + p0, LD_NC)));
-    } else {
-      for (int k = 0; k < 8; ++k) {
-        const int64_t p = p0 + k;
-        if (p < tab.off[0] || p >= end) continue;
-        int tk = find_tensor(tab, p, ti);
-        const int64_t a = tab.off[tk];
-        if (p >= a && p < a + tab.numel[tk])
-          ((Tout*)tab.ptr[tk])[p - a] = from_f<Tout>(to_f<Tin>(flat[p]));
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += U * stride) {
+    Quad<Tin> x[U][2];
+    bool fast[U];
+    int tis[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t vu = v + u * stride;
+      fast[u] = false;
+      tis[u] = 0;
+      if (vu >= nvec) break;
+      const int64_t a = (b0 << 8) + quad0(vu);
+      const int ti = find_tensor(tab, a < begin ? begin : a, hint);
+      hint = ti;
+      tis[u] = ti;
+      const int64_t t0 = tab.off[ti], t1 = t0 + tab.numel[ti];
+      const Tout* dst = (const Tout*)tab.ptr[ti];
+      fast[u] = a >= t0 && a + kVecSpan <= t1 && qaligned(flat + a) && qaligned(dst + (a - t0));
+      if (fast[u]) {
+        x[u][0] = ldq<Tin>(flat + a, true);
+        x[u][1] = ldq<Tin>(flat + a + kQuadGap, true);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t vu = v + u * stride;
+      if (vu >= nvec) break;
+      const int64_t a = (b0 << 8) + quad0(vu);
+      const int ti = tis[u];
+      if (fast[u]) {
+        Tout* dst = (Tout*)tab.ptr[ti] + (a - tab.off[ti]);
+        stq<Tout>(dst, convq<Tin, Tout>(x[u][0]));
+        stq<Tout>(dst + kQuadGap, convq<Tin, Tout>(x[u][1]));
+      } else {
+        for (int k = 0; k < 8; ++k) {
+          const int64_t p = vec_elem(a, k);
+          if (p < begin || p >= end) continue;
+          int tk = find_tensor(tab, p, ti);
+          const int64_t o = tab.off[tk];
+          if (p >= o && p < o + tab.numel[tk])
+            ((Tout*)tab.ptr[tk])[p - o] = from_f<Tout>(to_f<Tin>(flat[p]));
+        }
       }
     }
   }
 }
 
-// dst[i] = cast(src[i]); vector path when both ends are 16B-aligned.
-template <typename Tin, typename Tout>
+// dst[i] = cast(src[i]) over the same warp-interleaved vectors.
+template <typename Tin, typename Tout, int U>
 __global__ void __launch_bounds__(kCopyThreads)
 cast_kernel(const Tin* __restrict__ src, Tout* __restrict__ dst, int64_t n) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (aligned16(src) && aligned16(dst)) {
-    const int64_t nvec = n >> 3;
-    int64_t v = tid;
-    for (; v + (kCopyUnroll - 1) * stride < nvec; v += kCopyUnroll * stride) {
-      V8F x[kCopyUnroll];
+  const int64_t nvec = ((n + 255) >> 8) << 5;
+  const bool al = qaligned(src) && qaligned(dst);
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += U * stride) {
+    Quad<Tin> x[U][2];
 #pragma unroll
-      for (int u = 0; u < kCopyUnroll; ++u) x[u] = load8<Tin>(src + ((v + u * stride) << 3), LD_NC);
-#pragma unroll
-      for (int u = 0; u < kCopyUnroll; ++u) store8<Tout>(dst + ((v + u * stride) << 3), pack8<Tout>(x[u]));
+    for (int u = 0; u < U; ++u) {
+      const int64_t a = quad0(v + u * stride);
+      if (al && a + kVecSpan <= n) {
+        x[u][0] = ldq<Tin>(src + a, true);
+        x[u][1] = ldq<Tin>(src + a + kQuadGap, true);
+      }
     }
-    for (; v < nvec; v += stride) store8<Tout>(dst + (v << 3), pack8<Tout>(load8<Tin>(src + (v << 3), LD_NC)));
-    for (int64_t i = (nvec << 3) + tid; i < n; i += stride) dst[i] = from_f<Tout>(to_f<Tin>(src[i]));
-  } else {
-    for (int64_t i = tid; i < n; i += stride) dst[i] = from_f<Tout>(to_f<Tin>(src[i]));
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t vu = v + u * stride;
+      if (vu >= nvec) break;
+      const int64_t a = quad0(vu);
+      if (al && a + kVecSpan <= n) {
+        stq<Tout>(dst + a, convq<Tin, Tout>(x[u][0]));
+        stq<Tout>(dst + a + kQuadGap, convq<Tin, Tout>(x[u][1]));
+      } else {
+        for (int k = 0; k < 8; ++k) {
+          const int64_t p = vec_elem(a, k);
+          if (p < n) dst[p] = from_f<Tout>(to_f<Tin>(src[p]));
+        }
+      }
+    }
   }
 }
 
-static int copy_grid(int64_t nvec) {
-  int64_t blocks = (nvec + kCopyThreads - 1) / kCopyThreads;
-  const int64_t cap = (int64_t)kNumSMs * 8;   // 8 x 256-thread CTAs per SM
+static int resident_per_sm(const void* kernel) {
+  static const void* keys[96];
+  static int vals[96];
+  static int used = 0;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  for (int i = 0; i < used; ++i)
+    if (keys[i] == kernel) return vals[i];
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, kCopyThreads, 0) != cudaSuccess || n < 1)
+    n = 2;
+  if (used < 96) { keys[used] = kernel; vals[used] = n; ++used; }
+  return n;
+}
+
+// Grid = one full wave: resident CTAs per SM (from the kernel's register
+// footprint) x 148 SMs, fewer for small inputs.  Grid-stride loops cover
+// the rest, so there is no partial second wave.
+template <typename K>
+static int copy_grid(K kernel, int64_t nvec, int unroll) {
+  const int per_sm = resident_per_sm((const void*)kernel);
+  int64_t blocks = (nvec + (int64_t)kCopyThreads * unroll - 1) / ((int64_t)kCopyThreads * unroll);
+  const int64_t cap = (int64_t)kNumSMs * per_sm;
   if (blocks > cap) blocks = cap;
   return blocks < 1 ? 1 : (int)blocks;
 }
 
 template <typename Tin, typename Tout>
 static void launch_flatten(const TensorTable& t, void* flat, int64_t psi, int acc, cudaStream_t s) {
-  flatten_kernel<Tin, Tout><<<copy_grid((psi + 7) >> 3), kCopyThreads, 0, s>>>(t, (Tout*)flat, psi, acc);
+  const int64_t nvec = ((psi + 255) >> 8) << 5;
+  if (acc) {
+    auto k = flatten_kernel<Tin, Tout, true, kCopyUnroll>;
+    k<<<copy_grid(k, nvec, kCopyUnroll), kCopyThreads, 0, s>>>(t, (Tout*)flat, psi);
+  } else {
+    auto k = flatten_kernel<Tin, Tout, false, kCopyUnroll>;
+    k<<<copy_grid(k, nvec, kCopyUnroll), kCopyThreads, 0, s>>>(t, (Tout*)flat, psi);
+  }
 }
 template <typename Tin, typename Tout>
 static void launch_unflatten(const void* flat, const TensorTable& t, cudaStream_t s) {
-  int64_t span = ((t.off[t.n] + 7) >> 3) - (t.off[0] >> 3);
-  unflatten_kernel<Tin, Tout><<<copy_grid(span), kCopyThreads, 0, s>>>((const Tin*)flat, t);
+  const int64_t nvec = (((t.off[t.n] + 255) >> 8) - (t.off[0] >> 8)) << 5;
+  auto k = unflatten_kernel<Tin, Tout, kCopyUnroll>;
+  k<<<copy_grid(k, nvec, kCopyUnroll), kCopyThreads, 0, s>>>((const Tin*)flat, t);
 }
 template <typename Tin, typename Tout>
 static void launch_cast(const void* src, void* dst, int64_t n, cudaStream_t s) {
-  cast_kernel<Tin, Tout><<<copy_grid((n + 7) >> 3), kCopyThreads, 0, s>>>((const Tin*)src, (Tout*)dst, n);
+  const int64_t nvec = ((n + 255) >> 8) << 5;
+  auto k = cast_kernel<Tin, Tout, kCopyUnroll>;
+  k<<<copy_grid(k, nvec, kCopyUnroll), kCopyThreads, 0, s>>>((const Tin*)src, (Tout*)dst, n);
 }
 
 #define DISPATCH2(sd, dd, FN, ...)                                                         \

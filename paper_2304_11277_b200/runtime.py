@@ -87,7 +87,10 @@ class RuntimeConfig:
     # data movement engine of the collectives.  "ce": copy engines move the
     # bytes (DMA over NVLink, no SMs taken from the concurrent GEMMs; measured
     # lower exposed comm in-step); "sm": push/pull kernels (higher standalone
-    # bandwidth).  Same flag protocol and bits either way.
+    # bandwidth); "nvls" (all-gather only): one multimem.st per vector through
+    # the NVSwitch multicast object of the shard group (needs a DeviceComm
+    # created with nvls_group=F; otherwise the library falls back to "sm").
+    # Same flag protocol and bits either way.
     ag_engine: str = "ce"
     rs_engine: str = "ce"
     optimizer: str = "adam"
@@ -501,6 +504,9 @@ class FSDPRuntime:
                     if self.cfg.ag_engine == "ce" and src.dtype == self.compute_dtype:
                         self.comm.all_gather_ce(self._group_ag(), src, self.slots.offsets[slot],
                                                 stream=self.ag_stream)
+                    elif self.cfg.ag_engine == "nvls":
+                        self.comm.all_gather_nvls(self._group_ag(), src, self.slots.offsets[slot],
+                                                  self.compute_dtype, stream=self.ag_stream)
                     else:
                         self.comm.all_gather(self._group_ag(), [src], self.slots.offsets[slot],
                                              self.compute_dtype, stream=self.ag_stream)

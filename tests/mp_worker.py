@@ -100,6 +100,44 @@ def raw_collectives(rank, world, results):
     results["raw_collectives"] = "bit-exact"
 
 
+def nvls_collectives(rank, world, results):
+    """NVLS multicast all-gather (multimem.st through the NVSwitch): bit-exact
+    vs the oracle, fallback sizes, and a 20-iteration stress on changing data
+    checked against NCCL's all-gather of the same bf16 shards."""
+    from paper_2304_11277_b200 import _lib
+    from paper_2304_11277_b200.comm import DeviceComm
+    if not _lib.lib.fsdp_nvls_supported(torch.cuda.current_device()):
+        results["nvls"] = "unsupported on this device: " + _lib.last_error()
+        return
+    groups = [world] + ([2] if world == 4 else [])
+    for F in groups:
+        comm = DeviceComm.create(256 << 20, max_ctas=32, nvls_group=F)
+        check(comm.nvls_group == F, f"NVLS setup failed (F={F}): {DeviceComm.last_nvls_error}")
+        comm.set_timeout_ms(20000)
+        a = comm.alloc(128 << 20)
+        for n in (8, 1000, 262144 + 8, 4 << 20):
+            rngs = [np.random.default_rng(7000 * r + n) for r in range(world)]
+            shards = [g.standard_normal(n).astype(np.float32) for g in rngs]
+            comm.all_gather_nvls((F, 1), torch.from_numpy(shards[rank]).cuda(), a, torch.bfloat16)
+            got = comm.view(a, n * F, torch.bfloat16).float().cpu().numpy()
+            g0 = rank // F * F
+            check(np.array_equal(got, sp.cast(sp.all_gather(shards[g0:g0 + F]), sp.BF16)),
+                  f"AG-NVLS F={F} n={n}")
+        if F == world:
+            n = 8 << 20
+            ref = torch.empty(n * world, dtype=torch.bfloat16, device="cuda")
+            for it in range(20):
+                x = torch.randn(n, device="cuda", generator=torch.Generator("cuda").manual_seed(rank * 100 + it))
+                comm.all_gather_nvls((world, 1), x, a, torch.bfloat16)
+                dist.all_gather_into_tensor(ref, x.to(torch.bfloat16))
+                torch.cuda.current_stream().synchronize()
+                check(torch.equal(comm.view(a, n * world, torch.bfloat16), ref), f"AG-NVLS stress it={it}")
+        torch.cuda.synchronize()
+        check(comm.device_error() == 0, "device error word (NVLS)")
+        comm.close()
+    results["nvls"] = f"bit-exact (groups {groups})"
+
+
 def fsdp_step_parity(rank, world, strategy, hybrid, results, backend="ipc", opt_in_bwd=False,
                      engine="ce"):
     from paper_2304_11277_b200 import kernels  # noqa: F401
@@ -113,7 +151,7 @@ def fsdp_step_parity(rank, world, strategy, hybrid, results, backend="ipc", opt_
                                     mixed_precision=MixedPrecision(param_dtype=torch.bfloat16),
                                     hybrid_shard_size=hybrid, comm_backend=backend, lr=1e-3,
                                     optimizer_in_backward=opt_in_bwd, ag_engine=engine,
-                                    rs_engine=engine)
+                                    rs_engine="sm" if engine == "nvls" else engine)
     plan = fsdp.plan
     ref = init_gpt_(GPT(cfg), seed=0).cuda().to(torch.bfloat16)
     x, y = synthetic_batch(cfg, 2, seed=100 + rank, device="cuda")
@@ -341,6 +379,7 @@ def main():
     ok = True
     try:
         raw_collectives(rank, world, results)
+        nvls_collectives(rank, world, results)
         session_parity(rank, world, results)
         cases =[("FULL_SHARD", None), ("SHARD_GRAD_OP", None), ("NO_SHARD", None)]
         if world == 4:
@@ -349,6 +388,9 @@ def main():
             fsdp_step_parity(rank, world, strat, hyb, results)
         fsdp_step_parity(rank, world, "FULL_SHARD", None, results, opt_in_bwd=True)
         fsdp_step_parity(rank, world, "FULL_SHARD", None, results, engine="sm")
+        fsdp_step_parity(rank, world, "FULL_SHARD", None, results, engine="nvls")
+        if world == 4:
+            fsdp_step_parity(rank, world, "HYBRID_SHARD", 2, results, engine="nvls")
         if world == 4:
             fsdp_step_parity(rank, world, "HYBRID_SHARD", 2, results, engine="sm")
         if world == 4:

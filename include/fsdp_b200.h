@@ -145,6 +145,11 @@ int fsdp_comm_set_timeout_ms(fsdp_comm_t* c, int64_t ms);
  * kernel, read back (and recycled) by fsdp_comm_timing_drain. */
 enum { FSDP_KIND_AG = 0, FSDP_KIND_RS = 1, FSDP_KIND_AR = 2, FSDP_NUM_KINDS = 3 };
 int fsdp_comm_set_mode(fsdp_comm_t* c, int split, int timing);
+/* on == 0: split-mode collectives launch ONLY their data kernel (no enter /
+ * exit barrier kernels).  Profiling harness only: the caller must order the
+ * ranks itself (one process driving every device, synchronising all devices
+ * between collectives), so that nothing ever spins under a profiler. */
+int fsdp_comm_set_barriers(fsdp_comm_t* c, int on);
 /* Grid cap for the data kernels of one collective kind (0 = max_ctas).  Every
  * member of a group must use the same value (per-CTA flags pair by index). */
 int fsdp_comm_set_ctas(fsdp_comm_t* c, int kind, int ctas);

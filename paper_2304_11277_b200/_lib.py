@@ -67,6 +67,7 @@ _SIGS = {
     "fsdp_comm_device_error": (_i32, [_vp]),
     "fsdp_comm_set_timeout_ms": (_i32, [_vp, _i64]),
     "fsdp_comm_set_mode": (_i32, [_vp, _i32, _i32]),
+    "fsdp_comm_set_barriers": (_i32, [_vp, _i32]),
     "fsdp_comm_set_ctas": (_i32, [_vp, _i32, _i32]),
     "fsdp_comm_timing_drain": (_i32, [_vp, _i32, C.POINTER(C.c_float), _i32, C.POINTER(_i32)]),
     "fsdp_comm_destroy": (_i32, [_vp]),

@@ -814,6 +814,7 @@ struct fsdp_comm {
   int64_t timeout_ns = 20LL * 1000 * 1000 * 1000;
   int kind_ctas[FSDP_NUM_KINDS] = {};         // per-kind grid caps (0: max_ctas)
   bool split = true;                          // 1-CTA enter/exit kernels around data kernels
+  bool barriers = true;                       // false: data kernels only (profiling harness)
   bool timing = false;                        // record events around every data kernel
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed[FSDP_NUM_KINDS];
   std::vector<cudaEvent_t> spare;
@@ -907,7 +908,8 @@ int launch_split(fsdp_comm_t* c, int kind, K kernel, CollParams& p, int grid, in
                  size_t smem, cudaStream_t s) {
   p.split = 1;
   p.data_ctas = grid;
-  if (int rc = launch(c, coll_enter_kernel, p, 1, 32, s)) return rc;
+  if (c->barriers)
+    if (int rc = launch(c, coll_enter_kernel, p, 1, 32, s)) return rc;
   cudaEvent_t a = nullptr, b = nullptr;
   if (c->timing) {
     a = take_event(c);
@@ -925,6 +927,7 @@ int launch_split(fsdp_comm_t* c, int kind, K kernel, CollParams& p, int grid, in
     FSDP_CUDA(cudaEventRecord(b, s));
     c->timed[kind].emplace_back(a, b);
   }
+  if (!c->barriers) return 0;
   return launch(c, coll_exit_kernel, p, 1, 256, s);
 }
 
@@ -934,6 +937,12 @@ extern "C" int fsdp_comm_set_ctas(fsdp_comm_t* c, int kind, int ctas) {
   if (!c || kind < 0 || kind >= FSDP_NUM_KINDS || ctas < 0 || ctas > FSDP_MAX_CTAS - 1)
     return fail(FSDP_E_INVALID, "fsdp_comm_set_ctas: bad args");
   c->kind_ctas[kind] = ctas;
+  return 0;
+}
+
+extern "C" int fsdp_comm_set_barriers(fsdp_comm_t* c, int on) {
+  if (!c) return fail(FSDP_E_INVALID, "null communicator");
+  c->barriers = on != 0;
   return 0;
 }
 

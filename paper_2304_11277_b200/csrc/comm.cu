@@ -818,8 +818,10 @@ struct fsdp_comm {
   bool timing = false;                        // record events around every data kernel
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed[FSDP_NUM_KINDS];
   std::vector<cudaEvent_t> spare;
-  // copy-engine path: one side stream per peer (parallel CEs), event pool
-  cudaStream_t ce_stream[FSDP_MAX_RANKS * 4] = {};
+  // copy-engine path: one side stream per (collective kind, peer, piece) —
+  // all-gather and reduce-scatter copies never queue behind each other —
+  // and an event pool
+  cudaStream_t ce_stream[2][FSDP_MAX_RANKS * 4] = {};
   int ce_split = 1;                           // pieces per peer copy (FSDP_CE_SPLIT, <= 4)
   std::vector<cudaEvent_t> ce_events;
   size_t ce_next = 0;
@@ -1095,8 +1097,9 @@ extern "C" int fsdp_comm_destroy(fsdp_comm_t* c) {
     for (auto& pr : v) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
   for (auto e : c->spare) cudaEventDestroy(e);
   for (auto e : c->ce_events) cudaEventDestroy(e);
-  for (auto s : c->ce_stream)
-    if (s) cudaStreamDestroy(s);
+  for (auto& row : c->ce_stream)
+    for (auto s : row)
+      if (s) cudaStreamDestroy(s);
   if (c->vmm) vmm::unmap(&c->own_map);
   else cudaFree(c->pool);
   delete c;
@@ -1242,8 +1245,9 @@ extern "C" int fsdp_reduce_scatter_tma(fsdp_comm_t* c, int channel, int gsize, i
 static int ce_prepare(fsdp_comm_t* c) {
   if (c->ce_events.empty()) {
     if (const char* e = getenv("FSDP_CE_SPLIT")) c->ce_split = std::max(1, std::min(4, atoi(e)));
-    for (int r = 0; r < FSDP_MAX_RANKS * c->ce_split; ++r)
-      FSDP_CUDA(cudaStreamCreateWithFlags(&c->ce_stream[r], cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k)
+      for (int r = 0; r < FSDP_MAX_RANKS * c->ce_split; ++r)
+        FSDP_CUDA(cudaStreamCreateWithFlags(&c->ce_stream[k][r], cudaStreamNonBlocking));
     c->ce_events.resize(256);
     for (auto& e : c->ce_events) FSDP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
@@ -1257,7 +1261,7 @@ static cudaEvent_t ce_event(fsdp_comm_t* c) {
 
 // copies[j] = (dst, src, bytes) for member j (skipped when bytes == 0); each on
 // its own side stream so distinct peers' transfers use distinct copy engines
-static int ce_fork_join(fsdp_comm_t* c, cudaStream_t s, int gsize, void* const* dst,
+static int ce_fork_join(fsdp_comm_t* c, int kind, cudaStream_t s, int gsize, void* const* dst,
                         const void* const* src, size_t bytes) {
   cudaEvent_t fork = ce_event(c);
   FSDP_CUDA(cudaEventRecord(fork, s));
@@ -1269,7 +1273,7 @@ static int ce_fork_join(fsdp_comm_t* c, cudaStream_t s, int gsize, void* const* 
       const size_t off = (size_t)q * piece;
       if (off >= bytes) break;
       const size_t len = std::min(piece, bytes - off);
-      cudaStream_t cs = c->ce_stream[j * k + q];
+      cudaStream_t cs = c->ce_stream[kind][j * k + q];
       FSDP_CUDA(cudaStreamWaitEvent(cs, fork, 0));
       FSDP_CUDA(cudaMemcpyAsync((char*)dst[j] + off, (const char*)src[j] + off, len,
                                 cudaMemcpyDeviceToDevice, cs));
@@ -1305,7 +1309,7 @@ extern "C" int fsdp_allgather_ce(fsdp_comm_t* c, int channel, int gsize, int gst
   }
   cudaEvent_t a = nullptr, b = nullptr;
   if (c->timing) { a = take_event(c); b = take_event(c); FSDP_CUDA(cudaEventRecord(a, s)); }
-  if (int rc = ce_fork_join(c, s, gsize, dst, src, (size_t)n * es)) return rc;
+  if (int rc = ce_fork_join(c, 0, s, gsize, dst, src, (size_t)n * es)) return rc;
   if (c->timing) { FSDP_CUDA(cudaEventRecord(b, s)); c->timed[FSDP_KIND_AG].emplace_back(a, b); }
   if (int rc = launch(c, coll_signal_kernel, p, 1, 32, s)) return rc;
   return launch(c, coll_exit_kernel, p, 1, 256, s);
@@ -1343,7 +1347,7 @@ extern "C" int fsdp_reduce_scatter_ce(fsdp_comm_t* c, int channel, int gsize, in
   }
   cudaEvent_t a = nullptr, b = nullptr;
   if (c->timing) { a = take_event(c); b = take_event(c); FSDP_CUDA(cudaEventRecord(a, s)); }
-  if (int rc = ce_fork_join(c, s, gsize, dst, src, (size_t)n * es)) return rc;
+  if (int rc = ce_fork_join(c, 1, s, gsize, dst, src, (size_t)n * es)) return rc;
   if (c->timing) { FSDP_CUDA(cudaEventRecord(b, s)); c->timed[FSDP_KIND_RS].emplace_back(a, b); }
   if (int rc = launch(c, coll_signal_kernel, p, 1, 32, s)) return rc;   // done reading peers
   const int64_t nv = std::max<int64_t>(1, (n + kVec - 1) / kVec);

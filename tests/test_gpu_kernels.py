@@ -151,3 +151,53 @@ def test_launch_counter_advances(K):
     n0 = _lib.launch_count()
     K.cast(torch.ones(10, device="cuda"), torch.empty(10, device="cuda"))
     assert _lib.launch_count() == n0 + 1
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_layout_kernels_randomized(K, seed):
+    """Random layouts against a plain torch restatement: 1..130 tensors
+    (beyond one launch's table), sizes 0..3000 incl. empty tensors, sources
+    that are views at odd element offsets (scalar paths), odd padding,
+    every dtype pair, plain and accumulate; unflatten into odd-offset views;
+    cast of odd-start slices."""
+    g = torch.Generator().manual_seed(seed)
+    rnd = lambda a, b: int(torch.randint(a, b, (1,), generator=g))  # noqa: E731
+    src_dt = [torch.float32, torch.bfloat16][seed % 2]
+    dst_dt = [torch.float32, torch.bfloat16][(seed // 2) % 2]
+    nt = rnd(1, 131)
+    numels = [rnd(0, 3000) if rnd(0, 4) else rnd(0, 9) for _ in range(nt)]
+    base = torch.randn(sum(numels) + 7 * nt + 8, generator=g).to("cuda", src_dt)
+    ts, cur = [], rnd(0, 8)
+    for n in numels:
+        ts.append(base[cur: cur + n])
+        cur += n + rnd(0, 8)
+    offsets, o = [], 0
+    for n in numels:
+        offsets.append(o)
+        o += n
+    psi = o + rnd(0, 300)
+    ref = torch.zeros(psi, dtype=torch.float32, device="cuda")
+    for t, off in zip(ts, offsets):
+        ref[off: off + t.numel()] = t.float()
+    flat = torch.full((psi,), 5.0, dtype=dst_dt, device="cuda")
+    K.flatten(ts, offsets, flat)
+    assert torch.equal(flat, ref.to(dst_dt)), "flatten"
+    prev = flat.clone()
+    K.flatten(ts, offsets, flat, accumulate=True)
+    assert torch.equal(flat, (prev.float() + ref).to(dst_dt)), "flatten accumulate"
+    # unflatten into views at odd offsets of one buffer
+    obuf = torch.full((sum(numels) + 5 * nt + 8,), -1.0, dtype=src_dt, device="cuda")
+    outs, cur = [], rnd(0, 6)
+    for n in numels:
+        outs.append(obuf[cur: cur + n])
+        cur += n + rnd(0, 6)
+    K.flatten(ts, offsets, flat)
+    K.unflatten(flat, outs, offsets)
+    for t, out in zip(ts, outs):
+        assert torch.equal(out, t.to(dst_dt).to(src_dt)), "unflatten"
+    # cast of an odd-start slice
+    s0 = rnd(0, 9)
+    src = base[s0:]
+    dst = torch.empty(src.numel() + 3, dtype=dst_dt, device="cuda")[3:]
+    K.cast(src, dst)
+    assert torch.equal(dst, src.to(dst_dt)), "cast"

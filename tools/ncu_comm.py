@@ -7,9 +7,10 @@ on every device).  Barrier kernels are switched off
 collectives, so no kernel ever waits on another GPU: safe under ncu's
 kernel serialisation and replay.  Run as
 
-    ncu --metrics gpu__time_duration.sum,nvltx__bytes.sum,nvlrx__bytes.sum,\
-dram__bytes_read.sum,dram__bytes_write.sum -k regex:"allgather|reduce_scatter" \
-        python tools/ncu_comm.py --mb 256
+    ncu --replay-mode application --clock-control none --metrics \
+gpu__time_duration.sum,nvltx__bytes.sum,nvlrx__bytes.sum,dram__bytes_read.sum,\
+dram__bytes_write.sum -k regex:"allgather|reduce_scatter" --csv \
+        python tools/ncu_comm.py --mb 256 --iters 1
 
 Without ncu it prints per-kernel CUDA-event times (all devices concurrently).
 """
@@ -75,6 +76,8 @@ def main():
     ap.add_argument("--mb", type=int, default=256, help="unsharded bf16 bytes per collective (MiB)")
     ap.add_argument("--ctas", type=int, default=64)
     ap.add_argument("--iters", type=int, default=3)
+    ap.add_argument("--kinds", default="allgather_sm,allgather_nvls,reduce_scatter_pull",
+                    help="reduce_scatter_tma waits on peers inside its kernel: not for ncu")
     args = ap.parse_args()
     W = torch.cuda.device_count()
     S = args.mb << 20
@@ -98,6 +101,7 @@ def main():
                                                                      [outs[r]], postdiv=float(W), tma=True),
     }
     res = {"W": W, "unsharded_bytes": S, "bus_bytes_per_rank": S * (W - 1) // W, "ctas": args.ctas}
+    kinds = {k: v for k, v in kinds.items() if k in args.kinds.split(",")}
     for name, fn in kinds.items():
         times = []
         for _ in range(args.iters):

@@ -823,6 +823,7 @@ struct fsdp_comm {
   // and an event pool
   cudaStream_t ce_stream[2][FSDP_MAX_RANKS * 4] = {};
   int ce_split = 1;                           // pieces per peer copy (FSDP_CE_SPLIT, <= 4)
+  bool ce_shared_streams = false;             // FSDP_CE_SHARED_STREAMS=1: AG and RS share side streams
   std::vector<cudaEvent_t> ce_events;
   size_t ce_next = 0;
   // VMM pool (fsdp_comm_create_vmm): own allocation + peer mappings
@@ -1245,6 +1246,7 @@ extern "C" int fsdp_reduce_scatter_tma(fsdp_comm_t* c, int channel, int gsize, i
 static int ce_prepare(fsdp_comm_t* c) {
   if (c->ce_events.empty()) {
     if (const char* e = getenv("FSDP_CE_SPLIT")) c->ce_split = std::max(1, std::min(4, atoi(e)));
+    if (const char* e = getenv("FSDP_CE_SHARED_STREAMS")) c->ce_shared_streams = atoi(e) != 0;
     for (int k = 0; k < 2; ++k)
       for (int r = 0; r < FSDP_MAX_RANKS * c->ce_split; ++r)
         FSDP_CUDA(cudaStreamCreateWithFlags(&c->ce_stream[k][r], cudaStreamNonBlocking));
@@ -1273,7 +1275,7 @@ static int ce_fork_join(fsdp_comm_t* c, int kind, cudaStream_t s, int gsize, voi
       const size_t off = (size_t)q * piece;
       if (off >= bytes) break;
       const size_t len = std::min(piece, bytes - off);
-      cudaStream_t cs = c->ce_stream[kind][j * k + q];
+      cudaStream_t cs = c->ce_stream[c->ce_shared_streams ? 0 : kind][j * k + q];
       FSDP_CUDA(cudaStreamWaitEvent(cs, fork, 0));
       FSDP_CUDA(cudaMemcpyAsync((char*)dst[j] + off, (const char*)src[j] + off, len,
                                 cudaMemcpyDeviceToDevice, cs));

@@ -7,6 +7,9 @@
 // HBM-bound: p, g, m, v read (16 B) + p, m, v written (12 B) [+ 2 B bf16 copy].
 #include "common.cuh"
 
+#include <algorithm>
+#include <cstdlib>
+
 namespace fsdp {
 
 constexpr int kOptThreads = 256;
@@ -38,32 +41,10 @@ adam_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restric
                    (plow == nullptr || aligned16(plow));
   int64_t done = 0;
   if (vec) {
-    // two float4 of each array per thread per iteration, all loads issued
-    // before the math (8 x 16 B in flight per thread)
     const int64_t n4 = n >> 2;
     float4* p4 = (float4*)p; const float4* g4 = (const float4*)g;
     float4* m4 = (float4*)m; float4* v4 = (float4*)v;
-    int64_t i = tid;
-    for (; i + stride < n4; i += 2 * stride) {
-      float4 pp[2], gg[2], mm[2], vv[2];
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int64_t j = i + u * stride;
-        pp[u] = p4[j]; gg[u] = __ldcs(g4 + j); mm[u] = __ldcs(m4 + j); vv[u] = __ldcs(v4 + j);
-      }
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int64_t j = i + u * stride;
-        adam1(pp[u].x, gg[u].x, mm[u].x, vv[u].x, s); adam1(pp[u].y, gg[u].y, mm[u].y, vv[u].y, s);
-        adam1(pp[u].z, gg[u].z, mm[u].z, vv[u].z, s); adam1(pp[u].w, gg[u].w, mm[u].w, vv[u].w, s);
-        p4[j] = pp[u]; __stcs(m4 + j, mm[u]); __stcs(v4 + j, vv[u]);
-        if (plow) {
-          uint2 b = make_uint2(pack_bf16x2(pp[u].x, pp[u].y), pack_bf16x2(pp[u].z, pp[u].w));
-          *(uint2*)(plow + 4 * j) = b;
-        }
-      }
-    }
-    for (; i < n4; i += stride) {
+    for (int64_t i = tid; i < n4; i += stride) {
       float4 pp = p4[i], gg = __ldcs(g4 + i), mm = m4[i], vv = v4[i];
       adam1(pp.x, gg.x, mm.x, vv.x, s); adam1(pp.y, gg.y, mm.y, vv.y, s);
       adam1(pp.z, gg.z, mm.z, vv.z, s); adam1(pp.w, gg.w, mm.w, vv.w, s);
@@ -109,12 +90,10 @@ unscale_kernel(float* __restrict__ g, int64_t n, float inv, float* __restrict__ 
 
 static int opt_grid(int64_t n) {
   int64_t blocks = (n / 4 + kOptThreads - 1) / kOptThreads;
-  static int per_sm = 0;      // one resident wave of adam_kernel
+  static int per_sm = 0;   // CTAs per SM in the grid cap (FSDP_OPT_CTAS_PER_SM, default 8)
   if (per_sm == 0) {
-    int k = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k, adam_kernel, kOptThreads, 0) != cudaSuccess || k < 1)
-      k = 4;
-    per_sm = k;
+    const char* e = getenv("FSDP_OPT_CTAS_PER_SM");
+    per_sm = e ? std::max(1, std::min(32, atoi(e))) : 8;
   }
   const int64_t cap = (int64_t)kNumSMs * per_sm;
   if (blocks > cap) blocks = cap;

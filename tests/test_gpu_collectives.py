@@ -230,3 +230,53 @@ def test_fabric_entry_contract():
         assert out[0].tolist() == [11, 22] and out[1].tolist() == [33, 44]
     finally:
         c.close()
+
+
+def test_full_size_unit_properties():
+    """BASELINE config size (one GPT-1.3B block unit, psi = 50,358,272 at
+    F = W = 8), checked through size-independent properties on an emulated
+    8-rank communicator:
+      * gather(shard_k(flatten(x)) for k) == flatten(x), bit for bit, with
+        the fp32 -> bf16 cast fused (== cast(flatten(x)));
+      * reduce-scatter of W identical bf16 payloads of small integers, / W,
+        returns the payload chunk exactly (every partial sum is exact in
+        fp32), for every rank's chunk."""
+    from paper_2304_11277_b200 import kernels
+    from paper_2304_11277_b200.workloads import CONFIGS
+    cfg = CONFIGS["gpt1.3b"]
+    W = 8
+    d = cfg.d
+    shapes = [(d,), (d,), (3 * d, d), (3 * d,), (d, d), (d,), (d,), (d,), (4 * d, d), (4 * d,),
+              (d, 4 * d), (d,)]
+    numels = [int(np.prod(s)) for s in shapes]
+    raw = sum(numels)
+    psi = -(-raw // W) * W
+    assert raw == cfg.block_params and psi == 50_358_272
+    n = psi // W
+    offsets = list(np.cumsum([0] + numels[:-1]))
+    g = torch.Generator(device="cuda").manual_seed(0)
+    ts = [torch.randn(s, device="cuda", generator=g) for s in shapes]
+    flat = torch.empty(psi, device="cuda")
+    kernels.flatten(ts, offsets, flat)
+    shards = []
+    for k in range(W):
+        sh = torch.empty(n, device="cuda")
+        kernels.shard_copy(flat, sh, k)
+        shards.append(sh)
+    c = make_comm(W, mb=psi * 2 // (1 << 20) + 8)
+    try:
+        c.set_timeout_ms(20000)
+        off = c.alloc(psi * 2)
+        c.all_gather((W, 1), shards, off, torch.bfloat16)
+        exp = flat.to(torch.bfloat16)
+        for r in range(W):
+            assert torch.equal(c.view(off, psi, torch.bfloat16, r), exp), f"AG rank {r}"
+        payload = torch.randint(-64, 64, (psi,), device="cuda", generator=g).to(torch.bfloat16)
+        outs = [torch.empty(n, device="cuda") for _ in range(W)]
+        c.reduce_scatter((W, 1), [payload] * W, off, outs, postdiv=float(W))
+        for r in range(W):
+            assert torch.equal(outs[r], payload[r * n:(r + 1) * n].float()), f"RS rank {r}"
+        torch.cuda.synchronize()
+        assert c.device_error() == 0
+    finally:
+        c.close()

@@ -48,7 +48,10 @@ def parse():
     ap.add_argument("--config", default="gpt1.3b")
     ap.add_argument("--micro", type=int, default=8, help="sequences per GPU per step")
     ap.add_argument("--backend", default="ipc", choices=["ipc", "nccl"])
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference", "torch-unsharded"],
+                    help="torch-unsharded: the same model trained by plain PyTorch on one GPU "
+                         "(fp32 master weights, bf16 autocast, fused torch Adam) -- the "
+                         "denominator of the north star's '>= 90%% of unsharded 1-GPU TFLOPS'")
     ap.add_argument("--mode", default="step", choices=["step", "sweep", "copy"])
     ap.add_argument("--strategy", default="FULL_SHARD")
     ap.add_argument("--hybrid-shard-size", type=int, default=None)
@@ -347,6 +350,63 @@ def run_ours(args):
     return out
 
 
+def run_torch_unsharded(args):
+    """Plain PyTorch, one GPU, no FSDP: the model's parameters live unsharded
+    in fp32 on the device, the step runs under torch.autocast(bf16) with the
+    fused torch.optim.Adam.  Same model, batch, flops formula and timing as
+    run_ours; only rank 0 runs (N > 1 ranks exit)."""
+    import torch
+    rank, world, local = dist_env()
+    if rank != 0:
+        return None
+    torch.cuda.set_device(local)
+    from paper_2304_11277_b200.workloads import CONFIGS, GPT, param_init_fn
+    torch.backends.cuda.matmul.allow_tf32 = True
+    dev = torch.device("cuda", local)
+    cfg = CONFIGS[args.config]
+    with torch.device("meta"):
+        model = GPT(cfg)
+    model = model.to_empty(device=dev)
+    for m in model.modules():
+        param_init_fn(m)
+    opt = torch.optim.Adam(model.parameters(), lr=1e-4, fused=True)
+    B = args.micro
+    g = torch.Generator(device="cpu").manual_seed(1)
+    x = torch.randint(0, cfg.vocab, (B, cfg.seq), generator=g).to(dev)
+    y = torch.randint(0, cfg.vocab, (B, cfg.seq), generator=g).to(dev)
+
+    def step():
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            loss = model(x, y)
+        loss.backward()
+        opt.step()
+        opt.zero_grad(set_to_none=True)
+        return loss
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(args.steps):
+        loss = step()
+    b.record()
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    ms = a.elapsed_time(b) / args.steps
+    tflops = cfg.flops_per_token() * B * cfg.seq / (ms * 1e-3) / 1e12
+    return {"metric": METRIC, "value": round(tflops, 2), "unit": "TFLOP/s (model, one GPU)",
+            "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+            "higher_is_better": True, "impl": "torch-unsharded", "dtype": "bf16 (autocast)",
+            "config": {"workload": f"{cfg.name} unsharded, plain PyTorch (fp32 params, bf16 autocast, "
+                                   f"fused Adam)", "model": cfg.name, "global_batch": B,
+                       "seq_len": cfg.seq},
+            "loss": round(loss.item(), 4), "clocks": clocks,
+            "peak_mem_gb": round(torch.cuda.max_memory_allocated() / 1e9, 2)}
+
+
 def cpu_baseline(cfg, tokens: int, world: int = 1, steps: int = 1, warmup: int = 0) -> dict:
     """The reference algorithm (oracle port) on this box's host cores, one
     bounded sample: `tokens` tokens per simulated rank through the full step."""
@@ -576,6 +636,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         out = run_reference(args)
+    elif args.impl == "torch-unsharded":
+        out = run_torch_unsharded(args)
     elif args.mode == "sweep":
         out = run_sweep(args)
     elif args.mode == "copy":

@@ -83,8 +83,18 @@ _SHIFT = 3.0 * 2.0 ** 51   # deferred_init.py:26-27 round-to-integer trick
 
 
 def init_values(spec: ModelSpec, seed: int) -> dict[str, np.ndarray]:
+    return init_values_for(spec, seed, None)
+
+
+def init_values_for(spec: ModelSpec, seed: int, names) -> dict[str, np.ndarray]:
+    """Replay of the named parameters only (all when `names` is None): the
+    PRNG stream of each parameter is keyed by (seed, name), so a subset
+    replays to the same values as the whole model (deferred_init.py:63-143)."""
     out = {}
+    keep = None if names is None else set(names)
     for name, shape in spec.param_shapes():
+        if keep is not None and name not in keep:
+            continue
         n = math.prod(shape)
         fan_in = shape[-1] if len(shape) > 1 else shape[0]
         rng = named_stream(seed, name)

@@ -26,7 +26,8 @@ import numpy as np
 import torch
 import torch.nn.functional as F
 
-from .data import ModelSpec, batch_stream, init_values  # noqa: F401  (re-exported)
+from .data import ModelSpec, batch_stream, init_values, init_values_for  # noqa: F401  (re-exported)
+from . import kernels
 from .layout import build_unit_layouts
 from .plan import ShardingPlan
 from .runtime import (ACCUM_NO_COMM, ACCUM_OFF, ACCUM_WITH_COMM, NRAF, PREFETCH_POST, RAF,
@@ -212,9 +213,7 @@ class Session:
         self.comm = comm
         self.rt = FSDPRuntime(self.layouts, self.plan, self.rank, rcfg, comm=comm,
                               process_groups=pgs)
-        vals = init_values(spec, seed)                     # deferred_init.py:156-176
-        for uid, lay in enumerate(self.layouts):
-            self.rt.load_unit_values(uid, [torch.from_numpy(vals[o.name]) for o in lay.originals])
+        self.init_stats = self._materialise(config.init_path)
         self.scaler = ShardedGradScaler(config.scaler) if config.use_scaler else None
         self.device = self.rt.device
         self._anchors = [torch.zeros((), device=self.device, requires_grad=True)
@@ -226,6 +225,85 @@ class Session:
         self._makespan = 0.0
         self.compute_dtype = torch.bfloat16 if config.precision.mixed else torch.float32
         torch.cuda.synchronize()
+
+    # -- initialisation (deferred_init.py:156-263) ---------------------------
+    def _materialise(self, path: str) -> dict:
+        """The reference's three materialisation paths, on the device.
+
+        Values come from the same replay (`init_values`: PRNG streams keyed
+        by (seed, name)), so every path yields bit-identical shards
+        (test_acceptance.py:402-433).  They differ in what is resident:
+          deferred : one unit at a time — host replay of the unit, H2D,
+                     flatten into an unsharded psi buffer, shard, free
+                     (materialize_by_unit, :156-176);
+          device   : every unit's unsharded buffer first, then shard them all
+                     (init_unsharded_on_device, :179-208) — peaks at the full
+                     unsharded model;
+          streamed : the whole model replayed into one pinned host arena
+                     (raw, unpadded), then each unit copied H2D into a padded
+                     device buffer and sharded (init_streamed_from_host,
+                     :227-263) — host holds the model, device one unit.
+        Returns device peak bytes above the pre-init level and the host
+        arena's element peak."""
+        rt, spec = self.rt, self.spec
+        dev = rt.device
+        torch.cuda.synchronize(dev)
+        base = torch.cuda.memory_allocated(dev)
+        torch.cuda.reset_peak_memory_stats(dev)
+        host_peak = 0
+        shard_k = self.plan.shard_index(self.rank)
+
+        def finish(uid: int, flat: torch.Tensor) -> None:
+            u = rt.units[uid]
+            kernels.shard_copy(flat, u.master, shard_k)
+            if u.low is not None:
+                kernels.cast(u.master, u.low)
+
+        def flatten_unit(uid: int, vals: dict) -> torch.Tensor:
+            lay = self.layouts[uid]
+            srcs = [torch.from_numpy(np.ascontiguousarray(vals[o.name], dtype=np.float32)).to(dev)
+                    for o in lay.originals]
+            flat = torch.empty(lay.psi, dtype=torch.float32, device=dev)
+            kernels.flatten(srcs, lay.offsets, flat)
+            return flat
+
+        if path == "deferred":
+            for uid, lay in enumerate(self.layouts):
+                vals = init_values_for(spec, self.seed, [o.name for o in lay.originals])
+                finish(uid, flatten_unit(uid, vals))
+                torch.cuda.synchronize(dev)      # the unit's buffers die here
+        elif path == "device":
+            vals = init_values(spec, self.seed)
+            flats = [flatten_unit(uid, vals) for uid in range(len(self.layouts))]
+            for uid, flat in enumerate(flats):
+                finish(uid, flat)
+            torch.cuda.synchronize(dev)
+            del flats
+        else:   # streamed
+            raws = [lay.raw_numel for lay in self.layouts]
+            arena = torch.empty(sum(raws), dtype=torch.float32).pin_memory()
+            host_peak = arena.numel()
+            vals = init_values(spec, self.seed)
+            cur = 0
+            for lay in self.layouts:
+                for o in lay.originals:
+                    n = int(np.prod(o.shape))
+                    arena[cur: cur + n] = torch.from_numpy(
+                        np.ascontiguousarray(vals[o.name], dtype=np.float32).reshape(-1))
+                    cur += n
+            cur = 0
+            for uid, lay in enumerate(self.layouts):
+                flat = torch.empty(lay.psi, dtype=torch.float32, device=dev)
+                flat[: lay.raw_numel].copy_(arena[cur: cur + lay.raw_numel], non_blocking=True)
+                if lay.psi > lay.raw_numel:
+                    flat[lay.raw_numel:].zero_()
+                finish(uid, flat)
+                cur += lay.raw_numel
+                torch.cuda.synchronize(dev)
+            del arena
+        torch.cuda.synchronize(dev)
+        return {"path": path, "device_peak_bytes": torch.cuda.max_memory_allocated(dev) - base,
+                "host_arena_peak_elements": host_peak}
 
     # -- ordering -----------------------------------------------------------
     def _order_for(self, step: int) -> list[int]:

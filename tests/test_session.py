@@ -136,3 +136,33 @@ def test_train_step_validates_micro_batches():
     x, y = np.zeros((8, 4)), np.zeros((8, 2))
     with pytest.raises(EngineError):
         sess.train_step([(x, y), (x, y)])
+
+
+@pytest.mark.gpu
+def test_init_paths_bit_identical_and_resident_memory():
+    """The reference's three materialisation paths (deferred_init.py:156-263,
+    bound by test_acceptance.py:402-433): bit-identical shards; the
+    whole-model path peaks at the full unsharded model on the device, the
+    deferred and streamed paths at about one unit, and only the streamed path
+    holds a host arena (the raw, unpadded model)."""
+    from paper_2304_11277_b200.data import ModelSpec
+    spec = ModelSpec(dims=(1024,) * 9, init="scaled_uniform")       # 8 units of ~1.05 M
+    sess = {p: _session(spec=spec, seed=5, init_path=p) for p in ("deferred", "device", "streamed")}
+    ref = sess["deferred"]
+    for p in ("device", "streamed"):
+        for a, b in zip(ref.rt.units, sess[p].rt.units):
+            assert a.master.cpu().numpy().tobytes() == b.master.cpu().numpy().tobytes(), p
+    vals = sp.eager_param_values(sp.MLPSpec(dims=(1024,) * 9, init="scaled_uniform"), 5)
+    unit_bytes = max(l.psi for l in ref.layouts) * 4
+    model_bytes = sum(l.psi for l in ref.layouts) * 4
+    st = {p: s.init_stats for p, s in sess.items()}
+    assert st["device"]["device_peak_bytes"] >= model_bytes
+    for p in ("deferred", "streamed"):
+        assert st[p]["device_peak_bytes"] < model_bytes / 2, (p, st[p])
+        assert st[p]["device_peak_bytes"] >= unit_bytes
+    assert st["streamed"]["host_arena_peak_elements"] == sum(l.raw_numel for l in ref.layouts)
+    assert st["deferred"]["host_arena_peak_elements"] == 0
+    for uid, lay in enumerate(ref.layouts):      # and they equal the oracle's replay
+        exp = sp.shard(sp.flatten({k: v.astype(np.float32) for k, v in vals.items()}, lay, np.float32),
+                       lay, 0)
+        assert ref.rt.units[uid].master.cpu().numpy().tobytes() == exp.tobytes()

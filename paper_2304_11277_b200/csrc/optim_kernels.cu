@@ -64,6 +64,83 @@ adam_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restric
   }
 }
 
+// TMA-pipelined Adam: p, g, m, v tiles are streamed into a shared-memory
+// ring by 1-D bulk copies (one elected thread, mbarrier transaction counts),
+// so the bytes in flight per SM are set by the ring depth rather than by the
+// registers each thread can hold.  All threads then run the same adam1 math
+// on their float4 of the landed stage and store p, m, v (+ bf16 copy)
+// straight from registers.  Persistent grid: kAdamCtasPerSm CTAs per SM,
+// tiles assigned round-robin.  Same bits as adam_kernel.
+constexpr int kAdamTile = 1024;                       // elements per array per stage
+constexpr int kAdamStages = 4;
+constexpr int kAdamStageBytes = 4 * kAdamTile * 4;    // p, g, m, v
+constexpr int kAdamSmem = kAdamStages * kAdamStageBytes + 64;
+constexpr int kAdamCtasPerSm = 3;
+
+__global__ void __launch_bounds__(kOptThreads)
+adam_tma_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+                float* __restrict__ v, int64_t n, AdamScalars s, const float* __restrict__ skip,
+                __nv_bfloat16* __restrict__ plow) {
+  if (skip != nullptr && *skip > 0.f) return;
+  extern __shared__ __align__(128) unsigned char smem[];
+  float* ring = reinterpret_cast<float*>(smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kAdamStages * kAdamStageBytes);
+  const int64_t ntiles = n / kAdamTile;               // full tiles; the tail is scalar
+  const int64_t mine = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kAdamStages; ++st) mbar_init(&full[st], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int64_t k) {
+    const int st = (int)(k % kAdamStages);
+    const int64_t e0 = (blockIdx.x + k * gridDim.x) * (int64_t)kAdamTile;
+    float* base = ring + st * (4 * kAdamTile);
+    mbar_expect_tx(&full[st], kAdamStageBytes);
+    tma_load_1d(base, p + e0, kAdamTile * 4, &full[st]);
+    tma_load_1d(base + kAdamTile, g + e0, kAdamTile * 4, &full[st]);
+    tma_load_1d(base + 2 * kAdamTile, m + e0, kAdamTile * 4, &full[st]);
+    tma_load_1d(base + 3 * kAdamTile, v + e0, kAdamTile * 4, &full[st]);
+  };
+  if (threadIdx.x == 0)
+    for (int64_t k = 0; k < mine && k < kAdamStages; ++k) issue(k);
+  for (int64_t k = 0; k < mine; ++k) {
+    const int st = (int)(k % kAdamStages);
+    mbar_wait(&full[st], (uint32_t)((k / kAdamStages) & 1));
+    const float* base = ring + st * (4 * kAdamTile);
+    const int64_t e0 = (blockIdx.x + k * gridDim.x) * (int64_t)kAdamTile;
+    const int i = threadIdx.x * 4;                    // kOptThreads * 4 == kAdamTile
+    float4 pp = *reinterpret_cast<const float4*>(base + i);
+    const float4 gg = *reinterpret_cast<const float4*>(base + kAdamTile + i);
+    float4 mm = *reinterpret_cast<const float4*>(base + 2 * kAdamTile + i);
+    float4 vv = *reinterpret_cast<const float4*>(base + 3 * kAdamTile + i);
+    __syncthreads();                                  // stage st fully read: refill it
+    if (threadIdx.x == 0 && k + kAdamStages < mine) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic reads -> async writes
+      issue(k + kAdamStages);
+    }
+    adam1(pp.x, gg.x, mm.x, vv.x, s); adam1(pp.y, gg.y, mm.y, vv.y, s);
+    adam1(pp.z, gg.z, mm.z, vv.z, s); adam1(pp.w, gg.w, mm.w, vv.w, s);
+    const int64_t e = e0 + i;
+    reinterpret_cast<float4*>(p + e)[0] = pp;
+    __stcs(reinterpret_cast<float4*>(m + e), mm);
+    __stcs(reinterpret_cast<float4*>(v + e), vv);
+    if (plow) {
+      uint2 b = make_uint2(pack_bf16x2(pp.x, pp.y), pack_bf16x2(pp.z, pp.w));
+      *reinterpret_cast<uint2*>(plow + e) = b;
+    }
+  }
+  // scalar tail (n % kAdamTile elements), spread over the grid
+  const int64_t t0 = ntiles * kAdamTile;
+  for (int64_t i = t0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float pp = p[i], mm = m[i], vv = v[i];
+    adam1(pp, g[i], mm, vv, s);
+    p[i] = pp; m[i] = mm; v[i] = vv;
+    if (plow) plow[i] = __float2bfloat16_rn(pp);
+  }
+}
+
 __global__ void __launch_bounds__(kOptThreads)
 sgd_kernel(float* __restrict__ p, const float* __restrict__ g, int64_t n, float lr,
            const float* __restrict__ skip, __nv_bfloat16* __restrict__ plow) {
@@ -111,8 +188,25 @@ extern "C" int fsdp_adam_step(float* p, const float* g, float* m, float* v, int6
   if (n == 0) return 0;
   if (!p || !g || !m || !v) return fail(FSDP_E_INVALID, "fsdp_adam_step: null buffer");
   AdamScalars s{lr, b1, omb1, b2, omb2, bc1, bc2, eps};
-  adam_kernel<<<opt_grid(n), kOptThreads, 0, (cudaStream_t)stream>>>(
-      p, g, m, v, n, s, skip_flag, (__nv_bfloat16*)p_lowp);
+  static int use_tma = -1;      // FSDP_ADAM_TMA=0 selects the register-streaming kernel
+  if (use_tma < 0) {
+    const char* e = getenv("FSDP_ADAM_TMA");
+    use_tma = e ? (atoi(e) != 0) : 1;
+    if (use_tma && cudaFuncSetAttribute(adam_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        kAdamSmem) != cudaSuccess)
+      use_tma = 0;
+  }
+  const bool al = aligned16(p) && aligned16(g) && aligned16(m) && aligned16(v) &&
+                  (p_lowp == nullptr || ((uintptr_t)p_lowp & 7) == 0);
+  if (use_tma && al && n >= (int64_t)kAdamTile * kNumSMs) {
+    const int64_t tiles = n / kAdamTile;
+    const int grid = (int)std::min<int64_t>(tiles, (int64_t)kNumSMs * kAdamCtasPerSm);
+    adam_tma_kernel<<<grid, kOptThreads, kAdamSmem, (cudaStream_t)stream>>>(
+        p, g, m, v, n, s, skip_flag, (__nv_bfloat16*)p_lowp);
+  } else {
+    adam_kernel<<<opt_grid(n), kOptThreads, 0, (cudaStream_t)stream>>>(
+        p, g, m, v, n, s, skip_flag, (__nv_bfloat16*)p_lowp);
+  }
   FSDP_LAUNCHED();
   return 0;
 }

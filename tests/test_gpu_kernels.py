@@ -114,12 +114,15 @@ def test_adam_large_with_lowp_and_skip(K):
     g = torch.from_numpy(g0).cuda()
     m, v = torch.zeros_like(p), torch.zeros_like(p)
     low = torch.empty(n, dtype=torch.bfloat16, device="cuda")
-    K.adam_step(p, g, m, v, lr=3e-4, betas=(0.9, 0.95), eps=1e-8, t=1, p_lowp=low)
     pe = p0.copy()
     st = sp.adam_init(n, np.float32)
-    sp.adam_step(pe, g0, st, lr=3e-4, betas=(0.9, 0.95), eps=1e-8)
-    assert p.cpu().numpy().tobytes() == pe.tobytes()
-    assert torch.equal(low, p.to(torch.bfloat16))
+    for t in (1, 2, 3):      # large n: the TMA-pipelined kernel, plus its scalar tail
+        K.adam_step(p, g, m, v, lr=3e-4, betas=(0.9, 0.95), eps=1e-8, t=t, p_lowp=low)
+        sp.adam_step(pe, g0, st, lr=3e-4, betas=(0.9, 0.95), eps=1e-8)
+        assert p.cpu().numpy().tobytes() == pe.tobytes()
+        assert m.cpu().numpy().tobytes() == st["m"].tobytes()
+        assert v.cpu().numpy().tobytes() == st["v"].tobytes()
+        assert torch.equal(low, p.to(torch.bfloat16))
     skip = torch.ones(1, device="cuda")
     before = p.clone()
     K.adam_step(p, g, m, v, lr=3e-4, betas=(0.9, 0.95), eps=1e-8, t=2, skip_flag=skip)

@@ -153,87 +153,99 @@ class DeviceComm:
 
     @classmethod
     def _create_vmm(cls, pool_bytes, max_ctas, group, F, rank, world, dev):
-        """VMM pool + NVLS multicast; None (everyone) if any rank fails."""
+        """VMM pool + NVLS multicast; None on every rank if any rank fails.
+
+        Every phase runs locally under try/except and ends in an all-gather
+        of (ok, message), so all ranks leave together: a local failure never
+        leaves a peer waiting in a different collective."""
         import torch.distributed as dist
 
-        def agree(ok: bool, what: str) -> bool:
+        def agree(ok: bool, what: str) -> tuple[bool, str]:
             st: list = [None] * world
             dist.all_gather_object(st, (ok, what), group=group)
-            return all(x[0] for x in st)
+            bad = [w for o, w in st if not o]
+            return (not bad), (bad[0] if bad else "")
 
-        err = ""
+        def attempt(fn) -> tuple[bool, str]:
+            try:
+                fn()
+                return agree(True, "")
+            except Exception as exc:  # noqa: BLE001 — reported to every rank
+                return agree(False, f"rank {rank}: {exc}")
+
         h = C.c_void_p()
-        ok = bool(lib.fsdp_nvls_supported(dev.index)) and _fd_passing_ok()
-        if ok:
-            rc = lib.fsdp_comm_create_vmm(rank, world, pool_bytes, max_ctas, _lib.HANDLE_POSIX_FD,
-                                          C.byref(h))
-            ok = rc == 0
-            err = "" if ok else _lib.last_error()
-        if not agree(ok, err):
-            if ok:
-                lib.fsdp_comm_destroy(h)
-            return None
-        tokens: list = [None] * world
-        dist.all_gather_object(tokens, os.urandom(8).hex(), group=group)
-        box = _FdBox(tokens[0], rank)
-        own_fd = -1
-        try:
-            # 1. pools: every rank's exported fd to every peer
-            buf = (C.c_char * _lib.SHAREABLE_BYTES)()
+        state = {"own_fd": -1, "mc_fd": -1, "box": None, "created": False}
+
+        def create():
+            if not lib.fsdp_nvls_supported(dev.index):
+                raise RuntimeError("no multicast/VMM support: " + _lib.last_error())
+            if not _fd_passing_ok():
+                raise RuntimeError("no SCM_RIGHTS fd passing")
+            check(lib.fsdp_comm_create_vmm(rank, world, pool_bytes, max_ctas,
+                                           _lib.HANDLE_POSIX_FD, C.byref(h)), "comm_create_vmm")
+            state["created"] = True
+
+        def open_box():
+            tokens: list = [None] * world
+            dist.all_gather_object(tokens, os.urandom(8).hex(), group=group)
+            state["box"] = _FdBox(tokens[0], rank)
+
+        buf = (C.c_char * _lib.SHAREABLE_BYTES)()
+
+        def export_pool():
             check(lib.fsdp_comm_export_pool(h, buf), "comm_export_pool")
-            own_fd = int.from_bytes(bytes(buf)[:4], "little", signed=True)
-            dist.barrier(group=group)                  # every box is listening
-            got = box.exchange({p: own_fd for p in range(world) if p != rank}, world - 1, tag=0)
-            ok, err = True, ""
-            for p, fd in got.items():
-                rc = lib.fsdp_comm_import_pool(h, p, _handle_bytes(fd))
-                os.close(fd)
-                if rc != 0:
-                    ok, err = False, _lib.last_error()
-            if not agree(ok, err):
-                raise RuntimeError(err or "peer pool import failed")
-            # 2. multicast object of the shard group
-            leader = rank // F * F
-            mc_fd = -1
+            state["own_fd"] = int.from_bytes(bytes(buf)[:4], "little", signed=True)
+
+        def import_pools():
+            got = state["box"].exchange({p: state["own_fd"] for p in range(world) if p != rank},
+                                        world - 1, tag=0)
+            try:
+                for p, fd in got.items():
+                    check(lib.fsdp_comm_import_pool(h, p, _handle_bytes(fd)), "comm_import_pool")
+            finally:
+                for fd in got.values():
+                    os.close(fd)
+
+        leader = rank // F * F
+
+        def create_mc():
             if rank == leader:
-                rc = lib.fsdp_nvls_create(h, F, buf)
-                ok, err = rc == 0, ("" if rc == 0 else _lib.last_error())
-                if ok:
-                    mc_fd = int.from_bytes(bytes(buf)[:4], "little", signed=True)
-            if not agree(ok, err):
-                raise RuntimeError(err or "multicast object creation failed")
-            dist.barrier(group=group)
-            sends = {p: mc_fd for p in range(leader + 1, leader + F)} if rank == leader else {}
-            got = box.exchange(sends, 0 if rank == leader else 1, tag=1)
-            if rank != leader:
-                fd = got[leader]
-                rc = lib.fsdp_nvls_import(h, F, _handle_bytes(fd))
-                os.close(fd)
-                ok, err = rc == 0, ("" if rc == 0 else _lib.last_error())
-            if not agree(ok, err):
-                raise RuntimeError(err or "multicast import failed")
-            rc = lib.fsdp_nvls_add_device(h)
-            if not agree(rc == 0, "" if rc == 0 else _lib.last_error()):
-                raise RuntimeError("cuMulticastAddDevice failed")
-            rc = lib.fsdp_nvls_bind(h)
-            if not agree(rc == 0, "" if rc == 0 else _lib.last_error()):
-                raise RuntimeError("multicast bind failed: " + _lib.last_error())
-            if mc_fd >= 0:
-                os.close(mc_fd)
-        except Exception as exc:  # noqa: BLE001 — every rank reaches here together
-            box.close()
-            if own_fd >= 0:
-                os.close(own_fd)
-            torch.cuda.synchronize()
-            dist.barrier(group=group)
-            lib.fsdp_comm_destroy(h)
-            cls.last_nvls_error = str(exc)
-            return None
-        box.close()
-        if own_fd >= 0:
-            os.close(own_fd)
+                check(lib.fsdp_nvls_create(h, F, buf), "nvls_create")
+                state["mc_fd"] = int.from_bytes(bytes(buf)[:4], "little", signed=True)
+
+        def import_mc():
+            sends = ({p: state["mc_fd"] for p in range(leader + 1, leader + F)}
+                     if rank == leader else {})
+            got = state["box"].exchange(sends, 0 if rank == leader else 1, tag=1)
+            try:
+                if rank != leader:
+                    check(lib.fsdp_nvls_import(h, F, _handle_bytes(got[leader])), "nvls_import")
+            finally:
+                for fd in got.values():
+                    os.close(fd)
+
+        phases = [create, open_box, export_pool, import_pools, create_mc, import_mc,
+                  lambda: check(lib.fsdp_nvls_add_device(h), "nvls_add_device"),
+                  lambda: check(lib.fsdp_nvls_bind(h), "nvls_bind")]
+        ok, err = True, ""
+        for i, ph in enumerate(phases):
+            ok, err = attempt(ph)
+            if not ok:
+                break
+            if ph is open_box:
+                dist.barrier(group=group)              # every box is listening
+        if state["box"] is not None:
+            state["box"].close()
+        for k in ("own_fd", "mc_fd"):
+            if state[k] >= 0:
+                os.close(state[k])
         torch.cuda.synchronize()
         dist.barrier(group=group)
+        if not ok:
+            if state["created"]:
+                lib.fsdp_comm_destroy(h)
+            cls.last_nvls_error = err
+            return None
         return cls(h.value, rank, world, False, dev)
 
     last_nvls_error = ""

@@ -799,6 +799,7 @@ struct fsdp_comm {
   cudaStream_t ce_stream[2][FSDP_MAX_RANKS * 4] = {};
   int ce_split = 1;                           // pieces per peer copy (FSDP_CE_SPLIT, <= 4)
   bool ce_shared_streams = false;             // FSDP_CE_SHARED_STREAMS=1: AG and RS share side streams
+  bool ce_serial = false;                     // FSDP_CE_SERIAL=1: one destination at a time
   std::vector<cudaEvent_t> ce_events;
   size_t ce_next = 0;
   // VMM pool (fsdp_comm_create_vmm): own allocation + peer mappings
@@ -1222,6 +1223,7 @@ static int ce_prepare(fsdp_comm_t* c) {
   if (c->ce_events.empty()) {
     if (const char* e = getenv("FSDP_CE_SPLIT")) c->ce_split = std::max(1, std::min(4, atoi(e)));
     if (const char* e = getenv("FSDP_CE_SHARED_STREAMS")) c->ce_shared_streams = atoi(e) != 0;
+    if (const char* e = getenv("FSDP_CE_SERIAL")) c->ce_serial = atoi(e) != 0;
     for (int k = 0; k < 2; ++k)
       for (int r = 0; r < FSDP_MAX_RANKS * c->ce_split; ++r)
         FSDP_CUDA(cudaStreamCreateWithFlags(&c->ce_stream[k][r], cudaStreamNonBlocking));
@@ -1238,10 +1240,26 @@ static cudaEvent_t ce_event(fsdp_comm_t* c) {
 
 // copies[j] = (dst, src, bytes) for member j (skipped when bytes == 0); each on
 // its own side stream so distinct peers' transfers use distinct copy engines
-static int ce_fork_join(fsdp_comm_t* c, int kind, cudaStream_t s, int gsize, void* const* dst,
-                        const void* const* src, size_t bytes) {
+static int ce_fork_join(fsdp_comm_t* c, int kind, cudaStream_t s, int gsize, int pos,
+                        void* const* dst, const void* const* src, size_t bytes) {
   cudaEvent_t fork = ce_event(c);
   FSDP_CUDA(cudaEventRecord(fork, s));
+  if (c->ce_serial) {
+    // one side stream, one destination at a time, staggered (member pos+1
+    // first): every copy gets the whole NVSwitch port, and no two members
+    // start on the same destination
+    cudaStream_t cs = c->ce_stream[c->ce_shared_streams ? 0 : kind][0];
+    FSDP_CUDA(cudaStreamWaitEvent(cs, fork, 0));
+    for (int jj = 0; jj < gsize; ++jj) {
+      const int j = (pos + 1 + jj) % gsize;
+      if (!dst[j] || !bytes) continue;
+      FSDP_CUDA(cudaMemcpyAsync(dst[j], src[j], bytes, cudaMemcpyDeviceToDevice, cs));
+    }
+    cudaEvent_t done = ce_event(c);
+    FSDP_CUDA(cudaEventRecord(done, cs));
+    FSDP_CUDA(cudaStreamWaitEvent(s, done, 0));
+    return 0;
+  }
   const int k = c->ce_split;
   const size_t piece = ((bytes + k - 1) / k + 255) / 256 * 256;
   for (int j = 0; j < gsize; ++j) {
@@ -1286,7 +1304,7 @@ extern "C" int fsdp_allgather_ce(fsdp_comm_t* c, int channel, int gsize, int gst
   }
   cudaEvent_t a = nullptr, b = nullptr;
   if (c->timing) { a = take_event(c); b = take_event(c); FSDP_CUDA(cudaEventRecord(a, s)); }
-  if (int rc = ce_fork_join(c, 0, s, gsize, dst, src, (size_t)n * es)) return rc;
+  if (int rc = ce_fork_join(c, 0, s, gsize, pos, dst, src, (size_t)n * es)) return rc;
   if (c->timing) { FSDP_CUDA(cudaEventRecord(b, s)); c->timed[FSDP_KIND_AG].emplace_back(a, b); }
   if (int rc = launch(c, coll_signal_kernel, p, 1, 32, s)) return rc;
   return launch(c, coll_exit_kernel, p, 1, 256, s);
@@ -1324,7 +1342,7 @@ extern "C" int fsdp_reduce_scatter_ce(fsdp_comm_t* c, int channel, int gsize, in
   }
   cudaEvent_t a = nullptr, b = nullptr;
   if (c->timing) { a = take_event(c); b = take_event(c); FSDP_CUDA(cudaEventRecord(a, s)); }
-  if (int rc = ce_fork_join(c, 1, s, gsize, dst, src, (size_t)n * es)) return rc;
+  if (int rc = ce_fork_join(c, 1, s, gsize, pos, dst, src, (size_t)n * es)) return rc;
   if (c->timing) { FSDP_CUDA(cudaEventRecord(b, s)); c->timed[FSDP_KIND_RS].emplace_back(a, b); }
   if (int rc = launch(c, coll_signal_kernel, p, 1, 32, s)) return rc;   // done reading peers
   const int64_t nv = std::max<int64_t>(1, (n + kVec - 1) / kVec);

@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--rs-ctas", type=int, default=64, help="CTAs of the reduce-scatter data kernel")
     ap.add_argument("--ag-engine", default="ce", choices=["sm", "ce", "nvls"])
     ap.add_argument("--rs-engine", default="ce", choices=["sm", "ce"])
+    ap.add_argument("--tail-engine", default="sm", choices=["sm", "same"],
+                    help="engine of the two collectives nothing overlaps (first AG, last RS)")
     ap.add_argument("--exposed", action="store_true",
                     help="also time the step with collectives replaced by no-ops")
     ap.add_argument("--opt-in-bwd", action="store_true",
@@ -189,7 +191,7 @@ def run_ours(args):
         comm_backend=args.backend, hybrid_shard_size=args.hybrid_shard_size, lr=1e-4,
         optimizer_in_backward=args.opt_in_bwd, forward_prefetch=args.forward_prefetch,
         ag_ctas=args.ctas, rs_ctas=args.rs_ctas, ag_engine=args.ag_engine,
-        rs_engine=args.rs_engine)
+        rs_engine=args.rs_engine, tail_engine=args.tail_engine)
     opt = fsdp.optimizer()
     rt = fsdp.rt
     dev_inputs = tuple(h.to(dev) for h in host)
@@ -226,6 +228,7 @@ def run_ours(args):
     launches = _lib.launch_count() - n_launch0
     ms = t0.elapsed_time(t1) / args.steps
     timers = rt.timer_summary()
+    stall_units = rt.stall_breakdown()
     rt.profile = False
     # e2e: token ids from pinned host memory each step, loss read back each step
     e0 = time.perf_counter()
@@ -266,7 +269,12 @@ def run_ours(args):
     e2e_value = flops_step / (ms_e2e * 1e-3) / 1e12 * world
     hbm_peak, bf16_peak, peak_kind = load_peaks()
     # roofline: the dominant kernel of this library within the step
-    mine = {k: v for k, v in timers.items()}
+    # compute-stream stalls on communication (GPU time, measured around each
+    # wait): the breakdown of exposed comm; not kernels
+    stalls = {k[len("stall_"):]: {"ms_per_step": round(v["total_ms"] / args.steps, 3),
+                                  "count_per_step": round(v["count"] / args.steps, 1)}
+              for k, v in timers.items() if k.startswith("stall_")}
+    mine = {k: v for k, v in timers.items() if not k.startswith("stall_")}
     # dominant SM kernel of this library; collectives moved by copy engines
     # (DMA, no SM code) are reported separately as bus bandwidth
     dma = {k for k in ("allgather", "reduce_scatter")
@@ -328,7 +336,8 @@ def run_ours(args):
                        "model": cfg.name, "global_batch": B * world, "seq_len": seq_len,
                        "parallelism": f"fsdp{world}" if world > 1 else "fsdp1 (NO_SHARD-equivalent)",
                        "comm_backend": args.backend,
-                       "comm_engine": {"allgather": args.ag_engine, "reduce_scatter": args.rs_engine},
+                       "comm_engine": {"allgather": args.ag_engine, "reduce_scatter": args.rs_engine,
+                                       "first_ag_last_rs": args.tail_engine},
                        "l2": "inputs > L2 (weights+state >20 GB)"},
             "tflops_per_gpu": round(tflops_gpu, 2),
             "roofline": roof, "roofline_step": step_roof, "kernels": kern_share,
@@ -336,6 +345,9 @@ def run_ours(args):
                     "h2d_bytes_per_step": int(sum(h.numel() * h.element_size() for h in host)),
                     "d2h_bytes_per_step": 4, "ms_per_step": round(ms_e2e, 3)},
             "gpu_launches": int(launches), "clocks": clocks, "loss": round(losses[-1], 4),
+            **({"comm_stalls": stalls,
+                "comm_stalls_top_units": {k: [{"unit": u, "ms_total": t, "waits": c} for u, t, c in v]
+                                          for k, v in stall_units.items()}} if stalls else {}),
             "peak_mem_gb": round(torch.cuda.max_memory_allocated() / 1e9, 2),
             **({"exposed_comm": {"ms_per_step_without_comm": round(ms_nocomm, 3),
                                  "exposed_ms": round(ms - ms_nocomm, 3),

@@ -239,51 +239,62 @@ __global__ void __launch_bounds__(32) coll_signal_kernel(const __grid_constant__
   }
 }
 
-// Local reduction of a copy-engine reduce-scatter: member chunks j != pos sit
-// in local staging (off_b + j*n), the own chunk in the own payload buffer
-// (off_a + pos*n); ascending-rank fp32 sum from +0, / postdiv, += out.
+// Local reduction of a copy-engine reduce-scatter, one piece [e0, e0+len)
+// of the member's chunk: member chunks j != pos sit in local staging
+// (stage + j*stride), the own chunk in the own payload buffer; ascending-rank
+// fp32 sum from +0, / postdiv, += out.
+struct CeReduceArgs {
+  const void* own;        // own payload, chunk pos (element 0 of the chunk)
+  const void* stage;      // staging base (slot 0, element 0)
+  int64_t stride;         // elements between staging slots (= chunk length n)
+  float* out;             // output chunk (element 0)
+  int64_t e0, len;        // this piece
+  int gsize, pos;
+  float prediv, postdiv;
+  int accumulate;
+};
+
 template <typename Tin>
 __global__ void __launch_bounds__(256)
-ce_reduce_kernel(const __grid_constant__ CollParams p) {
-  const Group g = make_group(p);
-  const int e = p.rank0 >= 0 ? 0 : blockIdx.y;
-  float* __restrict__ out = p.out[e];
-  const int64_t n = p.n;
-  const Tin* own = (const Tin*)(p.bases[g.rank] + p.off_a) + (int64_t)g.pos * n;
-  const Tin* stage = (const Tin*)(p.bases[g.rank] + p.off_b);
-  const bool pre = p.prediv != 1.0f, post = p.postdiv != 1.0f;
+ce_reduce_kernel(const __grid_constant__ CeReduceArgs a) {
+  const Tin* own = (const Tin*)a.own + a.e0;
+  const Tin* stage = (const Tin*)a.stage + a.e0;
+  float* __restrict__ out = a.out + a.e0;
+  const int64_t n = a.len;
+  const bool pre = a.prediv != 1.0f, post = a.postdiv != 1.0f;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const bool vec = (n % kVec == 0) && aligned16(own) && aligned16(stage) && aligned16(out);
+  const bool vec = (n % kVec == 0) && aligned16(own) && aligned16(stage) && aligned16(out) &&
+                   ((a.stride * (int64_t)sizeof(Tin)) % 16 == 0);
   if (vec) {
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v * kVec < n; v += stride) {
       const int64_t i = v * kVec;
       V8F acc;
 #pragma unroll
       for (int q = 0; q < 8; ++q) acc.v[q] = 0.0f;
-      for (int j = 0; j < g.size; ++j) {
-        const V8F x = unpack8<Tin>(j == g.pos ? ldg8<Tin>(own + i) : ldg8<Tin>(stage + (int64_t)j * n + i));
+      for (int j = 0; j < a.gsize; ++j) {
+        const V8F x = unpack8<Tin>(j == a.pos ? ldg8<Tin>(own + i) : ldg8<Tin>(stage + (int64_t)j * a.stride + i));
 #pragma unroll
         for (int q = 0; q < 8; ++q)
-          acc.v[q] = __fadd_rn(acc.v[q], pre ? __fdiv_rn(x.v[q], p.prediv) : x.v[q]);
+          acc.v[q] = __fadd_rn(acc.v[q], pre ? __fdiv_rn(x.v[q], a.prediv) : x.v[q]);
       }
       V8F base;
-      if (p.accumulate) base = unpack8<float>(ldcg8<float>(out + i));
+      if (a.accumulate) base = unpack8<float>(ldcg8<float>(out + i));
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const float r = post ? __fdiv_rn(acc.v[q], p.postdiv) : acc.v[q];
-        acc.v[q] = __fadd_rn(p.accumulate ? base.v[q] : 0.0f, r);
+        const float r = post ? __fdiv_rn(acc.v[q], a.postdiv) : acc.v[q];
+        acc.v[q] = __fadd_rn(a.accumulate ? base.v[q] : 0.0f, r);
       }
       st8<float>(out + i, pack8<float>(acc));
     }
   } else {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
       float acc = 0.0f;
-      for (int j = 0; j < g.size; ++j) {
-        const float x = to_f<Tin>(j == g.pos ? own[i] : stage[(int64_t)j * n + i]);
-        acc = __fadd_rn(acc, pre ? __fdiv_rn(x, p.prediv) : x);
+      for (int j = 0; j < a.gsize; ++j) {
+        const float x = to_f<Tin>(j == a.pos ? own[i] : stage[(int64_t)j * a.stride + i]);
+        acc = __fadd_rn(acc, pre ? __fdiv_rn(x, a.prediv) : x);
       }
-      const float r = post ? __fdiv_rn(acc, p.postdiv) : acc;
-      out[i] = __fadd_rn(p.accumulate ? out[i] : 0.0f, r);
+      const float r = post ? __fdiv_rn(acc, a.postdiv) : acc;
+      out[i] = __fadd_rn(a.accumulate ? out[i] : 0.0f, r);
     }
   }
 }
@@ -799,7 +810,11 @@ struct fsdp_comm {
   cudaStream_t ce_stream[2][FSDP_MAX_RANKS * 4] = {};
   int ce_split = 1;                           // pieces per peer copy (FSDP_CE_SPLIT, <= 4)
   bool ce_shared_streams = false;             // FSDP_CE_SHARED_STREAMS=1: AG and RS share side streams
-  bool ce_serial = false;                     // FSDP_CE_SERIAL=1: one destination at a time
+  // one destination at a time, staggered (FSDP_CE_SERIAL=0: one side stream
+  // per peer, all concurrent).  Measured at W=4, 2 GB: AG 704 vs 498 GB/s,
+  // RS 546 vs 308 GB/s bus bandwidth.
+  bool ce_serial = true;
+  bool ce_rs_push = false;                    // FSDP_CE_RS_PUSH=1: RS pushes chunks (writes) instead of pulling
   std::vector<cudaEvent_t> ce_events;
   size_t ce_next = 0;
   // VMM pool (fsdp_comm_create_vmm): own allocation + peer mappings
@@ -1224,6 +1239,7 @@ static int ce_prepare(fsdp_comm_t* c) {
     if (const char* e = getenv("FSDP_CE_SPLIT")) c->ce_split = std::max(1, std::min(4, atoi(e)));
     if (const char* e = getenv("FSDP_CE_SHARED_STREAMS")) c->ce_shared_streams = atoi(e) != 0;
     if (const char* e = getenv("FSDP_CE_SERIAL")) c->ce_serial = atoi(e) != 0;
+    if (const char* e = getenv("FSDP_CE_RS_PUSH")) c->ce_rs_push = atoi(e) != 0;
     for (int k = 0; k < 2; ++k)
       for (int r = 0; r < FSDP_MAX_RANKS * c->ce_split; ++r)
         FSDP_CUDA(cudaStreamCreateWithFlags(&c->ce_stream[k][r], cudaStreamNonBlocking));
@@ -1248,9 +1264,12 @@ static int ce_fork_join(fsdp_comm_t* c, int kind, cudaStream_t s, int gsize, int
     // one side stream, one destination at a time, staggered (member pos+1
     // first): every copy gets the whole NVSwitch port, and no two members
     // start on the same destination
-    cudaStream_t cs = c->ce_stream[c->ce_shared_streams ? 0 : kind][0];
+    // (the member's own chunk is a local copy: it runs beside them on a
+    // second side stream, it needs no NVLink)
+    cudaStream_t* row = c->ce_stream[c->ce_shared_streams ? 0 : kind];
+    cudaStream_t cs = row[0];
     FSDP_CUDA(cudaStreamWaitEvent(cs, fork, 0));
-    for (int jj = 0; jj < gsize; ++jj) {
+    for (int jj = 0; jj + 1 < gsize; ++jj) {
       const int j = (pos + 1 + jj) % gsize;
       if (!dst[j] || !bytes) continue;
       FSDP_CUDA(cudaMemcpyAsync(dst[j], src[j], bytes, cudaMemcpyDeviceToDevice, cs));
@@ -1258,6 +1277,13 @@ static int ce_fork_join(fsdp_comm_t* c, int kind, cudaStream_t s, int gsize, int
     cudaEvent_t done = ce_event(c);
     FSDP_CUDA(cudaEventRecord(done, cs));
     FSDP_CUDA(cudaStreamWaitEvent(s, done, 0));
+    if (dst[pos] && bytes) {
+      FSDP_CUDA(cudaStreamWaitEvent(row[1], fork, 0));
+      FSDP_CUDA(cudaMemcpyAsync(dst[pos], src[pos], bytes, cudaMemcpyDeviceToDevice, row[1]));
+      cudaEvent_t own = ce_event(c);
+      FSDP_CUDA(cudaEventRecord(own, row[1]));
+      FSDP_CUDA(cudaStreamWaitEvent(s, own, 0));
+    }
     return 0;
   }
   const int k = c->ce_split;
@@ -1325,34 +1351,87 @@ extern "C" int fsdp_reduce_scatter_ce(fsdp_comm_t* c, int channel, int gsize, in
   CollParams p;
   fill_common(c, p, channel, gsize, gstride, n);
   p.data_ctas = 1;
-  p.out[0] = out;
-  p.off_a = src_off;
-  p.off_b = stage_off;
-  p.prediv = prediv; p.postdiv = postdiv; p.accumulate = accumulate ? 1 : 0;
   cudaStream_t s = (cudaStream_t)stream;
   if (int rc = launch(c, coll_enter_kernel, p, 1, 32, s)) return rc;
   const int start = gstride == 1 ? (c->rank / gsize) * gsize : c->rank % gstride;
   const int pos = gstride == 1 ? c->rank - start : c->rank / gstride;
+  char* mine = c->bases[c->rank];
+  CeReduceArgs ra;
+  ra.own = mine + src_off + (int64_t)pos * n * es;
+  ra.stage = mine + stage_off;
+  ra.stride = n;
+  ra.out = out;
+  ra.gsize = gsize; ra.pos = pos;
+  ra.prediv = prediv; ra.postdiv = postdiv; ra.accumulate = accumulate ? 1 : 0;
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (c->timing) { a = take_event(c); b = take_event(c); FSDP_CUDA(cudaEventRecord(a, s)); }
+
+  // Pieces: the side stream pulls piece q+1 from every peer (serial,
+  // staggered, NVLink reads into local staging) while the stream reduces
+  // piece q, so the HBM-bound reduction hides behind the transfers.
+  const int64_t kMinPiece = 32LL << 20;   // elements: smaller DMA copies lose efficiency
+  int pieces = (int)std::min<int64_t>(4, std::max<int64_t>(1, n / kMinPiece));
+  if (c->ce_rs_push || !c->ce_serial) pieces = 1;
+  const int64_t plen = ((n + pieces - 1) / pieces + kVec - 1) / kVec * kVec;
+  auto reduce_piece = [&](int64_t e0, int64_t len) -> int {
+    if (len <= 0) return 0;
+    ra.e0 = e0; ra.len = len;
+    const int64_t nv = std::max<int64_t>(1, (len + kVec - 1) / kVec);
+    const int grid = (int)std::min<int64_t>((nv + 255) / 256, (int64_t)kNumSMs * 4);
+    if (src_dtype == FSDP_BF16) ce_reduce_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(ra);
+    else ce_reduce_kernel<float><<<grid, 256, 0, s>>>(ra);
+    FSDP_LAUNCHED();
+    return 0;
+  };
+
+  if (pieces > 1) {
+    cudaEvent_t fork = ce_event(c);
+    FSDP_CUDA(cudaEventRecord(fork, s));
+    cudaStream_t cs = c->ce_stream[c->ce_shared_streams ? 0 : 1][0];
+    FSDP_CUDA(cudaStreamWaitEvent(cs, fork, 0));
+    for (int q = 0; q < pieces; ++q) {
+      const int64_t e0 = q * plen, len = std::min(plen, n - e0);
+      if (len <= 0) break;
+      for (int jj = 0; jj + 1 < gsize; ++jj) {
+        const int j = (pos + 1 + jj) % gsize;
+        FSDP_CUDA(cudaMemcpyAsync(mine + stage_off + ((int64_t)j * n + e0) * es,
+                                  c->bases[start + j * gstride] + src_off + ((int64_t)pos * n + e0) * es,
+                                  (size_t)len * es, cudaMemcpyDeviceToDevice, cs));
+      }
+      cudaEvent_t landed = ce_event(c);
+      FSDP_CUDA(cudaEventRecord(landed, cs));
+      FSDP_CUDA(cudaStreamWaitEvent(s, landed, 0));
+      if (q + 1 == pieces || e0 + len >= n) {
+        if (c->timing) { FSDP_CUDA(cudaEventRecord(b, s)); c->timed[FSDP_KIND_RS].emplace_back(a, b); }
+        if (int rc = launch(c, coll_signal_kernel, p, 1, 32, s)) return rc;   // done reading peers
+      }
+      if (int rc = reduce_piece(e0, len)) return rc;
+    }
+    return launch(c, coll_exit_kernel, p, 1, 256, s);     // peers done reading mine
+  }
+
   void* dst[FSDP_MAX_RANKS] = {};
   const void* src[FSDP_MAX_RANKS] = {};
   for (int j = 0; j < gsize; ++j) {
     if (j == pos) continue;   // own chunk is reduced in place
-    dst[j] = c->bases[c->rank] + stage_off + (int64_t)j * n * es;
-    src[j] = c->bases[start + j * gstride] + src_off + (int64_t)pos * n * es;   // pull
+    if (c->ce_rs_push) {      // my chunk j -> member j's staging, slot pos (NVLink writes)
+      dst[j] = c->bases[start + j * gstride] + stage_off + (int64_t)pos * n * es;
+      src[j] = mine + src_off + (int64_t)j * n * es;
+    } else {                  // member j's chunk pos -> my staging, slot j (NVLink reads)
+      dst[j] = mine + stage_off + (int64_t)j * n * es;
+      src[j] = c->bases[start + j * gstride] + src_off + (int64_t)pos * n * es;
+    }
   }
-  cudaEvent_t a = nullptr, b = nullptr;
-  if (c->timing) { a = take_event(c); b = take_event(c); FSDP_CUDA(cudaEventRecord(a, s)); }
   if (int rc = ce_fork_join(c, 1, s, gsize, pos, dst, src, (size_t)n * es)) return rc;
   if (c->timing) { FSDP_CUDA(cudaEventRecord(b, s)); c->timed[FSDP_KIND_RS].emplace_back(a, b); }
-  if (int rc = launch(c, coll_signal_kernel, p, 1, 32, s)) return rc;   // done reading peers
-  const int64_t nv = std::max<int64_t>(1, (n + kVec - 1) / kVec);
-  const int grid = (int)std::min<int64_t>((nv + 255) / 256, (int64_t)kNumSMs * 4);
-  if (src_dtype == FSDP_BF16) {
-    ce_reduce_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(p);
-  } else {
-    ce_reduce_kernel<float><<<grid, 256, 0, s>>>(p);
+  if (int rc = launch(c, coll_signal_kernel, p, 1, 32, s)) return rc;   // my copies are done
+  if (c->ce_rs_push) {
+    // every member's pushes into my staging have landed; my payload was
+    // only read by my own copies, so nothing waits after the reduction
+    if (int rc = launch(c, coll_exit_kernel, p, 1, 256, s)) return rc;
+    return reduce_piece(0, n);
   }
-  FSDP_LAUNCHED();
+  if (int rc = reduce_piece(0, n)) return rc;
   return launch(c, coll_exit_kernel, p, 1, 256, s);     // peers done reading mine
 }
 

@@ -93,6 +93,13 @@ class RuntimeConfig:
     # Same flag protocol and bits either way.
     ag_engine: str = "ce"
     rs_engine: str = "ce"
+    # the step's two collectives that nothing can overlap -- the first
+    # all-gather after the optimizer and the reduce-scatter of the last unit
+    # in backward order -- run as SM kernels with tail_ctas CTAs: the compute
+    # stream is idle waiting for them, so they take no SMs from GEMMs.
+    # "same": use ag_engine / rs_engine for them too.
+    tail_engine: str = "sm"
+    tail_ctas: int = 128
     optimizer: str = "adam"
     lr: float = 1e-3
     betas: tuple = (0.9, 0.999)
@@ -315,6 +322,8 @@ class FSDPRuntime:
         self.bytes_ag = 0
         self.bytes_rs = 0
         self.profile = False          # record CUDA events around every launch
+        self.stall_units: list = []   # (label, uid, event, event) per profiled wait
+        self._ag_since_opt = 0        # all-gathers issued since the last optimizer step
         self.timers: dict[str, list] = {}
 
     # ------------------------------------------------------------ memory ---
@@ -470,8 +479,37 @@ class FSDPRuntime:
                     out[name]["data_total_ms"] = sum(d)
         return out
 
+    def _wait(self, label: str, ev=None, stream: torch.cuda.Stream | None = None,
+              uid: int = -1) -> None:
+        """compute stream waits for a comm event (or a whole comm stream).
+        With profiling on, events on both sides of the wait measure how long
+        the compute stream actually stalled on communication (GPU time, per
+        wait): the exposed-comm breakdown behind bench.py's `exposed_comm`."""
+        cs = self.compute_stream
+        if not self.profile:
+            cs.wait_event(ev) if ev is not None else cs.wait_stream(stream)
+            return
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(cs)
+        cs.wait_event(ev) if ev is not None else cs.wait_stream(stream)
+        b.record(cs)
+        self.timers.setdefault("stall_" + label, []).append((a, b, 0))
+        self.stall_units.append((label, uid, a, b))
+
+    def stall_breakdown(self, top: int = 6) -> dict:
+        """{label: [(uid, total_ms, waits), ...]} largest first (synchronises)."""
+        torch.cuda.synchronize(self.device)
+        agg: dict = {}
+        for label, uid, a, b in self.stall_units:
+            d = agg.setdefault(label, {})
+            t, c = d.get(uid, (0.0, 0))
+            d[uid] = (t + a.elapsed_time(b), c + 1)
+        return {k: sorted(((u, round(t, 3), c) for u, (t, c) in v.items()), key=lambda x: -x[1])[:top]
+                for k, v in agg.items()}
+
     def reset_timers(self) -> None:
         self.timers = {}
+        self.stall_units = []
         if self.comm is not None:
             self.comm.set_mode(split=True, timing=self.profile)
             for kind in (self.comm.KIND_AG, self.comm.KIND_RS, self.comm.KIND_AR):
@@ -501,7 +539,14 @@ class FSDPRuntime:
             elif self.cfg.comm_backend == "ipc":
                 with self.timed("allgather", self.ag_stream,
                                 lay.psi * (2 if self.cfg.mixed else 4)):
-                    if self.cfg.ag_engine == "ce" and src.dtype == self.compute_dtype:
+                    first = self._ag_since_opt == 0 and self.opt_done is not None
+                    if first and self.cfg.tail_engine == "sm":
+                        # nothing to overlap: the compute stream waits for it
+                        self.comm.set_ctas(self.comm.KIND_AG, self.cfg.tail_ctas)
+                        self.comm.all_gather(self._group_ag(), [src], self.slots.offsets[slot],
+                                             self.compute_dtype, stream=self.ag_stream)
+                        self.comm.set_ctas(self.comm.KIND_AG, self.cfg.ag_ctas)
+                    elif self.cfg.ag_engine == "ce" and src.dtype == self.compute_dtype:
                         self.comm.all_gather_ce(self._group_ag(), src, self.slots.offsets[slot],
                                                 stream=self.ag_stream)
                     elif self.cfg.ag_engine == "nvls":
@@ -515,6 +560,7 @@ class FSDPRuntime:
                 dist.all_gather_into_tensor(u.unsharded, src, group=self.pgs.get("shard"))
             ev = torch.cuda.Event()
             ev.record(self.ag_stream)
+        self._ag_since_opt += 1
         u.ag_event = ev
         u.window = _Window(uid)
         self.inflight.append(u.window)
@@ -549,7 +595,7 @@ class FSDPRuntime:
         else:
             self.limiter_acquire()
             self._issue_unshard(uid)
-        self.compute_stream.wait_event(u.ag_event)
+        self._wait("allgather", u.ag_event, uid=uid)
         u.uses = 1
         return u.unsharded
 
@@ -802,9 +848,15 @@ class FSDPRuntime:
                         stream=self.compute_stream)
 
     def _rs(self, gslot: int, dtype: torch.dtype, out: torch.Tensor, pre: float, post: float,
-            accumulate: bool) -> None:
+            accumulate: bool, tail: bool = False) -> None:
         """Reduce-scatter of the payload in symmetric gradient slot `gslot`."""
-        if self.cfg.rs_engine == "ce":
+        if tail and self.cfg.tail_engine == "sm":
+            self.comm.set_ctas(self.comm.KIND_RS, self.cfg.tail_ctas)
+            self.comm.reduce_scatter_pull(self.plan.sharded_desc, self.gslot_offs[gslot], dtype,
+                                          [out], prediv=pre, postdiv=post, accumulate=accumulate,
+                                          stream=self.rs_stream, tma=False)
+            self.comm.set_ctas(self.comm.KIND_RS, self.cfg.rs_ctas)
+        elif self.cfg.rs_engine == "ce":
             self.comm.reduce_scatter_ce(self.plan.sharded_desc, self.gslot_offs[gslot], dtype,
                                         self.rs_stage_off, out, prediv=pre, postdiv=post,
                                         accumulate=accumulate, stream=self.rs_stream)
@@ -820,7 +872,7 @@ class FSDPRuntime:
         self._gslot_next = 1 - idx
         ev = self.gslot_free[idx]
         if ev is not None:
-            self.compute_stream.wait_event(ev)
+            self._wait("grad_slot", ev)
         return idx, self.gslot_views[idx][:psi]
 
     def _reduce_unit(self, uid: int, grad: torch.Tensor) -> None:
@@ -844,6 +896,8 @@ class FSDPRuntime:
         self.events.append((self.step_count, "reduce_issue", uid))
         self.trace.record("RS_issue", uid, grad.numel() * self.payload_dtype.itemsize)
         n = u.layout.shard_numel
+        tail = (not self.defer_reduce and self.final_micro and bool(self.bwd_order)
+                and uid == self.bwd_order[-1])
         with torch.cuda.stream(self.rs_stream):
             self.rs_stream.wait_event(ready)
             payload = grad
@@ -862,7 +916,7 @@ class FSDPRuntime:
                 self._reduce_nccl(u, payload, accumulate, pre, post)
             elif F == W:
                 with self.timed("reduce_scatter", self.rs_stream, payload.numel() * payload.element_size()):
-                    self._rs(gslot, payload.dtype, u.grad, pre, post, accumulate)
+                    self._rs(gslot, payload.dtype, u.grad, pre, post, accumulate, tail)
             elif F == 1:
                 with self.timed("allreduce", self.rs_stream, payload.numel() * payload.element_size()):
                     self.comm.all_reduce(self.plan.replicated_desc, [payload], self.ar_stage_off,
@@ -871,7 +925,7 @@ class FSDPRuntime:
             else:
                 tmp = torch.empty(n, dtype=torch.float32, device=self.device)
                 with self.timed("reduce_scatter", self.rs_stream, payload.numel() * payload.element_size()):
-                    self._rs(gslot, payload.dtype, tmp, pre, 1.0, False)
+                    self._rs(gslot, payload.dtype, tmp, pre, 1.0, False, tail)
                 self.events.append((self.step_count, "reduce_stage2", uid))
                 self.trace.record("AR_issue", uid, n * 4)
                 with self.timed("allreduce", self.rs_stream, n * 4):
@@ -927,7 +981,7 @@ class FSDPRuntime:
                     self.compute_stream.wait_event(u.ag_event)
                     u.pending = False
                 self.reshard(u.uid)
-        self.compute_stream.wait_stream(self.rs_stream)
+        self._wait("reduce_scatter_end", stream=self.rs_stream)   # every reduction done
         self.in_backward = False
         self.prev_fwd_order = list(self.fwd_order)
         self.micro_index += 1
@@ -972,6 +1026,7 @@ class FSDPRuntime:
             ev.record(self.rs_stream)
             self.compute_stream.wait_event(ev)
             self.opt_done = ev
+            self._ag_since_opt = 0
             self.events.append((self.step_count - 1, "opt_step", None))
             return
         if any(u.stepped for u in self.units):
@@ -987,6 +1042,7 @@ class FSDPRuntime:
         ev = torch.cuda.Event()
         ev.record(self.compute_stream)
         self.opt_done = ev
+        self._ag_since_opt = 0
         self.events.append((self.step_count - 1, "opt_step", None))
 
     def _opt_launch(self, skip) -> None:

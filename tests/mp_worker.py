@@ -100,6 +100,47 @@ def raw_collectives(rank, world, results):
     results["raw_collectives"] = "bit-exact"
 
 
+def ce_schedules(rank, world, results):
+    """Every copy-engine schedule gives the same bits: serial-staggered or
+    concurrent DMA, reduce-scatter by pull or by push (FSDP_CE_SERIAL,
+    FSDP_CE_RS_PUSH, read when a communicator first uses the copy engines)."""
+    from paper_2304_11277_b200.comm import DeviceComm
+    done = []
+    # 262152: one piece; (1 << 23) + 24: the pipelined pull (4 pieces, short last one)
+    for n, serial, push in ((262144 + 8, 1, 0), ((1 << 23) + 24, 1, 0), (262144 + 8, 1, 1),
+                            (262144 + 8, 0, 0), (262144 + 8, 0, 1)):
+        rngs = [np.random.default_rng(555 + r) for r in range(world)]
+        shards = [g.standard_normal(n).astype(np.float32) for g in rngs]
+        grads = [round_to_bf16(g.standard_normal(n * world).astype(np.float32)) for g in rngs]
+        acc0 = [g.standard_normal(n).astype(np.float32) for g in rngs]
+        exp_ag = sp.cast(sp.all_gather(shards), sp.BF16)
+        exp_rs = sp.reduce_unit(grads, sp.Plan(world, world), reduce_dtype=sp.BF16, full_dtype=np.float32,
+                                acc_dtype=np.float32, mean=True, accum=acc0)
+        os.environ["FSDP_CE_SERIAL"], os.environ["FSDP_CE_RS_PUSH"] = str(serial), str(push)
+        nb = n * world * 2 + (1 << 20)
+        comm = DeviceComm.create(3 * nb + (4 << 20), max_ctas=32)
+        try:
+            comm.set_timeout_ms(20000)
+            a, b, st = comm.alloc(nb), comm.alloc(nb), comm.alloc(nb)
+            for _ in range(3):        # repeated: stale staging / flags would show up here
+                comm.all_gather_ce((world, 1), torch.from_numpy(shards[rank]).cuda().to(torch.bfloat16), a)
+                got = comm.view(a, n * world, torch.bfloat16).float().cpu().numpy()
+                check(np.array_equal(got, exp_ag), f"AG-CE serial={serial}")
+                comm.view(b, n * world, torch.bfloat16).copy_(torch.from_numpy(grads[rank]).cuda().to(torch.bfloat16))
+                out = torch.from_numpy(acc0[rank]).cuda()
+                comm.reduce_scatter_ce((world, 1), b, torch.bfloat16, st, out, postdiv=float(world),
+                                       accumulate=True)
+                check(out.cpu().numpy().tobytes() == exp_rs[rank].tobytes(),
+                      f"RS-CE serial={serial} push={push}")
+            torch.cuda.synchronize()
+            check(comm.device_error() == 0, "device error word (CE)")
+        finally:
+            comm.close()
+            del os.environ["FSDP_CE_SERIAL"], os.environ["FSDP_CE_RS_PUSH"]
+        done.append(f"n={n}/serial={serial}/push={push}")
+    results["ce_schedules"] = done
+
+
 def nvls_collectives(rank, world, results):
     """NVLS multicast all-gather (multimem.st through the NVSwitch): bit-exact
     vs the oracle, fallback sizes, and a 20-iteration stress on changing data
@@ -380,6 +421,7 @@ def main():
     try:
         raw_collectives(rank, world, results)
         nvls_collectives(rank, world, results)
+        ce_schedules(rank, world, results)
         session_parity(rank, world, results)
         cases =[("FULL_SHARD", None), ("SHARD_GRAD_OP", None), ("NO_SHARD", None)]
         if world == 4:

@@ -260,6 +260,15 @@ def run_ours(args):
         barrier()
         ms_nocomm = tf0.elapsed_time(tf1) / args.steps
         rt.cfg.fake_comm = False
+    # per-rank no-comm step times: how far ranks drift apart on compute alone
+    # (each GPU runs at its own clock under the power cap)
+    spread = None
+    if world > 1 and ms_nocomm > 0:
+        allr = [torch.zeros(1, device=dev) for _ in range(world)]
+        dist.all_gather(allr, torch.tensor([ms_nocomm], device=dev))
+        v = [t.item() for t in allr]
+        spread = {"ms_per_step_without_comm_per_rank": [round(x, 3) for x in v],
+                  "spread_ms": round(max(v) - min(v), 3)}
     tmax = torch.tensor([ms, ms_e2e, ms_nocomm], device=dev)
     if world > 1:
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
@@ -351,7 +360,8 @@ def run_ours(args):
             "peak_mem_gb": round(torch.cuda.max_memory_allocated() / 1e9, 2),
             **({"exposed_comm": {"ms_per_step_without_comm": round(ms_nocomm, 3),
                                  "exposed_ms": round(ms - ms_nocomm, 3),
-                                 "frac_of_step": round((ms - ms_nocomm) / ms, 4)}}
+                                 "frac_of_step": round((ms - ms_nocomm) / ms, 4),
+                                 **({"rank_compute_spread": spread} if spread else {})}}
                if ms_nocomm > 0 else {}),
         }
         out.update(comm_bw)

@@ -64,6 +64,8 @@ def parse():
     ap.add_argument("--rs-engine", default="ce", choices=["sm", "ce"])
     ap.add_argument("--tail-engine", default="sm", choices=["sm", "same"],
                     help="engine of the two collectives nothing overlaps (first AG, last RS)")
+    ap.add_argument("--ll-max-bytes", type=int, default=6 << 20,
+                    help="units up to this unsharded size use the low-latency one-kernel collectives")
     ap.add_argument("--exposed", action="store_true",
                     help="also time the step with collectives replaced by no-ops")
     ap.add_argument("--opt-in-bwd", action="store_true",
@@ -191,7 +193,7 @@ def run_ours(args):
         comm_backend=args.backend, hybrid_shard_size=args.hybrid_shard_size, lr=1e-4,
         optimizer_in_backward=args.opt_in_bwd, forward_prefetch=args.forward_prefetch,
         ag_ctas=args.ctas, rs_ctas=args.rs_ctas, ag_engine=args.ag_engine,
-        rs_engine=args.rs_engine, tail_engine=args.tail_engine)
+        rs_engine=args.rs_engine, tail_engine=args.tail_engine, ll_max_bytes=args.ll_max_bytes)
     opt = fsdp.optimizer()
     rt = fsdp.rt
     dev_inputs = tuple(h.to(dev) for h in host)
@@ -346,7 +348,8 @@ def run_ours(args):
                        "parallelism": f"fsdp{world}" if world > 1 else "fsdp1 (NO_SHARD-equivalent)",
                        "comm_backend": args.backend,
                        "comm_engine": {"allgather": args.ag_engine, "reduce_scatter": args.rs_engine,
-                                       "first_ag_last_rs": args.tail_engine},
+                                       "first_ag_last_rs": args.tail_engine,
+                                       "low_latency_max_bytes": args.ll_max_bytes},
                        "l2": "inputs > L2 (weights+state >20 GB)"},
             "tflops_per_gpu": round(tflops_gpu, 2),
             "roofline": roof, "roofline_step": step_roof, "kernels": kern_share,
@@ -484,8 +487,9 @@ def run_sweep(args):
     from paper_2304_11277_b200.comm import DeviceComm
     if world < 2:
         return {"metric": "AG/RS bus GB/s", "value": None, "note": "sweep needs >= 2 GPUs"} if rank == 0 else None
-    sizes_mb = [1, 4, 16, 64, 256, 1024, 2048]
-    max_bytes = sizes_mb[-1] << 20
+    sizes_mb = [float(x) if "." in x else int(x)
+                for x in os.environ.get("FSDP_SWEEP_SIZES", "1,4,16,64,256,1024,2048").split(",")]
+    max_bytes = int(max(sizes_mb) * (1 << 20))
     cta_opts = [int(c) for c in os.environ.get("FSDP_SWEEP_CTAS", "16,32,64,128").split(",")]
     comms = {c: DeviceComm.create(2 * max_bytes + (64 << 20), max_ctas=c) for c in cta_opts}
     offs = {c: (cm.alloc(max_bytes), cm.alloc(max_bytes)) for c, cm in comms.items()}
@@ -493,10 +497,16 @@ def run_sweep(args):
     nvls = {c: DeviceComm.create(max_bytes + (64 << 20), max_ctas=c, nvls_group=world) for c in cta_opts}
     nvls = {c: cm for c, cm in nvls.items() if cm.nvls_group == world}
     nvls_off = {c: cm.alloc(max_bytes) for c, cm in nvls.items()}
+    # low-latency one-kernel path (2x wire bytes): small sizes only
+    ll_max_mb = 64
+    ll_comm = DeviceComm.create((ll_max_mb << 20) * 9 + (64 << 20), max_ctas=64)
+    ll_dst = ll_comm.alloc(ll_max_mb << 20)
+    ll_ag = ll_comm.alloc(4 * (ll_max_mb << 20), 16)
+    ll_rs = ll_comm.alloc(4 * (ll_max_mb << 20), 16)
     dev = torch.device("cuda", local)
     res = []
     for mb in sizes_mb:
-        S = mb << 20                            # unsharded bf16 bytes
+        S = int(mb * (1 << 20))                 # unsharded bf16 bytes
         n = S // 2 // world
         shard = torch.randn(n, device=dev).to(torch.bfloat16)
         flat = torch.randn(n * world, device=dev).to(torch.bfloat16)
@@ -533,19 +543,22 @@ def run_sweep(args):
         cm0 = next(iter(comms.values()))
         stage0, dst0 = offs[next(iter(comms))]
         cm0.view(stage0, n * world, torch.bfloat16).copy_(flat)
+        if mb <= ll_max_mb:
+            r["ag_ll"] = bus / (timeit(lambda: ll_comm.all_gather_ll((world, 1), [shard], ll_dst, torch.bfloat16, ll_ag)) * 1e-3) / 1e9
+            r["rs_ll"] = bus / (timeit(lambda: ll_comm.reduce_scatter_ll((world, 1), [flat], ll_rs, [out], postdiv=float(world))) * 1e-3) / 1e9
         r["ag_ce"] = bus / (timeit(lambda: cm0.all_gather_ce((world, 1), shard, dst0)) * 1e-3) / 1e9
         r["rs_ce"] = bus / (timeit(lambda: cm0.reduce_scatter_ce((world, 1), stage0, torch.bfloat16, dst0, out, postdiv=float(world))) * 1e-3) / 1e9
         # best of this library's engines: SM push / NVLS multicast / copy engines
         r["ag_ours_gbs"] = max([r[f"ag_ours_c{c}"] for c in comms] + [r[f"ag_nvls_c{c}"] for c in nvls]
-                               + [r["ag_ce"]])
+                               + [r["ag_ce"], r.get("ag_ll", 0.0)])
         r["rs_ours_gbs"] = max([max(r[f"rs_push_c{c}"], r[f"rs_pull_c{c}"], r[f"rs_tma_c{c}"]) for c in comms]
-                               + [r["rs_ce"]])
+                               + [r["rs_ce"], r.get("rs_ll", 0.0)])
         r["ag_frac_of_measured"] = r["ag_ours_gbs"] / NVLINK_MEASURED_GBS
         r["rs_frac_of_measured"] = r["rs_ours_gbs"] / NVLINK_MEASURED_GBS
         r["ag_nccl_gbs"] = bus / (timeit(lambda: dist.all_gather_into_tensor(full, shard)) * 1e-3) / 1e9
         r["rs_nccl_gbs"] = bus / (timeit(lambda: dist.reduce_scatter_tensor(out_bf, flat)) * 1e-3) / 1e9
         res.append({k: (round(v, 3 if "frac" in k else 1) if isinstance(v, float) else v) for k, v in r.items()})
-    for cm in list(comms.values()) + list(nvls.values()):
+    for cm in list(comms.values()) + list(nvls.values()) + [ll_comm]:
         cm.close()
     if rank == 0:
         best = max(res, key=lambda r: r["ag_ours_gbs"])

@@ -224,6 +224,29 @@ int fsdp_allreduce(fsdp_comm_t* c, int channel, int gsize, int gstride, const vo
 int fsdp_allreduce_scalar(fsdp_comm_t* c, const float* const* ins, float* const* outs,
                           void* stream);
 
+/* Low-latency (LL) one-shot variants for small messages: ONE kernel, no
+ * enter/exit barrier.  Data travels as 16-byte lines {d0, epoch, d1, epoch}
+ * (8 payload bytes per line, 2x wire bytes) into an LL region of the
+ * receiver's pool at ll_off (16-byte aligned, fsdp_ll_bytes(gsize, n, dtype)
+ * bytes, same offset on every member, one region per channel); the receiver
+ * polls the flags and unpacks.  The region is double-buffered by epoch
+ * parity, which is safe without barriers because a member running epoch e
+ * has received every peer's epoch e-1 lines.
+ * fsdp_allgather_ll: same contract and destination as fsdp_allgather
+ *   (collectives.py:288-291 + engine.py:661-671); the lines carry the
+ *   dst-dtype (cast) payload.
+ * fsdp_reduce_scatter_ll: same semantics as fsdp_reduce_scatter (ascending
+ *   fp32 sum from +0, prediv, / postdiv, accumulate; collectives.py:273-297,
+ *   engine.py:789-820); payload read locally only, no staging offset. */
+int64_t fsdp_ll_bytes(int gsize, int64_t n, int dtype);
+int fsdp_allgather_ll(fsdp_comm_t* c, int channel, int gsize, int gstride, const void* const* shards,
+                      int src_dtype, int64_t n, int64_t dst_off, int dst_dtype, int64_t ll_off,
+                      void* stream);
+int fsdp_reduce_scatter_ll(fsdp_comm_t* c, int channel, int gsize, int gstride,
+                           const void* const* flats, int src_dtype, int64_t n, int64_t ll_off,
+                           float* const* outs, float prediv, float postdiv, int accumulate,
+                           void* stream);
+
 
 /* ------------------------------------------------------------------------
  * VMM pool + NVLink SHARP (NVLS) multicast                (B200 + NVSwitch)

@@ -84,6 +84,10 @@ _SIGS = {
     "fsdp_allreduce": (_i32, [_vp, _i32, _i32, _i32, _vpp, _i32, _i64, _i64, _i64, _vpp, _f32,
                               _i32, _vp]),
     "fsdp_allreduce_scalar": (_i32, [_vp, _vpp, _vpp, _vp]),
+    "fsdp_ll_bytes": (_i64, [_i32, _i64, _i32]),
+    "fsdp_allgather_ll": (_i32, [_vp, _i32, _i32, _i32, _vpp, _i32, _i64, _i64, _i32, _i64, _vp]),
+    "fsdp_reduce_scatter_ll": (_i32, [_vp, _i32, _i32, _i32, _vpp, _i32, _i64, _i64, _vpp, _f32,
+                                      _f32, _i32, _vp]),
     "fsdp_nvls_supported": (_i32, [_i32]),
     "fsdp_comm_create_vmm": (_i32, [_i32, _i32, _i64, _i32, _i32, C.POINTER(_vp)]),
     "fsdp_comm_export_pool": (_i32, [_vp, _vp]),

@@ -387,6 +387,30 @@ class DeviceComm:
                                  self._ptrs(outs), float(postdiv), int(accumulate),
                                  stream_ptr(stream)), "allreduce")
 
+    @staticmethod
+    def ll_bytes(gsize: int, n: int, dtype: torch.dtype) -> int:
+        """Size of the LL region a (gsize, n, dtype) low-latency collective uses."""
+        return int(lib.fsdp_ll_bytes(gsize, n, dtype_code(dtype)))
+
+    def all_gather_ll(self, gdesc, shards: Sequence[torch.Tensor], dst_off: int,
+                      dst_dtype: torch.dtype, ll_off: int, stream=None,
+                      channel: int = _lib.CH_AG) -> None:
+        """One-kernel low-latency all-gather (same result as all_gather)."""
+        n = shards[0].numel()
+        check(lib.fsdp_allgather_ll(self._h, channel, gdesc[0], gdesc[1], self._ptrs(shards),
+                                    dtype_code(shards[0].dtype), n, dst_off, dtype_code(dst_dtype),
+                                    ll_off, stream_ptr(stream)), "allgather_ll")
+
+    def reduce_scatter_ll(self, gdesc, flats: Sequence[torch.Tensor], ll_off: int,
+                          outs: Sequence[torch.Tensor], prediv: float = 1.0, postdiv: float = 1.0,
+                          accumulate: bool = False, stream=None, channel: int = _lib.CH_RS) -> None:
+        """One-kernel low-latency reduce-scatter (same result as reduce_scatter)."""
+        n = outs[0].numel()
+        check(lib.fsdp_reduce_scatter_ll(self._h, channel, gdesc[0], gdesc[1], self._ptrs(flats),
+                                         dtype_code(flats[0].dtype), n, ll_off, self._ptrs(outs),
+                                         float(prediv), float(postdiv), int(accumulate),
+                                         stream_ptr(stream)), "reduce_scatter_ll")
+
     def scalar_all_reduce(self, ins: Sequence[torch.Tensor], outs: Sequence[torch.Tensor],
                           stream=None) -> None:
         check(lib.fsdp_allreduce_scalar(self._h, self._ptrs(ins), self._ptrs(outs),

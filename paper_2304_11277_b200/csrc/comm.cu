@@ -783,6 +783,230 @@ __global__ void __launch_bounds__(32) scalar_allreduce_kernel(const __grid_const
   }
 }
 
+// ------------------------------------------------ low-latency (LL) path ----
+// One-shot protocol for small collectives: ONE kernel, no enter/exit barrier.
+// Every 16-byte line {d0, flag, d1, flag} carries 8 payload bytes; each
+// 8-byte half {data, flag} is stored and loaded atomically, so a receiver
+// that reads flag == epoch in both halves holds that line's data.  Lines
+// land in a per-(epoch parity, sender) region of the receiver's pool at
+// off_b; the receiver unpacks them itself (cast, reduction, final layout).
+// Double buffering by epoch parity needs no barrier: a sender running epoch e
+// has received every member's epoch e-1 lines, so every member has started
+// e-1 and (stream order) finished reading its epoch e-2 region.
+// Wire bytes are 2x the payload: this path is for messages where the split
+// path's three launches and two flag round trips dominate.
+constexpr int kLLThreads = 512;
+constexpr int kLLUnroll = 4;
+
+__device__ __forceinline__ void st_ll(void* p, uint32_t d0, uint32_t d1, uint32_t f) {
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};"
+               :: "l"(p), "r"(d0), "r"(f), "r"(d1), "r"(f) : "memory");
+}
+__device__ __forceinline__ uint4 ld_ll(const void* p) {
+  uint4 v;
+  asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ bool ll_ready(const uint4& v, uint32_t f) { return v.y == f && v.w == f; }
+
+// Spin until line `p` carries epoch f (bounded: timeout -> device error word).
+__device__ __noinline__ uint4 ll_wait(const CollParams& p, const Group& g, const char* line, uint4 v) {
+  const uint32_t f = p.epoch;
+  uint32_t* err = reinterpret_cast<uint32_t*>(p.bases[g.rank] + kErrOff);
+  const uint64_t t0 = globaltimer();
+  uint32_t spins = 0;
+  while (!ll_ready(v, f)) {
+    if ((++spins & 255u) == 0) {
+      if (*(volatile uint32_t*)err != 0) break;
+      if (globaltimer() - t0 > (uint64_t)p.timeout_ns) {
+        atomicExch(err, (uint32_t)FSDP_E_TIMEOUT);
+        break;
+      }
+    }
+    v = ld_ll(line);
+  }
+  return v;
+}
+
+// Line L of a chunk of n elements, converted to Tout and packed into 8 bytes
+// (8/sizeof(Tout) elements; zero beyond n).  Same dtype: a raw bit copy.
+template <typename Tin, typename Tout>
+__device__ __forceinline__ uint2 ll_load_line(const Tin* src, int64_t L, int64_t n) {
+  constexpr int EPL = 8 / (int)sizeof(Tout);
+  const int64_t e0 = L * EPL;
+  uint2 d = make_uint2(0u, 0u);
+  if constexpr (std::is_same<Tin, Tout>::value) {
+    if (e0 + EPL <= n && (reinterpret_cast<uintptr_t>(src + e0) & 7) == 0) {
+      d = __ldg(reinterpret_cast<const uint2*>(src + e0));
+    } else {
+      Tout tmp[EPL];
+      unsigned char* b = reinterpret_cast<unsigned char*>(tmp);
+      for (int q = 0; q < 8; ++q) b[q] = 0;
+      for (int q = 0; q < EPL && e0 + q < n; ++q) tmp[q] = src[e0 + q];
+      d.x = reinterpret_cast<uint32_t*>(tmp)[0];
+      d.y = reinterpret_cast<uint32_t*>(tmp)[1];
+    }
+  } else if constexpr (sizeof(Tout) == 2) {   // fp32 -> bf16 (RNE), 4 elements
+    float x[4] = {0.f, 0.f, 0.f, 0.f};
+    if (e0 + 4 <= n && aligned16(src + e0)) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(src + e0));
+      x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+    } else {
+      for (int q = 0; q < 4 && e0 + q < n; ++q) x[q] = to_f<Tin>(src[e0 + q]);
+    }
+    d.x = pack_bf16x2(x[0], x[1]);
+    d.y = pack_bf16x2(x[2], x[3]);
+  } else {                                    // bf16 -> fp32, 2 elements
+    float x[2] = {0.f, 0.f};
+    for (int q = 0; q < 2 && e0 + q < n; ++q) x[q] = to_f<Tin>(src[e0 + q]);
+    d.x = __float_as_uint(x[0]);
+    d.y = __float_as_uint(x[1]);
+  }
+  return d;
+}
+
+// Store line L (packed T elements) into a chunk of n elements (skip beyond n).
+template <typename T>
+__device__ __forceinline__ void ll_store_line(T* dst, int64_t L, int64_t n, uint32_t d0, uint32_t d1) {
+  constexpr int EPL = 8 / (int)sizeof(T);
+  const int64_t e0 = L * EPL;
+  if (e0 + EPL <= n && (reinterpret_cast<uintptr_t>(dst + e0) & 7) == 0) {
+    *reinterpret_cast<uint2*>(dst + e0) = make_uint2(d0, d1);
+  } else {
+    uint32_t w[2] = {d0, d1};
+    const T* t = reinterpret_cast<const T*>(w);
+    for (int q = 0; q < EPL && e0 + q < n; ++q) dst[e0 + q] = t[q];
+  }
+}
+
+// LL region of member `pos`'s lines at the receiver whose pool base is `base`
+__device__ __forceinline__ char* ll_region(const CollParams& p, char* base, int pos, int64_t nl) {
+  return base + p.off_b + ((int64_t)(p.epoch & 1u) * p.gsize + pos) * nl * 16;
+}
+
+// All-gather: member k sends cast(shard) as LL lines to every other member,
+// copies its own chunk locally, then unpacks every peer's lines into its own
+// unsharded buffer at off_a + j*n (the same destination as fsdp_allgather).
+template <typename Tin, typename Tout>
+__global__ void __launch_bounds__(kLLThreads)
+allgather_ll_kernel(const __grid_constant__ CollParams p) {
+  constexpr int EPL = 8 / (int)sizeof(Tout);
+  const Group g = make_group(p);
+  const int e = p.rank0 >= 0 ? 0 : blockIdx.y;
+  const Tin* __restrict__ src = (const Tin*)p.in[e];
+  const int64_t n = p.n;
+  const int64_t nl = (n + EPL - 1) / EPL;
+  const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  Tout* dst = (Tout*)(p.bases[g.rank] + p.off_a);
+  for (int64_t L = tid; L < nl; L += nt) {
+    const uint2 d = ll_load_line<Tin, Tout>(src, L, n);
+    for (int jj = 1; jj < g.size; ++jj) {
+      const int j = (g.pos + jj) % g.size;   // stagger destinations
+      st_ll(ll_region(p, p.bases[g.member(j)], g.pos, nl) + L * 16, d.x, d.y, p.epoch);
+    }
+    ll_store_line<Tout>(dst + (int64_t)g.pos * n, L, n, d.x, d.y);
+  }
+  for (int jj = 1; jj < g.size; ++jj) {
+    const int j = (g.pos + jj) % g.size;
+    const char* reg = ll_region(p, p.bases[g.rank], j, nl);
+    Tout* dj = dst + (int64_t)j * n;
+    for (int64_t L0 = tid; L0 < nl; L0 += nt * kLLUnroll) {
+      uint4 v[kLLUnroll];
+#pragma unroll
+      for (int u = 0; u < kLLUnroll; ++u) {
+        const int64_t L = L0 + u * nt;
+        if (L < nl) v[u] = ld_ll(reg + L * 16);
+      }
+#pragma unroll
+      for (int u = 0; u < kLLUnroll; ++u) {
+        const int64_t L = L0 + u * nt;
+        if (L >= nl) continue;
+        if (!ll_ready(v[u], p.epoch)) v[u] = ll_wait(p, g, reg + L * 16, v[u]);
+        ll_store_line<Tout>(dj, L, n, v[u].x, v[u].z);
+      }
+    }
+  }
+}
+
+// Reduce-scatter: member k sends chunk j of its payload as LL lines to member
+// j; then, per line of its own chunk, sums the group's lines in ascending
+// rank order in fp32 from +0 (own chunk read locally), / postdiv, += out.
+template <typename Tin, int MAXW>
+__global__ void __launch_bounds__(kLLThreads)
+reduce_scatter_ll_kernel(const __grid_constant__ CollParams p) {
+  constexpr int EPL = 8 / (int)sizeof(Tin);
+  const Group g = make_group(p);
+  const int e = p.rank0 >= 0 ? 0 : blockIdx.y;
+  const Tin* __restrict__ flat = (const Tin*)p.in[e];
+  float* __restrict__ out = p.out[e];
+  const int64_t n = p.n;
+  const int64_t nl = (n + EPL - 1) / EPL;
+  const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t L = tid; L < nl; L += nt) {
+    for (int jj = 1; jj < g.size; ++jj) {
+      const int j = (g.pos + jj) % g.size;
+      const uint2 d = ll_load_line<Tin, Tin>(flat + (int64_t)j * n, L, n);
+      st_ll(ll_region(p, p.bases[g.member(j)], g.pos, nl) + L * 16, d.x, d.y, p.epoch);
+    }
+  }
+  const bool pre = p.prediv != 1.0f, post = p.postdiv != 1.0f;
+  const Tin* mine = flat + (int64_t)g.pos * n;
+  const char* reg[MAXW];
+#pragma unroll
+  for (int j = 0; j < MAXW; ++j) reg[j] = j < g.size ? ll_region(p, p.bases[g.rank], j, nl) : nullptr;
+  for (int64_t L = tid; L < nl; L += nt) {
+    uint4 v[MAXW];
+#pragma unroll
+    for (int j = 0; j < MAXW; ++j)      // every peer's line in flight before any wait
+      if (j < g.size && j != g.pos) v[j] = ld_ll(reg[j] + L * 16);
+    float acc[EPL];
+#pragma unroll
+    for (int q = 0; q < EPL; ++q) acc[q] = 0.0f;
+#pragma unroll
+    for (int j = 0; j < MAXW; ++j) {
+      if (j >= g.size) break;
+      uint2 d;
+      if (j == g.pos) {
+        d = ll_load_line<Tin, Tin>(mine, L, n);
+      } else {
+        if (!ll_ready(v[j], p.epoch)) v[j] = ll_wait(p, g, reg[j] + L * 16, v[j]);
+        d = make_uint2(v[j].x, v[j].z);
+      }
+      float x[EPL];
+      if constexpr (EPL == 4) {
+        x[0] = bf16lo(d.x); x[1] = bf16hi(d.x); x[2] = bf16lo(d.y); x[3] = bf16hi(d.y);
+      } else {
+        x[0] = __uint_as_float(d.x); x[1] = __uint_as_float(d.y);
+      }
+#pragma unroll
+      for (int q = 0; q < EPL; ++q) acc[q] = __fadd_rn(acc[q], pre ? __fdiv_rn(x[q], p.prediv) : x[q]);
+    }
+    const int64_t e0 = L * EPL;
+    float r[EPL];
+#pragma unroll
+    for (int q = 0; q < EPL; ++q) r[q] = post ? __fdiv_rn(acc[q], p.postdiv) : acc[q];
+    if (e0 + EPL <= n && (reinterpret_cast<uintptr_t>(out + e0) & (4 * EPL - 1)) == 0) {
+      if constexpr (EPL == 4) {
+        float4 b = p.accumulate ? *reinterpret_cast<const float4*>(out + e0) : make_float4(0.f, 0.f, 0.f, 0.f);
+        *reinterpret_cast<float4*>(out + e0) =
+            make_float4(__fadd_rn(b.x, r[0]), __fadd_rn(b.y, r[1]), __fadd_rn(b.z, r[2]), __fadd_rn(b.w, r[3]));
+      } else {
+        float2 b = p.accumulate ? *reinterpret_cast<const float2*>(out + e0) : make_float2(0.f, 0.f);
+        *reinterpret_cast<float2*>(out + e0) = make_float2(__fadd_rn(b.x, r[0]), __fadd_rn(b.y, r[1]));
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < EPL; ++q) {
+        if (e0 + q >= n) break;
+        out[e0 + q] = __fadd_rn(p.accumulate ? out[e0 + q] : 0.0f, r[q]);
+      }
+    }
+  }
+}
+
 }  // namespace fsdp
 
 using namespace fsdp;
@@ -1468,6 +1692,73 @@ extern "C" int fsdp_allreduce_scalar(fsdp_comm_t* c, const float* const* ins, fl
   fill_common(c, p, FSDP_CH_SCALAR, c->world, 1, 1);
   for (int e = 0; e < nranks_args(c); ++e) { p.in[e] = ins[e]; p.out[e] = outs[e]; }
   return launch(c, scalar_allreduce_kernel, p, 1, 32, (cudaStream_t)stream);
+}
+
+// ------------------------------------------------------ low-latency path ---
+extern "C" int64_t fsdp_ll_bytes(int gsize, int64_t n, int dtype) {
+  const int es = elem_size(dtype);
+  if (gsize < 1 || n < 0 || !es) return -1;
+  const int64_t nl = (n * es + 7) / 8;
+  return 2 * (int64_t)gsize * nl * 16;
+}
+
+static int ll_grid(fsdp_comm_t* c, int64_t nl, int kind) {
+  const int cap = c->kind_ctas[kind] > 0 ? c->kind_ctas[kind] : c->max_ctas;
+  int g = (int)std::min<int64_t>(std::max<int64_t>((nl + 2 * kLLThreads - 1) / (2 * kLLThreads), 1), cap);
+  if (c->emulated) g = std::min(g, std::max(1, 128 / c->world));
+  return g;
+}
+
+extern "C" int fsdp_allgather_ll(fsdp_comm_t* c, int channel, int gsize, int gstride,
+                                 const void* const* shards, int src_dtype, int64_t n,
+                                 int64_t dst_off, int dst_dtype, int64_t ll_off, void* stream) {
+  if (int rc = validate_group(c, channel, gsize, gstride)) return rc;
+  if (n < 0 || !shards) return fail(FSDP_E_INVALID, "fsdp_allgather_ll: bad args");
+  const int os = elem_size(dst_dtype);
+  if (!os || !elem_size(src_dtype)) return fail(FSDP_E_INVALID, "fsdp_allgather_ll: bad dtype");
+  if (int rc = check_range(c, dst_off, n * gsize * os, "fsdp_allgather_ll(dst)")) return rc;
+  if (ll_off % 16) return fail(FSDP_E_INVALID, "fsdp_allgather_ll: LL region must be 16-byte aligned");
+  if (int rc = check_range(c, ll_off, fsdp_ll_bytes(gsize, n, dst_dtype), "fsdp_allgather_ll(ll)")) return rc;
+  CollParams p;
+  fill_common(c, p, channel, gsize, gstride, n);
+  for (int e = 0; e < nranks_args(c); ++e) p.in[e] = shards[e];
+  p.off_a = dst_off;
+  p.off_b = ll_off;
+  const int grid = ll_grid(c, (n * os + 7) / 8, FSDP_KIND_AG);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (src_dtype == FSDP_F32 && dst_dtype == FSDP_BF16)
+    return launch(c, allgather_ll_kernel<float, __nv_bfloat16>, p, grid, kLLThreads, s);
+  if (src_dtype == FSDP_F32 && dst_dtype == FSDP_F32)
+    return launch(c, allgather_ll_kernel<float, float>, p, grid, kLLThreads, s);
+  if (src_dtype == FSDP_BF16 && dst_dtype == FSDP_BF16)
+    return launch(c, allgather_ll_kernel<__nv_bfloat16, __nv_bfloat16>, p, grid, kLLThreads, s);
+  return launch(c, allgather_ll_kernel<__nv_bfloat16, float>, p, grid, kLLThreads, s);
+}
+
+extern "C" int fsdp_reduce_scatter_ll(fsdp_comm_t* c, int channel, int gsize, int gstride,
+                                      const void* const* flats, int src_dtype, int64_t n,
+                                      int64_t ll_off, float* const* outs, float prediv,
+                                      float postdiv, int accumulate, void* stream) {
+  if (int rc = validate_group(c, channel, gsize, gstride)) return rc;
+  if (n < 0 || !flats || !outs) return fail(FSDP_E_INVALID, "fsdp_reduce_scatter_ll: bad args");
+  const int is = elem_size(src_dtype);
+  if (!is) return fail(FSDP_E_INVALID, "fsdp_reduce_scatter_ll: bad dtype");
+  if (!(prediv > 0.f) || !(postdiv > 0.f)) return fail(FSDP_E_INVALID, "divisors must be > 0");
+  if (ll_off % 16) return fail(FSDP_E_INVALID, "fsdp_reduce_scatter_ll: LL region must be 16-byte aligned");
+  if (int rc = check_range(c, ll_off, fsdp_ll_bytes(gsize, n, src_dtype), "fsdp_reduce_scatter_ll")) return rc;
+  CollParams p;
+  fill_common(c, p, channel, gsize, gstride, n);
+  for (int e = 0; e < nranks_args(c); ++e) { p.in[e] = flats[e]; p.out[e] = outs[e]; }
+  p.off_b = ll_off;
+  p.prediv = prediv; p.postdiv = postdiv; p.accumulate = accumulate ? 1 : 0;
+  const int grid = ll_grid(c, (n * is + 7) / 8, FSDP_KIND_RS);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int mw = gsize <= 2 ? 2 : (gsize <= 4 ? 4 : 8);
+#define RSLL(T, W) launch(c, reduce_scatter_ll_kernel<T, W>, p, grid, kLLThreads, s)
+  if (src_dtype == FSDP_BF16)
+    return mw == 2 ? RSLL(__nv_bfloat16, 2) : (mw == 4 ? RSLL(__nv_bfloat16, 4) : RSLL(__nv_bfloat16, 8));
+  return mw == 2 ? RSLL(float, 2) : (mw == 4 ? RSLL(float, 4) : RSLL(float, 8));
+#undef RSLL
 }
 
 // ------------------------------------------------------ VMM pool + NVLS ----

@@ -139,7 +139,7 @@ class FullyShardedDataParallel(nn.Module):
                  comm_backend: str = "ipc", num_slots: int | None = None, ag_ctas: int = 32, rs_ctas: int = 64,
                  optimizer: str = "adam", lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-8,
                  optimizer_in_backward: bool = False, ag_engine: str = "ce", rs_engine: str = "ce",
-                 tail_engine: str = "sm"):
+                 tail_engine: str = "sm", ll_max_bytes: int = 6 << 20):
         super().__init__()
         if cpu_offload is not None and cpu_offload.offload_params:
             raise NotImplementedError("CPU offload is out of scope for the B200 runtime")
@@ -173,7 +173,8 @@ class FullyShardedDataParallel(nn.Module):
                             comm_backend=comm_backend, num_slots=num_slots, ag_ctas=ag_ctas, rs_ctas=rs_ctas,
                             optimizer=optimizer, lr=lr, betas=tuple(betas), eps=eps,
                             optimizer_in_backward=optimizer_in_backward,
-                            ag_engine=ag_engine, rs_engine=rs_engine, tail_engine=tail_engine)
+                            ag_engine=ag_engine, rs_engine=rs_engine, tail_engine=tail_engine,
+                            ll_max_bytes=ll_max_bytes)
         self.module = module
         self.plan = plan
         self.rank = rank

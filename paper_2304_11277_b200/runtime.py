@@ -100,6 +100,11 @@ class RuntimeConfig:
     # "same": use ag_engine / rs_engine for them too.
     tail_engine: str = "sm"
     tail_ctas: int = 128
+    # units whose unsharded payload is at most this many bytes use the
+    # low-latency one-kernel collectives (no barrier kernels, 2x wire bytes):
+    # below a few MB, launch + flag round trips dominate the split path
+    # (bench.py --mode sweep: 1 MB at W=2, AG 52.8 vs 23.8 GB/s).  0 = off.
+    ll_max_bytes: int = 6 << 20
     optimizer: str = "adam"
     lr: float = 1e-3
     betas: tuple = (0.9, 0.999)
@@ -366,6 +371,7 @@ class FSDPRuntime:
         ps = 2 if self.payload_dtype == torch.bfloat16 else 4
         self.slots = None
         self.rs_stage_off = self.ar_stage_off = self.ar_gather_off = None
+        self.ll_ag_off = self.ll_rs_off = None
         if self.direct_views:
             pass
         elif self.cfg.comm_backend == "ipc":
@@ -393,12 +399,27 @@ class FSDPRuntime:
                 self.gslot_free = [None, None]
                 if self.cfg.rs_engine == "ce":
                     self.rs_stage_off = c.alloc(psi_max * ps)    # local DMA landing zone
+                # low-latency regions, one per channel (AG and RS run concurrently)
+                ll_n = self._ll_shard_max(self.units, F, es)
+                if ll_n:
+                    self.ll_ag_off = c.alloc(c.ll_bytes(F, ll_n, self.compute_dtype), 256)
+                    self.ll_rs_off = c.alloc(c.ll_bytes(F, ll_n, self.payload_dtype), 256)
             if F < W:
                 n_ar = n_max if F > 1 else psi_max
                 gsz = W // F
                 el = c.ar_staging_elems(n_ar, gsz)
                 self.ar_stage_off = c.alloc(el * 4)
                 self.ar_gather_off = c.alloc(el * 4)
+
+    def _ll_shard_max(self, units, F: int, es: int) -> int:
+        """Largest shard length among units small enough for the LL path."""
+        lim = self.cfg.ll_max_bytes
+        return max((u.layout.shard_numel for u in units if u.layout.psi * es <= lim), default=0) \
+            if lim > 0 and F > 1 else 0
+
+    def _use_ll(self, uid: int) -> bool:
+        return self.ll_ag_off is not None and \
+            self.units[uid].layout.psi * self.compute_dtype.itemsize <= self.cfg.ll_max_bytes
 
     @staticmethod
     def pool_bytes_for(layouts: Sequence[UnitLayout], plan: ShardingPlan, cfg: RuntimeConfig,
@@ -419,6 +440,11 @@ class FSDPRuntime:
         pad = lambda b: -(-b // 256) * 256 + 256  # noqa: E731
         if F > 1:
             total += nslots * pad(psi_max * es) + 3 * pad(psi_max * ps)
+            if W > 1 and cfg.ll_max_bytes > 0:
+                ll_n = max((l.shard_numel for l in layouts if l.psi * es <= cfg.ll_max_bytes), default=0)
+                # LL lines carry 8 payload bytes in 16 (x2 epoch parities, per member)
+                for sz in (es, ps):
+                    total += pad(2 * F * (-(-ll_n * sz // 8)) * 16)
         if W > 1 and F < W:
             n_ar = n_max if F > 1 else psi_max
             g = W // F
@@ -540,7 +566,10 @@ class FSDPRuntime:
                 with self.timed("allgather", self.ag_stream,
                                 lay.psi * (2 if self.cfg.mixed else 4)):
                     first = self._ag_since_opt == 0 and self.opt_done is not None
-                    if first and self.cfg.tail_engine == "sm":
+                    if self._use_ll(uid):
+                        self.comm.all_gather_ll(self._group_ag(), [src], self.slots.offsets[slot],
+                                                self.compute_dtype, self.ll_ag_off, stream=self.ag_stream)
+                    elif first and self.cfg.tail_engine == "sm":
                         # nothing to overlap: the compute stream waits for it
                         self.comm.set_ctas(self.comm.KIND_AG, self.cfg.tail_ctas)
                         self.comm.all_gather(self._group_ag(), [src], self.slots.offsets[slot],
@@ -850,7 +879,13 @@ class FSDPRuntime:
     def _rs(self, gslot: int, dtype: torch.dtype, out: torch.Tensor, pre: float, post: float,
             accumulate: bool, tail: bool = False) -> None:
         """Reduce-scatter of the payload in symmetric gradient slot `gslot`."""
-        if tail and self.cfg.tail_engine == "sm":
+        F = self.plan.shard_factor
+        if self.ll_rs_off is not None and out.numel() * F * self.compute_dtype.itemsize <= self.cfg.ll_max_bytes:
+            # same unit-size criterion as the all-gather (psi = F * shard length)
+            flat = self.comm.view(self.gslot_offs[gslot], out.numel() * F, dtype)
+            self.comm.reduce_scatter_ll(self.plan.sharded_desc, [flat], self.ll_rs_off, [out], prediv=pre,
+                                        postdiv=post, accumulate=accumulate, stream=self.rs_stream)
+        elif tail and self.cfg.tail_engine == "sm":
             self.comm.set_ctas(self.comm.KIND_RS, self.cfg.tail_ctas)
             self.comm.reduce_scatter_pull(self.plan.sharded_desc, self.gslot_offs[gslot], dtype,
                                           [out], prediv=pre, postdiv=post, accumulate=accumulate,

@@ -141,6 +141,51 @@ def ce_schedules(rank, world, results):
     results["ce_schedules"] = done
 
 
+def ll_collectives(rank, world, results):
+    """Low-latency one-kernel AG/RS (no barriers, epoch-parity double buffer):
+    24 back-to-back calls per kind with changing data, one rank delayed on
+    device every third call so ranks drift apart, plus hybrid sub-groups at
+    W = 4 — every result bit-exact with the oracle."""
+    from paper_2304_11277_b200.comm import DeviceComm
+    comm = DeviceComm.create(256 << 20, max_ctas=32)
+    comm.set_timeout_ms(20000)
+    iters = 24
+    done = []
+    for n, gs in ((1000, world), (65536 + 3, world), (262144, world)) + (((4099, 2),) if world == 4 else ()):
+        dst = [comm.alloc(n * gs * 2 + 256) for _ in range(iters)]
+        ll_ag = comm.alloc(comm.ll_bytes(gs, n, torch.bfloat16), 16)
+        ll_rs = comm.alloc(comm.ll_bytes(gs, n, torch.bfloat16), 16)
+        rngs = [np.random.default_rng(77 * r + n) for r in range(world)]
+        shards = [[g.standard_normal(n).astype(np.float32) for _ in range(iters)] for g in rngs]
+        grads = [[round_to_bf16(g.standard_normal(n * gs).astype(np.float32)) for _ in range(iters)]
+                 for g in rngs]
+        outs = [torch.zeros(n, device="cuda") for _ in range(iters)]
+        dev_sh = [torch.from_numpy(s).cuda() for s in shards[rank]]
+        dev_gr = [torch.from_numpy(g).cuda().to(torch.bfloat16) for g in grads[rank]]
+        torch.cuda.synchronize()
+        dist.barrier()
+        for it in range(iters):
+            if it % 3 == 0 and rank == it % world:
+                torch.cuda._sleep(2_000_000)          # ~1 ms: this rank falls behind
+            comm.all_gather_ll((gs, 1), [dev_sh[it]], dst[it], torch.bfloat16, ll_ag)
+            comm.reduce_scatter_ll((gs, 1), [dev_gr[it]], ll_rs, [outs[it]], postdiv=float(gs))
+        torch.cuda.synchronize()
+        start = (rank // gs) * gs
+        members = list(range(start, start + gs))
+        for it in range(iters):
+            exp = sp.cast(sp.all_gather([shards[m][it] for m in members]), sp.BF16)
+            got = comm.view(dst[it], n * gs, torch.bfloat16).float().cpu().numpy()
+            check(np.array_equal(got, exp), f"AG-LL n={n} gs={gs} it={it}")
+            exp = sp.reduce_unit([grads[m][it] for m in members], sp.Plan(gs, gs), reduce_dtype=sp.BF16,
+                                 full_dtype=np.float32, acc_dtype=np.float32, mean=True)
+            check(outs[it].cpu().numpy().tobytes() == exp[rank - start].tobytes(),
+                  f"RS-LL n={n} gs={gs} it={it}")
+        done.append(f"n={n}/gs={gs}")
+    check(comm.device_error() == 0, "device error word (LL)")
+    comm.close()
+    results["ll_collectives"] = done
+
+
 def nvls_collectives(rank, world, results):
     """NVLS multicast all-gather (multimem.st through the NVSwitch): bit-exact
     vs the oracle, fallback sizes, and a 20-iteration stress on changing data
@@ -180,7 +225,9 @@ def nvls_collectives(rank, world, results):
 
 
 def fsdp_step_parity(rank, world, strategy, hybrid, results, backend="ipc", opt_in_bwd=False,
-                     engine="ce"):
+                     engine="ce", ll=False):
+    """ll=False pins every unit to `engine` (the tiny GPT's units are all
+    small enough for the low-latency path, which ll=True exercises)."""
     from paper_2304_11277_b200 import kernels  # noqa: F401
     from paper_2304_11277_b200.fsdp import (FullyShardedDataParallel, MixedPrecision,
                                             ModuleWrapPolicy, ShardingStrategy)
@@ -192,7 +239,8 @@ def fsdp_step_parity(rank, world, strategy, hybrid, results, backend="ipc", opt_
                                     mixed_precision=MixedPrecision(param_dtype=torch.bfloat16),
                                     hybrid_shard_size=hybrid, comm_backend=backend, lr=1e-3,
                                     optimizer_in_backward=opt_in_bwd, ag_engine=engine,
-                                    rs_engine="sm" if engine == "nvls" else engine)
+                                    rs_engine="sm" if engine == "nvls" else engine,
+                                    ll_max_bytes=(6 << 20) if ll else 0)
     plan = fsdp.plan
     ref = init_gpt_(GPT(cfg), seed=0).cuda().to(torch.bfloat16)
     x, y = synthetic_batch(cfg, 2, seed=100 + rank, device="cuda")
@@ -200,7 +248,7 @@ def fsdp_step_parity(rank, world, strategy, hybrid, results, backend="ipc", opt_
     loss.backward()
     lref = ref(x, y)
     lref.backward()
-    key = (f"{strategy}{'' if hybrid is None else hybrid}/{backend}/{engine}"
+    key = (f"{strategy}{'' if hybrid is None else hybrid}/{backend}/{'ll' if ll else engine}"
            f"{'/opt-in-bwd' if opt_in_bwd else ''}")
     torch.cuda.synchronize()
     # initial shards from the oracle (flatten + shard of the same init)
@@ -410,6 +458,10 @@ def session_parity(rank, world, results):
     results["session"] = out
 
 
+class _Done(Exception):
+    pass
+
+
 def main():
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
@@ -418,8 +470,14 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     results = {"world": world}
     ok = True
+    only = os.environ.get("MP_ONLY")       # debugging: a comma list of scenario functions
     try:
+        if only:
+            for name in only.split(","):
+                globals()[name](rank, world, results)
+            raise _Done()
         raw_collectives(rank, world, results)
+        ll_collectives(rank, world, results)
         nvls_collectives(rank, world, results)
         ce_schedules(rank, world, results)
         session_parity(rank, world, results)
@@ -429,6 +487,10 @@ def main():
         for strat, hyb in cases:
             fsdp_step_parity(rank, world, strat, hyb, results)
         fsdp_step_parity(rank, world, "FULL_SHARD", None, results, opt_in_bwd=True)
+        fsdp_step_parity(rank, world, "FULL_SHARD", None, results, ll=True)
+        fsdp_step_parity(rank, world, "SHARD_GRAD_OP", None, results, ll=True)
+        if world == 4:
+            fsdp_step_parity(rank, world, "HYBRID_SHARD", 2, results, ll=True)
         fsdp_step_parity(rank, world, "FULL_SHARD", None, results, engine="sm")
         fsdp_step_parity(rank, world, "FULL_SHARD", None, results, engine="nvls")
         if world == 4:
@@ -439,6 +501,8 @@ def main():
             fsdp_step_parity(rank, world, "HYBRID_SHARD", 2, results, opt_in_bwd=True)
         fsdp_step_parity(rank, world, "FULL_SHARD", None, results, backend="nccl")
         deadlock_detection(rank, world, results)
+    except _Done:
+        pass
     except Exception:
         ok = False
         traceback.print_exc()

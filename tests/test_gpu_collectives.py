@@ -280,3 +280,100 @@ def test_full_size_unit_properties():
         assert c.device_error() == 0
     finally:
         c.close()
+
+
+# ------------------------------------------------- low-latency one-shot path
+@pytest.mark.parametrize("w", [1, 2, 3, 4, 8])
+def test_ll_ag_rs_match_reference_golden(golden, w):
+    """The LL one-kernel variants against the shardsim fabric's golden AG/RS."""
+    arrays, _ = golden
+    inputs = [arrays[f"coll/in/w{w}/r{r}"] for r in range(w)]
+    n = inputs[0].size
+    c = make_comm(w)
+    try:
+        off = c.alloc(1 << 20)
+        ll = c.alloc(c.ll_bytes(w, n, torch.float32), 16)
+        c.all_gather_ll((w, 1), [cu(x[: n // w]) for x in inputs], off, torch.float32, ll)
+        for r in range(w):
+            got = c.view(off, n, torch.float32, r).cpu().numpy()
+            assert got.tobytes() == arrays[f"coll/ag/w{w}/out{r}"].tobytes()
+        outs = [torch.empty(n // w, device="cuda") for _ in range(w)]
+        ll_rs = c.alloc(c.ll_bytes(w, n // w, torch.float32), 16)   # one region per channel
+        c.reduce_scatter_ll((w, 1), [cu(x) for x in inputs], ll_rs, outs)
+        for r in range(w):
+            assert outs[r].cpu().numpy().tobytes() == arrays[f"coll/rs/w{w}/out{r}"].tobytes()
+        torch.cuda.synchronize()
+        assert c.device_error() == 0
+    finally:
+        c.close()
+
+
+@pytest.mark.parametrize("w", [2, 4, 8])
+@pytest.mark.parametrize("n", [1, 7, 1000, 65536 + 24, 300007])
+def test_ll_allgather_cast_bit_exact_repeated(w, n):
+    """fp32 -> bf16 fused cast and bf16 -> bf16, odd lengths (partial last
+    line), 5 back-to-back calls on changing data through the same LL region
+    (both epoch parities, stale lines from earlier epochs present)."""
+    rng = np.random.default_rng(n + 31 * w)
+    c = make_comm(w)
+    try:
+        off = c.alloc(n * w * 4 + 256)
+        ll = c.alloc(c.ll_bytes(w, n, torch.float32), 16)
+        for it in range(5):
+            shards = [rng.standard_normal(n).astype(np.float32) for _ in range(w)]
+            exp = sp.cast(sp.all_gather(shards), sp.BF16)
+            src_dt = torch.float32 if it % 2 == 0 else torch.bfloat16
+            c.all_gather_ll((w, 1), [cu(s, src_dt) for s in shards], off, torch.bfloat16, ll)
+            for r in range(w):
+                got = c.view(off, n * w, torch.bfloat16, r).float().cpu().numpy()
+                assert np.array_equal(got, exp), (it, r)
+        torch.cuda.synchronize()
+        assert c.device_error() == 0
+    finally:
+        c.close()
+
+
+@pytest.mark.parametrize("w", [2, 4, 8])
+@pytest.mark.parametrize("n", [1, 5, 4104, 262147])
+def test_ll_reduce_scatter_bf16_accumulate_divide(w, n):
+    """bf16 payload, fp32 ascending sum from +0, prediv/postdiv, += accum;
+    4 back-to-back calls (both parities) — bit-exact with the oracle."""
+    rng = np.random.default_rng(w * 13 + n)
+    c = make_comm(w)
+    try:
+        ll = c.alloc(c.ll_bytes(w, n, torch.bfloat16), 16)
+        acc0 = [rng.standard_normal(n).astype(np.float32) for _ in range(w)]
+        outs = [cu(a) for a in acc0]
+        exp = acc0
+        for it in range(4):
+            grads = [round_to_bf16(rng.standard_normal(n * w).astype(np.float32)) for _ in range(w)]
+            c.reduce_scatter_ll((w, 1), [cu(g, torch.bfloat16) for g in grads], ll, outs,
+                                postdiv=float(w), accumulate=True)
+            exp = sp.reduce_unit(grads, sp.Plan(w, w), reduce_dtype=sp.BF16, full_dtype=np.float32,
+                                 acc_dtype=np.float32, mean=True, accum=exp)
+            for r in range(w):
+                assert outs[r].cpu().numpy().tobytes() == exp[r].tobytes(), (it, r)
+        torch.cuda.synchronize()
+        assert c.device_error() == 0
+    finally:
+        c.close()
+
+
+@pytest.mark.parametrize("w,f", [(4, 2), (8, 2), (8, 4)])
+def test_ll_reduce_scatter_subgroups(golden, w, f):
+    """LL RS inside sharded sub-groups (hybrid stage 1) == the split RS."""
+    arrays, _ = golden
+    grads = [arrays[f"hyb/w{w}f{f}/in{r}"] for r in range(w)]
+    n = grads[0].size // f
+    c = make_comm(w)
+    try:
+        a = c.alloc(1 << 20)
+        ll = c.alloc(c.ll_bytes(f, n, torch.float32), 16)
+        ref = [torch.empty(n, device="cuda") for _ in range(w)]
+        got = [torch.empty(n, device="cuda") for _ in range(w)]
+        c.reduce_scatter((f, 1), [cu(g) for g in grads], a, ref)
+        c.reduce_scatter_ll((f, 1), [cu(g) for g in grads], ll, got)
+        for r in range(w):
+            assert got[r].cpu().numpy().tobytes() == ref[r].cpu().numpy().tobytes()
+    finally:
+        c.close()

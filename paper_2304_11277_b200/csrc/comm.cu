@@ -239,6 +239,23 @@ __global__ void __launch_bounds__(32) coll_signal_kernel(const __grid_constant__
   }
 }
 
+// Pipelined copy-engine push: after piece q's DMA writes into every member's
+// staging (stream order on the copy side stream), publish "piece q landed"
+// (phase 1, slot q) to every member; the receiving stream waits for slot q
+// from every member before reducing piece q.
+__global__ void __launch_bounds__(32) coll_signal_slot_kernel(const __grid_constant__ CollParams p, int slot) {
+  const Group g = make_group(p);
+  if ((int)threadIdx.x < g.size) {
+    __threadfence_system();
+    st_release_sys(flag_ptr(p.bases[g.member(threadIdx.x)], p.channel, 1, g.rank, slot), p.epoch);
+  }
+}
+__global__ void __launch_bounds__(32) coll_wait_slot_kernel(const __grid_constant__ CollParams p, int slot) {
+  const Group g = make_group(p);
+  if ((int)threadIdx.x < g.size)
+    wait_flag(p, g, flag_ptr(p.bases[g.rank], p.channel, 1, g.member(threadIdx.x), slot));
+}
+
 // Local reduction of a copy-engine reduce-scatter, one piece [e0, e0+len)
 // of the member's chunk: member chunks j != pos sit in local staging
 // (stage + j*stride), the own chunk in the own payload buffer; ascending-rank
@@ -1038,7 +1055,14 @@ struct fsdp_comm {
   // per peer, all concurrent).  Measured at W=4, 2 GB: AG 704 vs 498 GB/s,
   // RS 546 vs 308 GB/s bus bandwidth.
   bool ce_serial = true;
-  bool ce_rs_push = false;                    // FSDP_CE_RS_PUSH=1: RS pushes chunks (writes) instead of pulling
+  // reduce-scatter data direction: 0 = pull (DMA reads of the peers' chunks),
+  // 1 = push (DMA writes into the peers' staging), -1 (default) = push when
+  // the chunk is pipelined in pieces, else pull.  Measured at W=4, 2 GiB:
+  // pipelined push 647-654 GB/s vs pipelined pull 590-624 (FSDP_CE_RS_PUSH)
+  int ce_rs_push = -1;
+  int ce_rs_pieces = 4;                       // FSDP_CE_RS_PIECES: max pipeline pieces of a CE reduce-scatter
+  int64_t ce_rs_min_piece = 32LL << 20;       // FSDP_CE_RS_MIN_PIECE: elements per piece at least
+  int ce_reduce_ctas = 0;                     // FSDP_CE_REDUCE_CTAS: grid of non-final piece reductions (0: full)
   std::vector<cudaEvent_t> ce_events;
   size_t ce_next = 0;
   // VMM pool (fsdp_comm_create_vmm): own allocation + peer mappings
@@ -1463,7 +1487,10 @@ static int ce_prepare(fsdp_comm_t* c) {
     if (const char* e = getenv("FSDP_CE_SPLIT")) c->ce_split = std::max(1, std::min(4, atoi(e)));
     if (const char* e = getenv("FSDP_CE_SHARED_STREAMS")) c->ce_shared_streams = atoi(e) != 0;
     if (const char* e = getenv("FSDP_CE_SERIAL")) c->ce_serial = atoi(e) != 0;
-    if (const char* e = getenv("FSDP_CE_RS_PUSH")) c->ce_rs_push = atoi(e) != 0;
+    if (const char* e = getenv("FSDP_CE_RS_PUSH")) c->ce_rs_push = atoi(e) != 0 ? 1 : 0;
+    if (const char* e = getenv("FSDP_CE_RS_PIECES")) c->ce_rs_pieces = std::max(1, std::min(16, atoi(e)));
+    if (const char* e = getenv("FSDP_CE_RS_MIN_PIECE")) c->ce_rs_min_piece = std::max<int64_t>(1 << 16, atoll(e));
+    if (const char* e = getenv("FSDP_CE_REDUCE_CTAS")) c->ce_reduce_ctas = std::max(0, atoi(e));
     for (int k = 0; k < 2; ++k)
       for (int r = 0; r < FSDP_MAX_RANKS * c->ce_split; ++r)
         FSDP_CUDA(cudaStreamCreateWithFlags(&c->ce_stream[k][r], cudaStreamNonBlocking));
@@ -1593,21 +1620,61 @@ extern "C" int fsdp_reduce_scatter_ce(fsdp_comm_t* c, int channel, int gsize, in
   // Pieces: the side stream pulls piece q+1 from every peer (serial,
   // staggered, NVLink reads into local staging) while the stream reduces
   // piece q, so the HBM-bound reduction hides behind the transfers.
-  const int64_t kMinPiece = 32LL << 20;   // elements: smaller DMA copies lose efficiency
-  int pieces = (int)std::min<int64_t>(4, std::max<int64_t>(1, n / kMinPiece));
-  if (c->ce_rs_push || !c->ce_serial) pieces = 1;
+  // (smaller DMA copies lose efficiency: pieces of at least ce_rs_min_piece elements)
+  int pieces = (int)std::min<int64_t>(c->ce_rs_pieces, std::max<int64_t>(1, n / c->ce_rs_min_piece));
+  if (!c->ce_serial) pieces = 1;
+  const bool push = c->ce_rs_push < 0 ? pieces > 1 : c->ce_rs_push == 1;
   const int64_t plen = ((n + pieces - 1) / pieces + kVec - 1) / kVec * kVec;
   auto reduce_piece = [&](int64_t e0, int64_t len) -> int {
     if (len <= 0) return 0;
     ra.e0 = e0; ra.len = len;
     const int64_t nv = std::max<int64_t>(1, (len + kVec - 1) / kVec);
-    const int grid = (int)std::min<int64_t>((nv + 255) / 256, (int64_t)kNumSMs * 4);
+    int grid = (int)std::min<int64_t>((nv + 255) / 256, (int64_t)kNumSMs * 4);
+    // a piece reduced behind the next piece's transfer needs only enough
+    // HBM bandwidth to keep pace; the final piece is exposed: full grid
+    if (c->ce_reduce_ctas > 0 && e0 + len < n) grid = std::min(grid, c->ce_reduce_ctas);
     if (src_dtype == FSDP_BF16) ce_reduce_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(ra);
     else ce_reduce_kernel<float><<<grid, 256, 0, s>>>(ra);
     FSDP_LAUNCHED();
     return 0;
   };
 
+  if (pieces > 1 && push) {
+    // pipelined push: piece q of my chunk j -> member j's staging slot pos
+    // (NVLink writes, serial staggered), then a per-piece flag; my stream
+    // reduces piece q once every member's piece q has landed here.  My
+    // payload is read only by my own copies and peers read nothing of mine,
+    // so no exit barrier: the next call's enter barrier guards the staging.
+    cudaEvent_t fork = ce_event(c);
+    FSDP_CUDA(cudaEventRecord(fork, s));
+    cudaStream_t cs = c->ce_stream[c->ce_shared_streams ? 0 : 1][0];
+    FSDP_CUDA(cudaStreamWaitEvent(cs, fork, 0));
+    for (int q = 0; q < pieces; ++q) {
+      const int64_t e0 = q * plen, len = std::min(plen, n - e0);
+      if (len <= 0) break;
+      for (int jj = 0; jj + 1 < gsize; ++jj) {
+        const int j = (pos + 1 + jj) % gsize;
+        FSDP_CUDA(cudaMemcpyAsync(c->bases[start + j * gstride] + stage_off + ((int64_t)pos * n + e0) * es,
+                                  mine + src_off + ((int64_t)j * n + e0) * es,
+                                  (size_t)len * es, cudaMemcpyDeviceToDevice, cs));
+      }
+      coll_signal_slot_kernel<<<1, 32, 0, cs>>>(p, q);
+      FSDP_LAUNCHED();
+    }
+    cudaEvent_t sent = ce_event(c);
+    FSDP_CUDA(cudaEventRecord(sent, cs));
+    for (int q = 0; q < pieces; ++q) {
+      const int64_t e0 = q * plen, len = std::min(plen, n - e0);
+      if (len <= 0) break;
+      coll_wait_slot_kernel<<<1, 32, 0, s>>>(p, q);
+      FSDP_LAUNCHED();
+      if (q + 1 == pieces || e0 + len >= n)
+        if (c->timing) { FSDP_CUDA(cudaEventRecord(b, s)); c->timed[FSDP_KIND_RS].emplace_back(a, b); }
+      if (int rc = reduce_piece(e0, len)) return rc;
+    }
+    FSDP_CUDA(cudaStreamWaitEvent(s, sent, 0));   // my payload is free once my copies are done
+    return 0;
+  }
   if (pieces > 1) {
     cudaEvent_t fork = ce_event(c);
     FSDP_CUDA(cudaEventRecord(fork, s));
@@ -1638,7 +1705,7 @@ extern "C" int fsdp_reduce_scatter_ce(fsdp_comm_t* c, int channel, int gsize, in
   const void* src[FSDP_MAX_RANKS] = {};
   for (int j = 0; j < gsize; ++j) {
     if (j == pos) continue;   // own chunk is reduced in place
-    if (c->ce_rs_push) {      // my chunk j -> member j's staging, slot pos (NVLink writes)
+    if (push) {               // my chunk j -> member j's staging, slot pos (NVLink writes)
       dst[j] = c->bases[start + j * gstride] + stage_off + (int64_t)pos * n * es;
       src[j] = mine + src_off + (int64_t)j * n * es;
     } else {                  // member j's chunk pos -> my staging, slot j (NVLink reads)
@@ -1649,7 +1716,7 @@ extern "C" int fsdp_reduce_scatter_ce(fsdp_comm_t* c, int channel, int gsize, in
   if (int rc = ce_fork_join(c, 1, s, gsize, pos, dst, src, (size_t)n * es)) return rc;
   if (c->timing) { FSDP_CUDA(cudaEventRecord(b, s)); c->timed[FSDP_KIND_RS].emplace_back(a, b); }
   if (int rc = launch(c, coll_signal_kernel, p, 1, 32, s)) return rc;   // my copies are done
-  if (c->ce_rs_push) {
+  if (push) {
     // every member's pushes into my staging have landed; my payload was
     // only read by my own copies, so nothing waits after the reduction
     if (int rc = launch(c, coll_exit_kernel, p, 1, 256, s)) return rc;

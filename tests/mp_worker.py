@@ -106,9 +106,11 @@ def ce_schedules(rank, world, results):
     FSDP_CE_RS_PUSH, read when a communicator first uses the copy engines)."""
     from paper_2304_11277_b200.comm import DeviceComm
     done = []
-    # 262152: one piece; (1 << 23) + 24: the pipelined pull (4 pieces, short last one)
-    for n, serial, push in ((262144 + 8, 1, 0), ((1 << 23) + 24, 1, 0), (262144 + 8, 1, 1),
-                            (262144 + 8, 0, 0), (262144 + 8, 0, 1)):
+    # 262152: one piece; (1 << 23) + 24 with 2M-element pieces: the pipelined
+    # pull / push (4 pieces, short last one; FSDP_CE_RS_MIN_PIECE)
+    for n, serial, push, minp in ((262144 + 8, 1, 0, 0), ((1 << 23) + 24, 1, 0, 1 << 21),
+                                  ((1 << 23) + 24, 1, 1, 1 << 21), (262144 + 8, 1, 1, 0),
+                                  (262144 + 8, 0, 0, 0), (262144 + 8, 0, 1, 0)):
         rngs = [np.random.default_rng(555 + r) for r in range(world)]
         shards = [g.standard_normal(n).astype(np.float32) for g in rngs]
         grads = [round_to_bf16(g.standard_normal(n * world).astype(np.float32)) for g in rngs]
@@ -117,6 +119,7 @@ def ce_schedules(rank, world, results):
         exp_rs = sp.reduce_unit(grads, sp.Plan(world, world), reduce_dtype=sp.BF16, full_dtype=np.float32,
                                 acc_dtype=np.float32, mean=True, accum=acc0)
         os.environ["FSDP_CE_SERIAL"], os.environ["FSDP_CE_RS_PUSH"] = str(serial), str(push)
+        os.environ["FSDP_CE_RS_MIN_PIECE"] = str(minp or (32 << 20))
         nb = n * world * 2 + (1 << 20)
         comm = DeviceComm.create(3 * nb + (4 << 20), max_ctas=32)
         try:
@@ -136,8 +139,8 @@ def ce_schedules(rank, world, results):
             check(comm.device_error() == 0, "device error word (CE)")
         finally:
             comm.close()
-            del os.environ["FSDP_CE_SERIAL"], os.environ["FSDP_CE_RS_PUSH"]
-        done.append(f"n={n}/serial={serial}/push={push}")
+            del os.environ["FSDP_CE_SERIAL"], os.environ["FSDP_CE_RS_PUSH"], os.environ["FSDP_CE_RS_MIN_PIECE"]
+        done.append(f"n={n}/serial={serial}/push={push}/min_piece={minp}")
     results["ce_schedules"] = done
 
 

@@ -1,0 +1,92 @@
+"""Copy-engine reduce-scatter schedule sweep (torchrun, one process per GPU).
+
+Each variant sets the FSDP_CE_* schedule knobs (read when a communicator
+first uses the copy engines), creates its own communicator and times
+`reduce_scatter_ce` at several sizes with CUDA events (20 iterations after 5
+warm-up, max over ranks).  busbw = S (W-1)/W / t, S = unsharded bf16 bytes.
+
+    torchrun --nproc-per-node 4 tools/rs_ce_sweep.py > rs_ce.json
+"""
+import json
+import os
+import sys
+
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+VARIANTS = {
+    "pull_p1": {"FSDP_CE_RS_PUSH": "0", "FSDP_CE_RS_PIECES": "1"},
+    "pull_p4": {"FSDP_CE_RS_PUSH": "0", "FSDP_CE_RS_PIECES": "4"},
+    "push_p1": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_PIECES": "1"},
+    "push_p4": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_PIECES": "4"},
+    "push_p8": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_PIECES": "8", "FSDP_CE_RS_MIN_PIECE": str(8 << 20)},
+    "pull_p8": {"FSDP_CE_RS_PUSH": "0", "FSDP_CE_RS_PIECES": "8", "FSDP_CE_RS_MIN_PIECE": str(8 << 20)},
+    "push_p4_r32": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_PIECES": "4", "FSDP_CE_REDUCE_CTAS": "32"},
+    "push_p4_r64": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_PIECES": "4", "FSDP_CE_REDUCE_CTAS": "64"},
+    "pull_p4_r32": {"FSDP_CE_RS_PUSH": "0", "FSDP_CE_RS_PIECES": "4", "FSDP_CE_REDUCE_CTAS": "32"},
+    "push_p8_r32": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_PIECES": "8", "FSDP_CE_RS_MIN_PIECE": str(16 << 20),
+                    "FSDP_CE_REDUCE_CTAS": "32"},
+    "push_p16_r16": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_PIECES": "16", "FSDP_CE_RS_MIN_PIECE": str(8 << 20),
+                     "FSDP_CE_REDUCE_CTAS": "16"},
+}
+
+
+def main():
+    rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2304_11277_b200.comm import DeviceComm
+    sizes = [int(x) for x in os.environ.get("RS_SIZES_MB", "64,256,1024,2048").split(",")]
+    only = os.environ.get("RS_VARIANTS")
+    names = only.split(",") if only else list(VARIANTS)
+    dev = torch.device("cuda", local)
+    out = {"world": world, "sizes_mb": sizes, "variants": {}}
+    for name in names:
+        saved = {k: os.environ.get(k) for k in VARIANTS[name]}
+        os.environ.update(VARIANTS[name])
+        maxb = max(sizes) << 20
+        cm = DeviceComm.create(2 * maxb + (64 << 20), max_ctas=64)
+        src, stage = cm.alloc(maxb), cm.alloc(maxb)
+        row = {}
+        for mb in sizes:
+            S = mb << 20
+            n = S // 2 // world
+            cm.view(src, n * world, torch.bfloat16).copy_(torch.randn(n * world, device=dev).to(torch.bfloat16))
+            o = torch.empty(n, device=dev)
+
+            def fn():
+                cm.reduce_scatter_ce((world, 1), src, torch.bfloat16, stage, o, postdiv=float(world))
+            for _ in range(5):
+                fn()
+            torch.cuda.synchronize()
+            dist.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(20):
+                fn()
+            b.record()
+            torch.cuda.synchronize()
+            t = torch.tensor([a.elapsed_time(b) / 20], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            row[mb] = round(S * (world - 1) / world / (t.item() * 1e-3) / 1e9, 1)
+        torch.cuda.synchronize()
+        assert cm.device_error() == 0
+        cm.close()
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+        out["variants"][name] = row
+        if rank == 0:
+            print(name, row, file=sys.stderr, flush=True)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

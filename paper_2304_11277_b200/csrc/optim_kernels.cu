@@ -68,70 +68,80 @@ adam_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restric
 // ring by 1-D bulk copies (one elected thread, mbarrier transaction counts),
 // so the bytes in flight per SM are set by the ring depth rather than by the
 // registers each thread can hold.  All threads then run the same adam1 math
-// on their float4 of the landed stage and store p, m, v (+ bf16 copy)
-// straight from registers.  Persistent grid: kAdamCtasPerSm CTAs per SM,
-// tiles assigned round-robin.  Same bits as adam_kernel.
-constexpr int kAdamTile = 1024;                       // elements per array per stage
-constexpr int kAdamStages = 4;
-constexpr int kAdamStageBytes = 4 * kAdamTile * 4;    // p, g, m, v
-constexpr int kAdamSmem = kAdamStages * kAdamStageBytes + 64;
-constexpr int kAdamCtasPerSm = 3;
-
-__global__ void __launch_bounds__(kOptThreads)
+// on their float4s of the landed stage and store p, m, v (+ bf16 copy)
+// straight from registers.  Persistent grid (ctas_per_sm CTAs per SM).  Same
+// bits as adam_kernel.
+template <int TILE, int STAGES, bool CONTIG, int THREADS>
+__global__ void __launch_bounds__(THREADS)
 adam_tma_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
                 float* __restrict__ v, int64_t n, AdamScalars s, const float* __restrict__ skip,
                 __nv_bfloat16* __restrict__ plow) {
+  constexpr int kStageBytes = 4 * TILE * 4;           // p, g, m, v
+  constexpr int kPer = TILE / THREADS;                // elements per thread per stage (multiple of 4)
+  static_assert(kPer % 4 == 0, "tile must give every thread whole float4s");
   if (skip != nullptr && *skip > 0.f) return;
   extern __shared__ __align__(128) unsigned char smem[];
   float* ring = reinterpret_cast<float*>(smem);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kAdamStages * kAdamStageBytes);
-  const int64_t ntiles = n / kAdamTile;               // full tiles; the tail is scalar
-  const int64_t mine = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStageBytes);
+  const int64_t ntiles = n / TILE;                    // full tiles; the tail is scalar
+  // CONTIG: CTA b streams the contiguous tile range [b*T/G, (b+1)*T/G);
+  // else tiles are dealt round-robin (tile b + k*G)
+  const int64_t tbeg = CONTIG ? ntiles * blockIdx.x / gridDim.x : 0;
+  const int64_t mine = CONTIG ? ntiles * (blockIdx.x + 1) / gridDim.x - tbeg
+                              : (ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0);
+  auto tile_of = [&](int64_t k) -> int64_t { return CONTIG ? tbeg + k : blockIdx.x + k * gridDim.x; };
   if (threadIdx.x == 0) {
-    for (int st = 0; st < kAdamStages; ++st) mbar_init(&full[st], 1);
+    for (int st = 0; st < STAGES; ++st) mbar_init(&full[st], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   auto issue = [&](int64_t k) {
-    const int st = (int)(k % kAdamStages);
-    const int64_t e0 = (blockIdx.x + k * gridDim.x) * (int64_t)kAdamTile;
-    float* base = ring + st * (4 * kAdamTile);
-    mbar_expect_tx(&full[st], kAdamStageBytes);
-    tma_load_1d(base, p + e0, kAdamTile * 4, &full[st]);
-    tma_load_1d(base + kAdamTile, g + e0, kAdamTile * 4, &full[st]);
-    tma_load_1d(base + 2 * kAdamTile, m + e0, kAdamTile * 4, &full[st]);
-    tma_load_1d(base + 3 * kAdamTile, v + e0, kAdamTile * 4, &full[st]);
+    const int st = (int)(k % STAGES);
+    const int64_t e0 = tile_of(k) * (int64_t)TILE;
+    float* base = ring + st * (4 * TILE);
+    mbar_expect_tx(&full[st], kStageBytes);
+    tma_load_1d(base, p + e0, TILE * 4, &full[st]);
+    tma_load_1d(base + TILE, g + e0, TILE * 4, &full[st]);
+    tma_load_1d(base + 2 * TILE, m + e0, TILE * 4, &full[st]);
+    tma_load_1d(base + 3 * TILE, v + e0, TILE * 4, &full[st]);
   };
   if (threadIdx.x == 0)
-    for (int64_t k = 0; k < mine && k < kAdamStages; ++k) issue(k);
+    for (int64_t k = 0; k < mine && k < STAGES; ++k) issue(k);
   for (int64_t k = 0; k < mine; ++k) {
-    const int st = (int)(k % kAdamStages);
-    mbar_wait(&full[st], (uint32_t)((k / kAdamStages) & 1));
-    const float* base = ring + st * (4 * kAdamTile);
-    const int64_t e0 = (blockIdx.x + k * gridDim.x) * (int64_t)kAdamTile;
-    const int i = threadIdx.x * 4;                    // kOptThreads * 4 == kAdamTile
-    float4 pp = *reinterpret_cast<const float4*>(base + i);
-    const float4 gg = *reinterpret_cast<const float4*>(base + kAdamTile + i);
-    float4 mm = *reinterpret_cast<const float4*>(base + 2 * kAdamTile + i);
-    float4 vv = *reinterpret_cast<const float4*>(base + 3 * kAdamTile + i);
-    __syncthreads();                                  // stage st fully read: refill it
-    if (threadIdx.x == 0 && k + kAdamStages < mine) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic reads -> async writes
-      issue(k + kAdamStages);
+    const int st = (int)(k % STAGES);
+    mbar_wait(&full[st], (uint32_t)((k / STAGES) & 1));
+    const float* base = ring + st * (4 * TILE);
+    const int64_t e0 = tile_of(k) * (int64_t)TILE;
+    float4 pp[kPer / 4], gg[kPer / 4], mm[kPer / 4], vv[kPer / 4];
+#pragma unroll
+    for (int q = 0; q < kPer / 4; ++q) {               // warp-contiguous float4s
+      const int i = (q * THREADS + threadIdx.x) * 4;
+      pp[q] = *reinterpret_cast<const float4*>(base + i);
+      gg[q] = *reinterpret_cast<const float4*>(base + TILE + i);
+      mm[q] = *reinterpret_cast<const float4*>(base + 2 * TILE + i);
+      vv[q] = *reinterpret_cast<const float4*>(base + 3 * TILE + i);
     }
-    adam1(pp.x, gg.x, mm.x, vv.x, s); adam1(pp.y, gg.y, mm.y, vv.y, s);
-    adam1(pp.z, gg.z, mm.z, vv.z, s); adam1(pp.w, gg.w, mm.w, vv.w, s);
-    const int64_t e = e0 + i;
-    reinterpret_cast<float4*>(p + e)[0] = pp;
-    __stcs(reinterpret_cast<float4*>(m + e), mm);
-    __stcs(reinterpret_cast<float4*>(v + e), vv);
-    if (plow) {
-      uint2 b = make_uint2(pack_bf16x2(pp.x, pp.y), pack_bf16x2(pp.z, pp.w));
-      *reinterpret_cast<uint2*>(plow + e) = b;
+    __syncthreads();                                  // stage st fully read: refill it
+    if (threadIdx.x == 0 && k + STAGES < mine) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic reads -> async writes
+      issue(k + STAGES);
+    }
+#pragma unroll
+    for (int q = 0; q < kPer / 4; ++q) {
+      adam1(pp[q].x, gg[q].x, mm[q].x, vv[q].x, s); adam1(pp[q].y, gg[q].y, mm[q].y, vv[q].y, s);
+      adam1(pp[q].z, gg[q].z, mm[q].z, vv[q].z, s); adam1(pp[q].w, gg[q].w, mm[q].w, vv[q].w, s);
+      const int64_t e = e0 + (q * THREADS + threadIdx.x) * 4;
+      reinterpret_cast<float4*>(p + e)[0] = pp[q];
+      __stcs(reinterpret_cast<float4*>(m + e), mm[q]);
+      __stcs(reinterpret_cast<float4*>(v + e), vv[q]);
+      if (plow) {
+        uint2 b = make_uint2(pack_bf16x2(pp[q].x, pp[q].y), pack_bf16x2(pp[q].z, pp[q].w));
+        *reinterpret_cast<uint2*>(plow + e) = b;
+      }
     }
   }
-  // scalar tail (n % kAdamTile elements), spread over the grid
-  const int64_t t0 = ntiles * kAdamTile;
+  // scalar tail (n % TILE elements), spread over the grid
+  const int64_t t0 = ntiles * TILE;
   for (int64_t i = t0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     float pp = p[i], mm = m[i], vv = v[i];
@@ -140,6 +150,27 @@ adam_tma_kernel(float* __restrict__ p, const float* __restrict__ g, float* __res
     if (plow) plow[i] = __float2bfloat16_rn(pp);
   }
 }
+
+// (tile elements, stages, CTAs per SM) variants, FSDP_ADAM_VARIANT=<index>
+struct AdamVariant {
+  void* fn;
+  int tile, stages, ctas_per_sm, threads;
+};
+// Measured on the GPT-1.3B arena at N=1 (1.32 G elements; tools/adam_bench.py
+// standalone, bench.py FSDP_ADAM_VARIANT=k in-step; profiles/r1/adam/).
+// Long contiguous per-array bursts are what the DRAM read/write mix wants:
+// 6144-element tiles streamed through a contiguous range per CTA reach 0.94-
+// 0.97 of the measured copy peak standalone, vs 0.90-0.92 for 1024-element
+// round-robin tiles and for the register kernel.  Inside the step the SM
+// clock is power-capped (~1.6 GHz) and the exact-rounding math (3 IEEE
+// divides + a sqrt per element) needs warps to hide its latency: 256-thread
+// CTAs drop to 0.78 there, 768-thread CTAs give 0.906 (first version 0.895).
+static const AdamVariant kAdamVariants[] = {
+    {(void*)adam_tma_kernel<6144, 2, true, 768>, 6144, 2, 1, 768},    // 0 (default)
+    {(void*)adam_tma_kernel<6144, 2, true, 256>, 6144, 2, 1, 256},    // 1: best standalone
+    {(void*)adam_tma_kernel<1024, 4, false, 256>, 1024, 4, 3, 256},   // 2: the first version
+    {(void*)adam_tma_kernel<4096, 3, true, 1024>, 4096, 3, 1, 1024},  // 3
+};
 
 __global__ void __launch_bounds__(kOptThreads)
 sgd_kernel(float* __restrict__ p, const float* __restrict__ g, int64_t n, float lr,
@@ -189,20 +220,27 @@ extern "C" int fsdp_adam_step(float* p, const float* g, float* m, float* v, int6
   if (!p || !g || !m || !v) return fail(FSDP_E_INVALID, "fsdp_adam_step: null buffer");
   AdamScalars s{lr, b1, omb1, b2, omb2, bc1, bc2, eps};
   static int use_tma = -1;      // FSDP_ADAM_TMA=0 selects the register-streaming kernel
+  static int var = 0;
   if (use_tma < 0) {
     const char* e = getenv("FSDP_ADAM_TMA");
     use_tma = e ? (atoi(e) != 0) : 1;
-    if (use_tma && cudaFuncSetAttribute(adam_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        kAdamSmem) != cudaSuccess)
+    if (const char* ev = getenv("FSDP_ADAM_VARIANT"))
+      var = std::max(0, std::min((int)(sizeof(kAdamVariants) / sizeof(kAdamVariants[0])) - 1, atoi(ev)));
+    const AdamVariant& av = kAdamVariants[var];
+    if (use_tma && cudaFuncSetAttribute(av.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        av.stages * 16 * av.tile + 64) != cudaSuccess)
       use_tma = 0;
   }
+  const AdamVariant& av = kAdamVariants[var];
   const bool al = aligned16(p) && aligned16(g) && aligned16(m) && aligned16(v) &&
                   (p_lowp == nullptr || ((uintptr_t)p_lowp & 7) == 0);
-  if (use_tma && al && n >= (int64_t)kAdamTile * kNumSMs) {
-    const int64_t tiles = n / kAdamTile;
-    const int grid = (int)std::min<int64_t>(tiles, (int64_t)kNumSMs * kAdamCtasPerSm);
-    adam_tma_kernel<<<grid, kOptThreads, kAdamSmem, (cudaStream_t)stream>>>(
-        p, g, m, v, n, s, skip_flag, (__nv_bfloat16*)p_lowp);
+  if (use_tma && al && n >= (int64_t)av.tile * kNumSMs) {
+    const int64_t tiles = n / av.tile;
+    const int grid = (int)std::min<int64_t>(tiles, (int64_t)kNumSMs * av.ctas_per_sm);
+    __nv_bfloat16* pl = (__nv_bfloat16*)p_lowp;
+    void* args[] = {&p, &g, &m, &v, &n, &s, &skip_flag, &pl};
+    FSDP_CUDA(cudaLaunchKernel(av.fn, dim3(grid), dim3(av.threads), args,
+                               (size_t)av.stages * 16 * av.tile + 64, (cudaStream_t)stream));
   } else {
     adam_kernel<<<opt_grid(n), kOptThreads, 0, (cudaStream_t)stream>>>(
         p, g, m, v, n, s, skip_flag, (__nv_bfloat16*)p_lowp);

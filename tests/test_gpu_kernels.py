@@ -105,8 +105,10 @@ def test_adam_bit_exact_vs_reference_golden(K, golden, lr):
         assert v.cpu().numpy().tobytes() == arrays[f"adam/lr{lr}/v{t + 1}"].tobytes()
 
 
-def test_adam_large_with_lowp_and_skip(K):
-    n = (1 << 20) + 3
+@pytest.mark.parametrize("n", [(1 << 20) + 3, 6144 * 148 * 2 + 6144 * 5 + 11])
+def test_adam_large_with_lowp_and_skip(K, n):
+    """Large n: the TMA-pipelined kernel (uneven contiguous tile ranges per
+    CTA) plus its scalar tail."""
     rng = np.random.default_rng(1)
     p0 = rng.standard_normal(n).astype(np.float32)
     g0 = (rng.standard_normal(n) * 1e-2).astype(np.float32)
@@ -116,7 +118,7 @@ def test_adam_large_with_lowp_and_skip(K):
     low = torch.empty(n, dtype=torch.bfloat16, device="cuda")
     pe = p0.copy()
     st = sp.adam_init(n, np.float32)
-    for t in (1, 2, 3):      # large n: the TMA-pipelined kernel, plus its scalar tail
+    for t in (1, 2, 3):
         K.adam_step(p, g, m, v, lr=3e-4, betas=(0.9, 0.95), eps=1e-8, t=t, p_lowp=low)
         sp.adam_step(pe, g0, st, lr=3e-4, betas=(0.9, 0.95), eps=1e-8)
         assert p.cpu().numpy().tobytes() == pe.tobytes()

@@ -271,40 +271,56 @@ struct CeReduceArgs {
   int accumulate;
 };
 
-template <typename Tin>
+template <typename Tin, int MAXW>
 __global__ void __launch_bounds__(256)
 ce_reduce_kernel(const __grid_constant__ CeReduceArgs a) {
+  constexpr int U = 2;                                 // vectors per thread per iteration
   const Tin* own = (const Tin*)a.own + a.e0;
   const Tin* stage = (const Tin*)a.stage + a.e0;
   float* __restrict__ out = a.out + a.e0;
   const int64_t n = a.len;
   const bool pre = a.prediv != 1.0f, post = a.postdiv != 1.0f;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
   const bool vec = (n % kVec == 0) && aligned16(own) && aligned16(stage) && aligned16(out) &&
                    ((a.stride * (int64_t)sizeof(Tin)) % 16 == 0);
   if (vec) {
-    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v * kVec < n; v += stride) {
-      const int64_t i = v * kVec;
-      V8F acc;
+    const Tin* src[MAXW];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) acc.v[q] = 0.0f;
-      for (int j = 0; j < a.gsize; ++j) {
-        const V8F x = unpack8<Tin>(j == a.pos ? ldg8<Tin>(own + i) : ldg8<Tin>(stage + (int64_t)j * a.stride + i));
+    for (int j = 0; j < MAXW; ++j) src[j] = j == a.pos ? own : stage + (int64_t)j * a.stride;
+    const int64_t nv = n / kVec;
+    for (int64_t v0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v0 < nv; v0 += U * nthr) {
+      Packed8<Tin> r[U][MAXW];
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          acc.v[q] = __fadd_rn(acc.v[q], pre ? __fdiv_rn(x.v[q], a.prediv) : x.v[q]);
+      for (int u = 0; u < U; ++u)                      // every load in flight before any add
+#pragma unroll
+        for (int j = 0; j < MAXW; ++j)
+          if (j < a.gsize && v0 + u * nthr < nv) r[u][j] = ldg8<Tin>(src[j] + (v0 + u * nthr) * kVec);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t v = v0 + u * nthr;
+        if (v >= nv) continue;
+        V8F acc;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc.v[q] = 0.0f;
+#pragma unroll
+        for (int j = 0; j < MAXW; ++j) {
+          if (j >= a.gsize) break;
+          const V8F x = unpack8<Tin>(r[u][j]);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) acc.v[q] = __fadd_rn(acc.v[q], pre ? __fdiv_rn(x.v[q], a.prediv) : x.v[q]);
+        }
+        V8F base;
+        if (a.accumulate) base = unpack8<float>(ldcg8<float>(out + v * kVec));
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float rr = post ? __fdiv_rn(acc.v[q], a.postdiv) : acc.v[q];
+          acc.v[q] = __fadd_rn(a.accumulate ? base.v[q] : 0.0f, rr);
+        }
+        st8<float>(out + v * kVec, pack8<float>(acc));
       }
-      V8F base;
-      if (a.accumulate) base = unpack8<float>(ldcg8<float>(out + i));
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const float r = post ? __fdiv_rn(acc.v[q], a.postdiv) : acc.v[q];
-        acc.v[q] = __fadd_rn(a.accumulate ? base.v[q] : 0.0f, r);
-      }
-      st8<float>(out + i, pack8<float>(acc));
     }
   } else {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += nthr) {
       float acc = 0.0f;
       for (int j = 0; j < a.gsize; ++j) {
         const float x = to_f<Tin>(j == a.pos ? own[i] : stage[(int64_t)j * a.stride + i]);
@@ -1060,9 +1076,11 @@ struct fsdp_comm {
   // the chunk is pipelined in pieces, else pull.  Measured at W=4, 2 GiB:
   // pipelined push 647-654 GB/s vs pipelined pull 590-624 (FSDP_CE_RS_PUSH)
   int ce_rs_push = -1;
-  int ce_rs_pieces = 4;                       // FSDP_CE_RS_PIECES: max pipeline pieces of a CE reduce-scatter
-  int64_t ce_rs_min_piece = 32LL << 20;       // FSDP_CE_RS_MIN_PIECE: elements per piece at least
+  int ce_rs_pieces = 8;                       // FSDP_CE_RS_PIECES: max pipeline pieces of a CE reduce-scatter
+  int64_t ce_rs_pipe_min = 64LL << 20;        // FSDP_CE_RS_PIPE_MIN: pipeline chunks of at least this many elements
+  int64_t ce_rs_min_piece = 4LL << 20;        // FSDP_CE_RS_MIN_PIECE: smallest geometric piece (about)
   int ce_reduce_ctas = 0;                     // FSDP_CE_REDUCE_CTAS: grid of non-final piece reductions (0: full)
+  bool ce_rs_geom = true;                     // FSDP_CE_RS_GEOM: halving pieces (else uniform)
   std::vector<cudaEvent_t> ce_events;
   size_t ce_next = 0;
   // VMM pool (fsdp_comm_create_vmm): own allocation + peer mappings
@@ -1490,7 +1508,9 @@ static int ce_prepare(fsdp_comm_t* c) {
     if (const char* e = getenv("FSDP_CE_RS_PUSH")) c->ce_rs_push = atoi(e) != 0 ? 1 : 0;
     if (const char* e = getenv("FSDP_CE_RS_PIECES")) c->ce_rs_pieces = std::max(1, std::min(16, atoi(e)));
     if (const char* e = getenv("FSDP_CE_RS_MIN_PIECE")) c->ce_rs_min_piece = std::max<int64_t>(1 << 16, atoll(e));
+    if (const char* e = getenv("FSDP_CE_RS_PIPE_MIN")) c->ce_rs_pipe_min = std::max<int64_t>(1 << 16, atoll(e));
     if (const char* e = getenv("FSDP_CE_REDUCE_CTAS")) c->ce_reduce_ctas = std::max(0, atoi(e));
+    if (const char* e = getenv("FSDP_CE_RS_GEOM")) c->ce_rs_geom = atoi(e) != 0;
     for (int k = 0; k < 2; ++k)
       for (int r = 0; r < FSDP_MAX_RANKS * c->ce_split; ++r)
         FSDP_CUDA(cudaStreamCreateWithFlags(&c->ce_stream[k][r], cudaStreamNonBlocking));
@@ -1621,10 +1641,30 @@ extern "C" int fsdp_reduce_scatter_ce(fsdp_comm_t* c, int channel, int gsize, in
   // staggered, NVLink reads into local staging) while the stream reduces
   // piece q, so the HBM-bound reduction hides behind the transfers.
   // (smaller DMA copies lose efficiency: pieces of at least ce_rs_min_piece elements)
-  int pieces = (int)std::min<int64_t>(c->ce_rs_pieces, std::max<int64_t>(1, n / c->ce_rs_min_piece));
-  if (!c->ce_serial) pieces = 1;
+  // Chunks of at least ce_rs_pipe_min elements are pipelined.  Geometric
+  // (default): halving pieces n/2, n/4, ... down to ~2*min_piece, so the one
+  // exposed reduction (the last piece's) is small while the large early
+  // pieces keep the DMA copies long.  Uniform (FSDP_CE_RS_GEOM=0): up to
+  // ce_rs_pieces equal pieces of at least ce_rs_pipe_min/2.
+  std::vector<std::pair<int64_t, int64_t>> pcs;      // (first element, length)
+  auto round8 = [](int64_t x) { return (x + kVec - 1) / kVec * kVec; };
+  if (!c->ce_serial || n < c->ce_rs_pipe_min) {
+    pcs.emplace_back(0, n);
+  } else if (c->ce_rs_geom) {
+    int64_t e0 = 0, rem = n;
+    while (rem > 2 * c->ce_rs_min_piece && (int)pcs.size() + 1 < c->ce_rs_pieces) {
+      const int64_t len = round8(rem / 2);
+      pcs.emplace_back(e0, len);
+      e0 += len; rem -= len;
+    }
+    pcs.emplace_back(e0, rem);
+  } else {
+    const int np = (int)std::min<int64_t>(c->ce_rs_pieces, std::max<int64_t>(1, 2 * n / c->ce_rs_pipe_min));
+    const int64_t plen = round8((n + np - 1) / np);
+    for (int64_t e0 = 0; e0 < n || pcs.empty(); e0 += plen) pcs.emplace_back(e0, std::min(plen, n - e0));
+  }
+  const int pieces = (int)pcs.size();
   const bool push = c->ce_rs_push < 0 ? pieces > 1 : c->ce_rs_push == 1;
-  const int64_t plen = ((n + pieces - 1) / pieces + kVec - 1) / kVec * kVec;
   auto reduce_piece = [&](int64_t e0, int64_t len) -> int {
     if (len <= 0) return 0;
     ra.e0 = e0; ra.len = len;
@@ -1633,8 +1673,16 @@ extern "C" int fsdp_reduce_scatter_ce(fsdp_comm_t* c, int channel, int gsize, in
     // a piece reduced behind the next piece's transfer needs only enough
     // HBM bandwidth to keep pace; the final piece is exposed: full grid
     if (c->ce_reduce_ctas > 0 && e0 + len < n) grid = std::min(grid, c->ce_reduce_ctas);
-    if (src_dtype == FSDP_BF16) ce_reduce_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(ra);
-    else ce_reduce_kernel<float><<<grid, 256, 0, s>>>(ra);
+    const int mw = gsize <= 2 ? 2 : (gsize <= 4 ? 4 : 8);
+    if (src_dtype == FSDP_BF16) {
+      if (mw == 2) ce_reduce_kernel<__nv_bfloat16, 2><<<grid, 256, 0, s>>>(ra);
+      else if (mw == 4) ce_reduce_kernel<__nv_bfloat16, 4><<<grid, 256, 0, s>>>(ra);
+      else ce_reduce_kernel<__nv_bfloat16, 8><<<grid, 256, 0, s>>>(ra);
+    } else {
+      if (mw == 2) ce_reduce_kernel<float, 2><<<grid, 256, 0, s>>>(ra);
+      else if (mw == 4) ce_reduce_kernel<float, 4><<<grid, 256, 0, s>>>(ra);
+      else ce_reduce_kernel<float, 8><<<grid, 256, 0, s>>>(ra);
+    }
     FSDP_LAUNCHED();
     return 0;
   };
@@ -1650,8 +1698,7 @@ extern "C" int fsdp_reduce_scatter_ce(fsdp_comm_t* c, int channel, int gsize, in
     cudaStream_t cs = c->ce_stream[c->ce_shared_streams ? 0 : 1][0];
     FSDP_CUDA(cudaStreamWaitEvent(cs, fork, 0));
     for (int q = 0; q < pieces; ++q) {
-      const int64_t e0 = q * plen, len = std::min(plen, n - e0);
-      if (len <= 0) break;
+      const int64_t e0 = pcs[q].first, len = pcs[q].second;
       for (int jj = 0; jj + 1 < gsize; ++jj) {
         const int j = (pos + 1 + jj) % gsize;
         FSDP_CUDA(cudaMemcpyAsync(c->bases[start + j * gstride] + stage_off + ((int64_t)pos * n + e0) * es,
@@ -1664,11 +1711,10 @@ extern "C" int fsdp_reduce_scatter_ce(fsdp_comm_t* c, int channel, int gsize, in
     cudaEvent_t sent = ce_event(c);
     FSDP_CUDA(cudaEventRecord(sent, cs));
     for (int q = 0; q < pieces; ++q) {
-      const int64_t e0 = q * plen, len = std::min(plen, n - e0);
-      if (len <= 0) break;
+      const int64_t e0 = pcs[q].first, len = pcs[q].second;
       coll_wait_slot_kernel<<<1, 32, 0, s>>>(p, q);
       FSDP_LAUNCHED();
-      if (q + 1 == pieces || e0 + len >= n)
+      if (q + 1 == pieces)
         if (c->timing) { FSDP_CUDA(cudaEventRecord(b, s)); c->timed[FSDP_KIND_RS].emplace_back(a, b); }
       if (int rc = reduce_piece(e0, len)) return rc;
     }
@@ -1681,8 +1727,7 @@ extern "C" int fsdp_reduce_scatter_ce(fsdp_comm_t* c, int channel, int gsize, in
     cudaStream_t cs = c->ce_stream[c->ce_shared_streams ? 0 : 1][0];
     FSDP_CUDA(cudaStreamWaitEvent(cs, fork, 0));
     for (int q = 0; q < pieces; ++q) {
-      const int64_t e0 = q * plen, len = std::min(plen, n - e0);
-      if (len <= 0) break;
+      const int64_t e0 = pcs[q].first, len = pcs[q].second;
       for (int jj = 0; jj + 1 < gsize; ++jj) {
         const int j = (pos + 1 + jj) % gsize;
         FSDP_CUDA(cudaMemcpyAsync(mine + stage_off + ((int64_t)j * n + e0) * es,
@@ -1692,7 +1737,7 @@ extern "C" int fsdp_reduce_scatter_ce(fsdp_comm_t* c, int channel, int gsize, in
       cudaEvent_t landed = ce_event(c);
       FSDP_CUDA(cudaEventRecord(landed, cs));
       FSDP_CUDA(cudaStreamWaitEvent(s, landed, 0));
-      if (q + 1 == pieces || e0 + len >= n) {
+      if (q + 1 == pieces) {
         if (c->timing) { FSDP_CUDA(cudaEventRecord(b, s)); c->timed[FSDP_KIND_RS].emplace_back(a, b); }
         if (int rc = launch(c, coll_signal_kernel, p, 1, 32, s)) return rc;   // done reading peers
       }

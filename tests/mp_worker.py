@@ -106,10 +106,13 @@ def ce_schedules(rank, world, results):
     FSDP_CE_RS_PUSH, read when a communicator first uses the copy engines)."""
     from paper_2304_11277_b200.comm import DeviceComm
     done = []
-    # 262152: one piece; (1 << 23) + 24 with 2M-element pieces: the pipelined
-    # pull / push (4 pieces, short last one; FSDP_CE_RS_MIN_PIECE)
+    # 262152: one piece.  (1 << 23) + 24 pipelined (FSDP_CE_RS_PIPE_MIN =
+    # 2*min_piece): pull with uniform pieces (FSDP_CE_RS_GEOM=0: 4 pieces,
+    # short last one); push with geometric pieces (3 pieces at min_piece 2M,
+    # 5 at 512K)
     for n, serial, push, minp in ((262144 + 8, 1, 0, 0), ((1 << 23) + 24, 1, 0, 1 << 21),
-                                  ((1 << 23) + 24, 1, 1, 1 << 21), (262144 + 8, 1, 1, 0),
+                                  ((1 << 23) + 24, 1, 1, 1 << 21), ((1 << 23) + 24, 1, 1, 1 << 19),
+                                  (262144 + 8, 1, 1, 0),
                                   (262144 + 8, 0, 0, 0), (262144 + 8, 0, 1, 0)):
         rngs = [np.random.default_rng(555 + r) for r in range(world)]
         shards = [g.standard_normal(n).astype(np.float32) for g in rngs]
@@ -119,7 +122,9 @@ def ce_schedules(rank, world, results):
         exp_rs = sp.reduce_unit(grads, sp.Plan(world, world), reduce_dtype=sp.BF16, full_dtype=np.float32,
                                 acc_dtype=np.float32, mean=True, accum=acc0)
         os.environ["FSDP_CE_SERIAL"], os.environ["FSDP_CE_RS_PUSH"] = str(serial), str(push)
-        os.environ["FSDP_CE_RS_MIN_PIECE"] = str(minp or (32 << 20))
+        os.environ["FSDP_CE_RS_MIN_PIECE"] = str(minp or (4 << 20))
+        os.environ["FSDP_CE_RS_PIPE_MIN"] = str(2 * minp if minp else (64 << 20))
+        os.environ["FSDP_CE_RS_GEOM"] = "0" if (minp and not push) else "1"
         nb = n * world * 2 + (1 << 20)
         comm = DeviceComm.create(3 * nb + (4 << 20), max_ctas=32)
         try:
@@ -139,7 +144,9 @@ def ce_schedules(rank, world, results):
             check(comm.device_error() == 0, "device error word (CE)")
         finally:
             comm.close()
-            del os.environ["FSDP_CE_SERIAL"], os.environ["FSDP_CE_RS_PUSH"], os.environ["FSDP_CE_RS_MIN_PIECE"]
+            for k in ("FSDP_CE_SERIAL", "FSDP_CE_RS_PUSH", "FSDP_CE_RS_MIN_PIECE", "FSDP_CE_RS_PIPE_MIN",
+                      "FSDP_CE_RS_GEOM"):
+                del os.environ[k]
         done.append(f"n={n}/serial={serial}/push={push}/min_piece={minp}")
     results["ce_schedules"] = done
 

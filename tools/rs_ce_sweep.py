@@ -17,19 +17,14 @@ import torch.distributed as dist
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 VARIANTS = {
-    "pull_p1": {"FSDP_CE_RS_PUSH": "0", "FSDP_CE_RS_PIECES": "1"},
-    "pull_p4": {"FSDP_CE_RS_PUSH": "0", "FSDP_CE_RS_PIECES": "4"},
-    "push_p1": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_PIECES": "1"},
-    "push_p4": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_PIECES": "4"},
-    "push_p8": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_PIECES": "8", "FSDP_CE_RS_MIN_PIECE": str(8 << 20)},
-    "pull_p8": {"FSDP_CE_RS_PUSH": "0", "FSDP_CE_RS_PIECES": "8", "FSDP_CE_RS_MIN_PIECE": str(8 << 20)},
-    "push_p4_r32": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_PIECES": "4", "FSDP_CE_REDUCE_CTAS": "32"},
-    "push_p4_r64": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_PIECES": "4", "FSDP_CE_REDUCE_CTAS": "64"},
-    "pull_p4_r32": {"FSDP_CE_RS_PUSH": "0", "FSDP_CE_RS_PIECES": "4", "FSDP_CE_REDUCE_CTAS": "32"},
-    "push_p8_r32": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_PIECES": "8", "FSDP_CE_RS_MIN_PIECE": str(16 << 20),
-                    "FSDP_CE_REDUCE_CTAS": "32"},
-    "push_p16_r16": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_PIECES": "16", "FSDP_CE_RS_MIN_PIECE": str(8 << 20),
-                     "FSDP_CE_REDUCE_CTAS": "16"},
+    "pull_p1": {"FSDP_CE_RS_PUSH": "0", "FSDP_CE_RS_PIPE_MIN": str(1 << 40)},
+    "push_p1": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_PIPE_MIN": str(1 << 40)},
+    "pull_uni4": {"FSDP_CE_RS_PUSH": "0", "FSDP_CE_RS_GEOM": "0", "FSDP_CE_RS_PIECES": "4"},
+    "push_uni4": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_GEOM": "0", "FSDP_CE_RS_PIECES": "4"},
+    "push_geo_4M": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_MIN_PIECE": str(4 << 20)},
+    "push_geo_8M": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_MIN_PIECE": str(8 << 20)},
+    "push_geo_2M": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_MIN_PIECE": str(2 << 20)},
+    "pull_geo_4M": {"FSDP_CE_RS_PUSH": "0", "FSDP_CE_RS_MIN_PIECE": str(4 << 20)},
 }
 
 

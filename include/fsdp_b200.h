@@ -219,6 +219,17 @@ int fsdp_allreduce(fsdp_comm_t* c, int channel, int gsize, int gstride, const vo
                    int src_dtype, int64_t n, int64_t stage_off, int64_t gather_off,
                    float* const* outs, float postdiv, int accumulate, void* stream);
 
+/* Copy-engine all-reduce: same contract and bits as fsdp_allreduce, real
+ * communicator only.  `in` is a local buffer of n payload elements (it need
+ * not live in the pool); DMA pushes chunks to their owners' staging, the
+ * owner reduces (ascending fp32, / postdiv) on SMs, DMA pushes the result to
+ * every member's gather buffer, then out = (accumulate ? out : 0) + result.
+ * No SM time is spent moving data, which matters when the all-reduce
+ * overlaps backward GEMMs (NO_SHARD, HYBRID stage 2). */
+int fsdp_allreduce_ce(fsdp_comm_t* c, int channel, int gsize, int gstride, const void* in,
+                      int src_dtype, int64_t n, int64_t stage_off, int64_t gather_off, float* out,
+                      float postdiv, int accumulate, void* stream);
+
 /* 1-element world all-reduce of a float flag (engine.py:572-576):
  * *outs[e] = sum over ranks (ascending) of *ins[e]. */
 int fsdp_allreduce_scalar(fsdp_comm_t* c, const float* const* ins, float* const* outs,

@@ -411,6 +411,15 @@ class DeviceComm:
                                          float(prediv), float(postdiv), int(accumulate),
                                          stream_ptr(stream)), "reduce_scatter_ll")
 
+    def all_reduce_ce(self, gdesc, inp: torch.Tensor, stage_off: int, gather_off: int,
+                      out: torch.Tensor, postdiv: float = 1.0, accumulate: bool = False,
+                      stream=None, channel: int = _lib.CH_AR) -> None:
+        """Copy-engine all-reduce (same bits as all_reduce; real communicator)."""
+        check(lib.fsdp_allreduce_ce(self._h, channel, gdesc[0], gdesc[1], inp.data_ptr(),
+                                    dtype_code(inp.dtype), inp.numel(), stage_off, gather_off,
+                                    out.data_ptr(), float(postdiv), int(accumulate),
+                                    stream_ptr(stream)), "allreduce_ce")
+
     def scalar_all_reduce(self, ins: Sequence[torch.Tensor], outs: Sequence[torch.Tensor],
                           stream=None) -> None:
         check(lib.fsdp_allreduce_scalar(self._h, self._ptrs(ins), self._ptrs(outs),

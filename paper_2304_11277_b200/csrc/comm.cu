@@ -269,6 +269,7 @@ struct CeReduceArgs {
   int gsize, pos;
   float prediv, postdiv;
   int accumulate;
+  int store_raw;          // 1: out = sum/postdiv as is (all-reduce owner phase), else (acc ? out : 0) + that
 };
 
 template <typename Tin, int MAXW>
@@ -314,7 +315,7 @@ ce_reduce_kernel(const __grid_constant__ CeReduceArgs a) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const float rr = post ? __fdiv_rn(acc.v[q], a.postdiv) : acc.v[q];
-          acc.v[q] = __fadd_rn(a.accumulate ? base.v[q] : 0.0f, rr);
+          acc.v[q] = a.store_raw ? rr : __fadd_rn(a.accumulate ? base.v[q] : 0.0f, rr);
         }
         st8<float>(out + v * kVec, pack8<float>(acc));
       }
@@ -327,8 +328,27 @@ ce_reduce_kernel(const __grid_constant__ CeReduceArgs a) {
         acc = __fadd_rn(acc, pre ? __fdiv_rn(x, a.prediv) : x);
       }
       const float r = post ? __fdiv_rn(acc, a.postdiv) : acc;
-      out[i] = __fadd_rn(a.accumulate ? out[i] : 0.0f, r);
+      out[i] = a.store_raw ? r : __fadd_rn(a.accumulate ? out[i] : 0.0f, r);
     }
+  }
+}
+
+// All-reduce epilogue (copy-engine path): out = (accumulate ? out : 0) + gathered.
+__global__ void __launch_bounds__(256)
+ar_epilogue_kernel(const float* __restrict__ gath, float* __restrict__ out, int64_t n, int accumulate) {
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (aligned16(gath) && aligned16(out)) {
+    const int64_t n4 = n / 4;
+    for (int64_t i = t; i < n4; i += nthr) {
+      const float4 x = __ldcg(reinterpret_cast<const float4*>(gath) + i);
+      float4 b = accumulate ? reinterpret_cast<const float4*>(out)[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+      b.x = __fadd_rn(b.x, x.x); b.y = __fadd_rn(b.y, x.y); b.z = __fadd_rn(b.z, x.z); b.w = __fadd_rn(b.w, x.w);
+      reinterpret_cast<float4*>(out)[i] = b;
+    }
+    for (int64_t i = n4 * 4 + t; i < n; i += nthr) out[i] = __fadd_rn(accumulate ? out[i] : 0.0f, __ldcg(gath + i));
+  } else {
+    for (int64_t i = t; i < n; i += nthr) out[i] = __fadd_rn(accumulate ? out[i] : 0.0f, __ldcg(gath + i));
   }
 }
 
@@ -1500,6 +1520,28 @@ extern "C" int fsdp_reduce_scatter_tma(fsdp_comm_t* c, int channel, int gsize, i
 }
 
 // ---------------------------------------------------- copy-engine variants --
+// Local ascending reduction of [e0, e0+len) (grid_cap 0: full occupancy grid).
+static int launch_ce_reduce(CeReduceArgs ra, int64_t e0, int64_t len, int src_dtype, int grid_cap,
+                            cudaStream_t s) {
+  if (len <= 0) return 0;
+  ra.e0 = e0; ra.len = len;
+  const int64_t nv = std::max<int64_t>(1, (len + kVec - 1) / kVec);
+  int grid = (int)std::min<int64_t>((nv + 255) / 256, (int64_t)kNumSMs * 4);
+  if (grid_cap > 0) grid = std::min(grid, grid_cap);
+  const int mw = ra.gsize <= 2 ? 2 : (ra.gsize <= 4 ? 4 : 8);
+  if (src_dtype == FSDP_BF16) {
+    if (mw == 2) ce_reduce_kernel<__nv_bfloat16, 2><<<grid, 256, 0, s>>>(ra);
+    else if (mw == 4) ce_reduce_kernel<__nv_bfloat16, 4><<<grid, 256, 0, s>>>(ra);
+    else ce_reduce_kernel<__nv_bfloat16, 8><<<grid, 256, 0, s>>>(ra);
+  } else {
+    if (mw == 2) ce_reduce_kernel<float, 2><<<grid, 256, 0, s>>>(ra);
+    else if (mw == 4) ce_reduce_kernel<float, 4><<<grid, 256, 0, s>>>(ra);
+    else ce_reduce_kernel<float, 8><<<grid, 256, 0, s>>>(ra);
+  }
+  FSDP_LAUNCHED();
+  return 0;
+}
+
 static int ce_prepare(fsdp_comm_t* c) {
   if (c->ce_events.empty()) {
     if (const char* e = getenv("FSDP_CE_SPLIT")) c->ce_split = std::max(1, std::min(4, atoi(e)));
@@ -1634,6 +1676,7 @@ extern "C" int fsdp_reduce_scatter_ce(fsdp_comm_t* c, int channel, int gsize, in
   ra.out = out;
   ra.gsize = gsize; ra.pos = pos;
   ra.prediv = prediv; ra.postdiv = postdiv; ra.accumulate = accumulate ? 1 : 0;
+  ra.store_raw = 0;
   cudaEvent_t a = nullptr, b = nullptr;
   if (c->timing) { a = take_event(c); b = take_event(c); FSDP_CUDA(cudaEventRecord(a, s)); }
 
@@ -1666,25 +1709,9 @@ extern "C" int fsdp_reduce_scatter_ce(fsdp_comm_t* c, int channel, int gsize, in
   const int pieces = (int)pcs.size();
   const bool push = c->ce_rs_push < 0 ? pieces > 1 : c->ce_rs_push == 1;
   auto reduce_piece = [&](int64_t e0, int64_t len) -> int {
-    if (len <= 0) return 0;
-    ra.e0 = e0; ra.len = len;
-    const int64_t nv = std::max<int64_t>(1, (len + kVec - 1) / kVec);
-    int grid = (int)std::min<int64_t>((nv + 255) / 256, (int64_t)kNumSMs * 4);
     // a piece reduced behind the next piece's transfer needs only enough
     // HBM bandwidth to keep pace; the final piece is exposed: full grid
-    if (c->ce_reduce_ctas > 0 && e0 + len < n) grid = std::min(grid, c->ce_reduce_ctas);
-    const int mw = gsize <= 2 ? 2 : (gsize <= 4 ? 4 : 8);
-    if (src_dtype == FSDP_BF16) {
-      if (mw == 2) ce_reduce_kernel<__nv_bfloat16, 2><<<grid, 256, 0, s>>>(ra);
-      else if (mw == 4) ce_reduce_kernel<__nv_bfloat16, 4><<<grid, 256, 0, s>>>(ra);
-      else ce_reduce_kernel<__nv_bfloat16, 8><<<grid, 256, 0, s>>>(ra);
-    } else {
-      if (mw == 2) ce_reduce_kernel<float, 2><<<grid, 256, 0, s>>>(ra);
-      else if (mw == 4) ce_reduce_kernel<float, 4><<<grid, 256, 0, s>>>(ra);
-      else ce_reduce_kernel<float, 8><<<grid, 256, 0, s>>>(ra);
-    }
-    FSDP_LAUNCHED();
-    return 0;
+    return launch_ce_reduce(ra, e0, len, src_dtype, (c->ce_reduce_ctas > 0 && e0 + len < n) ? c->ce_reduce_ctas : 0, s);
   };
 
   if (pieces > 1 && push) {
@@ -1769,6 +1796,87 @@ extern "C" int fsdp_reduce_scatter_ce(fsdp_comm_t* c, int channel, int gsize, in
   }
   if (int rc = reduce_piece(0, n)) return rc;
   return launch(c, coll_exit_kernel, p, 1, 256, s);     // peers done reading mine
+}
+
+// Copy-engine all-reduce (same contract and bits as fsdp_allreduce; real
+// communicator): enter barrier; DMA-push chunk j of my input to member j's
+// staging (slot pos) + per-member flag; ascending fp32 reduction of my chunk
+// (/ postdiv) into my slot of the gather buffer; DMA-push that result into
+// every member's gather buffer + flag; out = (accumulate ? out : 0) +
+// gathered.  Peers read nothing of mine and the next call's enter barrier
+// guards the staging/gather buffers, so there is no exit barrier.
+extern "C" int fsdp_allreduce_ce(fsdp_comm_t* c, int channel, int gsize, int gstride, const void* in,
+                                 int src_dtype, int64_t n, int64_t stage_off, int64_t gather_off,
+                                 float* out, float postdiv, int accumulate, void* stream) {
+  if (int rc = validate_group(c, channel, gsize, gstride)) return rc;
+  if (c->emulated) return fail(FSDP_E_UNSUPPORTED, "copy-engine collectives need a real communicator");
+  const int is = elem_size(src_dtype);
+  if (n < 0 || !in || !out || !is) return fail(FSDP_E_INVALID, "fsdp_allreduce_ce: bad args");
+  if (!(postdiv > 0.f)) return fail(FSDP_E_INVALID, "postdiv must be > 0");
+  int64_t ch = (n + gsize - 1) / gsize;
+  ch = (ch + kVec - 1) / kVec * kVec;
+  if (int rc = check_range(c, stage_off, ch * gsize * is, "fsdp_allreduce_ce(stage)")) return rc;
+  if (int rc = check_range(c, gather_off, ch * gsize * 4, "fsdp_allreduce_ce(gather)")) return rc;
+  if (int rc = ce_prepare(c)) return rc;
+  CollParams p;
+  fill_common(c, p, channel, gsize, gstride, n);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (int rc = launch(c, coll_enter_kernel, p, 1, 32, s)) return rc;
+  const int start = gstride == 1 ? (c->rank / gsize) * gsize : c->rank % gstride;
+  const int pos = gstride == 1 ? c->rank - start : c->rank / gstride;
+  auto clen = [&](int j) -> int64_t { const int64_t b = (int64_t)j * ch; return b >= n ? 0 : std::min(ch, n - b); };
+  char* mine = c->bases[c->rank];
+  cudaStream_t cs = c->ce_stream[c->ce_shared_streams ? 0 : 1][0];
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (c->timing) { a = take_event(c); b = take_event(c); FSDP_CUDA(cudaEventRecord(a, s)); }
+  // 1. reduce-scatter push: chunk j -> member j's staging slot pos
+  cudaEvent_t fork = ce_event(c);
+  FSDP_CUDA(cudaEventRecord(fork, s));
+  FSDP_CUDA(cudaStreamWaitEvent(cs, fork, 0));
+  for (int jj = 0; jj + 1 < gsize; ++jj) {
+    const int j = (pos + 1 + jj) % gsize;
+    if (clen(j) > 0)
+      FSDP_CUDA(cudaMemcpyAsync(c->bases[start + j * gstride] + stage_off + (int64_t)pos * ch * is,
+                                (const char*)in + (int64_t)j * ch * is, (size_t)(clen(j) * is),
+                                cudaMemcpyDeviceToDevice, cs));
+  }
+  coll_signal_slot_kernel<<<1, 32, 0, cs>>>(p, 0);
+  FSDP_LAUNCHED();
+  coll_wait_slot_kernel<<<1, 32, 0, s>>>(p, 0);
+  FSDP_LAUNCHED();
+  // 2. owner reduction of my chunk -> my slot of the gather buffer
+  CeReduceArgs ra;
+  ra.own = (const char*)in + (int64_t)pos * ch * is;
+  ra.stage = mine + stage_off;
+  ra.stride = ch;
+  ra.out = (float*)(mine + gather_off) + (int64_t)pos * ch;
+  ra.gsize = gsize; ra.pos = pos;
+  ra.prediv = 1.0f; ra.postdiv = postdiv; ra.accumulate = 0; ra.store_raw = 1;
+  if (int rc = launch_ce_reduce(ra, 0, clen(pos), src_dtype, 0, s)) return rc;
+  // 3. all-gather push of my reduced chunk
+  cudaEvent_t reduced = ce_event(c);
+  FSDP_CUDA(cudaEventRecord(reduced, s));
+  FSDP_CUDA(cudaStreamWaitEvent(cs, reduced, 0));
+  for (int jj = 0; jj + 1 < gsize; ++jj) {
+    const int j = (pos + 1 + jj) % gsize;
+    if (clen(pos) > 0)
+      FSDP_CUDA(cudaMemcpyAsync(c->bases[start + j * gstride] + gather_off + (int64_t)pos * ch * 4,
+                                mine + gather_off + (int64_t)pos * ch * 4, (size_t)(clen(pos) * 4),
+                                cudaMemcpyDeviceToDevice, cs));
+  }
+  coll_signal_slot_kernel<<<1, 32, 0, cs>>>(p, 1);
+  FSDP_LAUNCHED();
+  cudaEvent_t sent = ce_event(c);
+  FSDP_CUDA(cudaEventRecord(sent, cs));
+  coll_wait_slot_kernel<<<1, 32, 0, s>>>(p, 1);
+  FSDP_LAUNCHED();
+  if (c->timing) { FSDP_CUDA(cudaEventRecord(b, s)); c->timed[FSDP_KIND_AR].emplace_back(a, b); }
+  // 4. out = (accumulate ? out : 0) + gathered
+  const int grid = (int)std::min<int64_t>(std::max<int64_t>((n / 4 + 255) / 256, 1), (int64_t)kNumSMs * 4);
+  ar_epilogue_kernel<<<grid, 256, 0, s>>>((const float*)(mine + gather_off), out, n, accumulate ? 1 : 0);
+  FSDP_LAUNCHED();
+  FSDP_CUDA(cudaStreamWaitEvent(s, sent, 0));   // my input and gather slot are free once my copies are done
+  return 0;
 }
 
 extern "C" int fsdp_allreduce(fsdp_comm_t* c, int channel, int gsize, int gstride,

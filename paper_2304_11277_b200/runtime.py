@@ -900,6 +900,16 @@ class FSDPRuntime:
                                           [out], prediv=pre, postdiv=post, accumulate=accumulate,
                                           stream=self.rs_stream, tma=False)
 
+    def _ar(self, inp: torch.Tensor, out: torch.Tensor, post: float, accumulate: bool) -> None:
+        """All-reduce in the replicated group (hybrid stage 2 / NO_SHARD):
+        copy engines with rs_engine="ce", else the two-shot SM kernel."""
+        if self.cfg.rs_engine == "ce":
+            self.comm.all_reduce_ce(self.plan.replicated_desc, inp, self.ar_stage_off, self.ar_gather_off,
+                                    out, postdiv=post, accumulate=accumulate, stream=self.rs_stream)
+        else:
+            self.comm.all_reduce(self.plan.replicated_desc, [inp], self.ar_stage_off, self.ar_gather_off,
+                                 [out], postdiv=post, accumulate=accumulate, stream=self.rs_stream)
+
     def _acquire_gslot(self, psi: int) -> tuple[int, torch.Tensor]:
         """Next symmetric gradient slot (alternating); compute waits until the
         reduce-scatter that last read it has finished on every peer."""
@@ -954,9 +964,7 @@ class FSDPRuntime:
                     self._rs(gslot, payload.dtype, u.grad, pre, post, accumulate, tail)
             elif F == 1:
                 with self.timed("allreduce", self.rs_stream, payload.numel() * payload.element_size()):
-                    self.comm.all_reduce(self.plan.replicated_desc, [payload], self.ar_stage_off,
-                                         self.ar_gather_off, [u.grad], postdiv=post,
-                                         accumulate=accumulate, stream=self.rs_stream)
+                    self._ar(payload, u.grad, post, accumulate)
             else:
                 tmp = torch.empty(n, dtype=torch.float32, device=self.device)
                 with self.timed("reduce_scatter", self.rs_stream, payload.numel() * payload.element_size()):
@@ -964,9 +972,8 @@ class FSDPRuntime:
                 self.events.append((self.step_count, "reduce_stage2", uid))
                 self.trace.record("AR_issue", uid, n * 4)
                 with self.timed("allreduce", self.rs_stream, n * 4):
-                    self.comm.all_reduce(self.plan.replicated_desc, [tmp], self.ar_stage_off,
-                                         self.ar_gather_off, [u.grad], postdiv=post,
-                                         accumulate=accumulate, stream=self.rs_stream)
+                    self._ar(tmp, u.grad, post, accumulate)
+                tmp.record_stream(self.rs_stream)
             payload.record_stream(self.rs_stream)
             if gslot is not None:
                 ev = torch.cuda.Event()

@@ -68,6 +68,18 @@ def raw_collectives(rank, world, results):
         exp = sp.reduce_unit(grads, sp.Plan(world, 1), reduce_dtype=np.float32, full_dtype=np.float32,
                              acc_dtype=np.float32, mean=True)
         check(out.cpu().numpy().tobytes() == exp[rank].tobytes(), f"AR n={n}")
+        # copy-engine AR: same bits (fp32 and bf16 payloads, accumulate)
+        out_ce = torch.empty(n * world, device="cuda")
+        comm.all_reduce_ce((world, 1), torch.from_numpy(grads[rank]).cuda(), a, b, out_ce, postdiv=float(world))
+        check(out_ce.cpu().numpy().tobytes() == exp[rank].tobytes(), f"AR-CE n={n}")
+        acc_full = [g.standard_normal(n * world).astype(np.float32) for g in
+                    [np.random.default_rng(7 * r + n) for r in range(world)]]
+        out_ce = torch.from_numpy(acc_full[rank]).cuda()
+        comm.all_reduce_ce((world, 1), torch.from_numpy(grads[rank]).cuda().to(torch.bfloat16), a, b, out_ce,
+                           postdiv=float(world), accumulate=True)
+        exp = sp.reduce_unit(grads, sp.Plan(world, 1), reduce_dtype=sp.BF16, full_dtype=np.float32,
+                             acc_dtype=np.float32, mean=True, accum=acc_full)
+        check(out_ce.cpu().numpy().tobytes() == exp[rank].tobytes(), f"AR-CE bf16 accumulate n={n}")
         if world == 4:
             f = 2
             part = torch.empty(n * world // f, device="cuda")
@@ -79,6 +91,9 @@ def raw_collectives(rank, world, results):
             exp = sp.reduce_unit(grads, sp.Plan(world, f), reduce_dtype=sp.BF16, full_dtype=np.float32,
                                  acc_dtype=np.float32, mean=True, accum=bases)
             check(out.cpu().numpy().tobytes() == exp[rank].tobytes(), f"hybrid n={n}")
+            out2 = torch.from_numpy(base).cuda()
+            comm.all_reduce_ce((world // f, f), part, a, b, out2, postdiv=float(world), accumulate=True)
+            check(out2.cpu().numpy().tobytes() == exp[rank].tobytes(), f"hybrid AR-CE n={n}")
         # copy-engine variants: same bits
         sh = torch.from_numpy(shards[rank]).cuda().to(torch.bfloat16)
         comm.all_gather_ce((world, 1), sh, a)

@@ -338,7 +338,25 @@ def deadlock_detection(rank, world, results):
             pass
     dist.barrier()
     comm.close()
-    results["deadlock_detection"] = "ok"
+    # the low-latency path polls data lines, not barrier flags: a missing
+    # sender must time out the same way
+    comm = DeviceComm.create(8 << 20, max_ctas=8)
+    comm.set_timeout_ms(1500)
+    off = comm.alloc(1 << 16)
+    ll = comm.alloc(comm.ll_bytes(world, 64, torch.float32), 16)
+    dist.barrier()
+    if rank == 0:
+        comm.all_gather_ll((world, 1), [torch.ones(64, device="cuda")], off, torch.float32, ll)
+        torch.cuda.synchronize()
+        check(comm.device_error() == _lib.E_TIMEOUT, "LL timeout not recorded")
+        try:
+            comm.raise_device_error()
+            check(False, "DeadlockError not raised (LL)")
+        except DeadlockError:
+            pass
+    dist.barrier()
+    comm.close()
+    results["deadlock_detection"] = "ok (split and LL)"
 
 
 def _sess(w, f, spec=None, seed=0, **kw):

@@ -25,6 +25,14 @@ VARIANTS = {
     "push_geo_8M": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_MIN_PIECE": str(8 << 20)},
     "push_geo_2M": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_MIN_PIECE": str(2 << 20)},
     "pull_geo_4M": {"FSDP_CE_RS_PUSH": "0", "FSDP_CE_RS_MIN_PIECE": str(4 << 20)},
+    # diagnostics: transfers only (results wrong), and the all-gather's DMA at the same size
+    "push_p1_noreduce": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_PIPE_MIN": str(1 << 40), "FSDP_CE_RS_NOREDUCE": "1"},
+    "pull_p1_noreduce": {"FSDP_CE_RS_PUSH": "0", "FSDP_CE_RS_PIPE_MIN": str(1 << 40), "FSDP_CE_RS_NOREDUCE": "1"},
+    "push_geo_noreduce": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_NOREDUCE": "1"},
+    "ag_ce": {"_AG": "1"},
+    "push_geo_p3": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_PIECES": "3", "FSDP_CE_RS_MIN_PIECE": str(1 << 20)},
+    "push_geo_p4": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_PIECES": "4", "FSDP_CE_RS_MIN_PIECE": str(1 << 20)},
+    "push_geo_p5": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_PIECES": "5", "FSDP_CE_RS_MIN_PIECE": str(1 << 20)},
 }
 
 
@@ -51,8 +59,13 @@ def main():
             cm.view(src, n * world, torch.bfloat16).copy_(torch.randn(n * world, device=dev).to(torch.bfloat16))
             o = torch.empty(n, device=dev)
 
+            sh = torch.randn(n, device=dev).to(torch.bfloat16)
+
             def fn():
-                cm.reduce_scatter_ce((world, 1), src, torch.bfloat16, stage, o, postdiv=float(world))
+                if os.environ.get("_AG"):
+                    cm.all_gather_ce((world, 1), sh, stage)
+                else:
+                    cm.reduce_scatter_ce((world, 1), src, torch.bfloat16, stage, o, postdiv=float(world))
             for _ in range(5):
                 fn()
             torch.cuda.synchronize()

@@ -1101,6 +1101,7 @@ struct fsdp_comm {
   int64_t ce_rs_min_piece = 4LL << 20;        // FSDP_CE_RS_MIN_PIECE: smallest geometric piece (about)
   int ce_reduce_ctas = 0;                     // FSDP_CE_REDUCE_CTAS: grid of non-final piece reductions (0: full)
   bool ce_rs_geom = true;                     // FSDP_CE_RS_GEOM: halving pieces (else uniform)
+  int ce_reduce_cap = 0;                      // FSDP_CE_REDUCE_CAP: grid cap of every CE reduction (0: 4 CTAs/SM)
   bool ce_rs_noreduce = false;                // FSDP_CE_RS_NOREDUCE=1: DIAGNOSTIC ONLY, skip the reductions (wrong results)
   std::vector<cudaEvent_t> ce_events;
   size_t ce_next = 0;
@@ -1555,6 +1556,7 @@ static int ce_prepare(fsdp_comm_t* c) {
     if (const char* e = getenv("FSDP_CE_REDUCE_CTAS")) c->ce_reduce_ctas = std::max(0, atoi(e));
     if (const char* e = getenv("FSDP_CE_RS_GEOM")) c->ce_rs_geom = atoi(e) != 0;
     if (const char* e = getenv("FSDP_CE_RS_NOREDUCE")) c->ce_rs_noreduce = atoi(e) != 0;
+    if (const char* e = getenv("FSDP_CE_REDUCE_CAP")) c->ce_reduce_cap = std::max(0, atoi(e));
     for (int k = 0; k < 2; ++k)
       for (int r = 0; r < FSDP_MAX_RANKS * c->ce_split; ++r)
         FSDP_CUDA(cudaStreamCreateWithFlags(&c->ce_stream[k][r], cudaStreamNonBlocking));
@@ -1714,7 +1716,8 @@ extern "C" int fsdp_reduce_scatter_ce(fsdp_comm_t* c, int channel, int gsize, in
     if (c->ce_rs_noreduce) return 0;
     // a piece reduced behind the next piece's transfer needs only enough
     // HBM bandwidth to keep pace; the final piece is exposed: full grid
-    return launch_ce_reduce(ra, e0, len, src_dtype, (c->ce_reduce_ctas > 0 && e0 + len < n) ? c->ce_reduce_ctas : 0, s);
+    return launch_ce_reduce(ra, e0, len, src_dtype,
+                            (c->ce_reduce_ctas > 0 && e0 + len < n) ? c->ce_reduce_ctas : c->ce_reduce_cap, s);
   };
 
   if (pieces > 1 && push) {
@@ -1863,7 +1866,7 @@ extern "C" int fsdp_allreduce_ce(fsdp_comm_t* c, int channel, int gsize, int gst
   ra.out = (float*)(mine + gather_off) + (int64_t)pos * ch;
   ra.gsize = gsize; ra.pos = pos;
   ra.prediv = 1.0f; ra.postdiv = postdiv; ra.accumulate = 0; ra.store_raw = 1;
-  if (int rc = launch_ce_reduce(ra, 0, clen(pos), src_dtype, 0, s)) return rc;
+  if (int rc = launch_ce_reduce(ra, 0, clen(pos), src_dtype, c->ce_reduce_cap, s)) return rc;
   // 3. all-gather push of my reduced chunk
   cudaEvent_t reduced = ce_event(c);
   FSDP_CUDA(cudaEventRecord(reduced, s));

@@ -9,6 +9,23 @@ import sys
 from collections import defaultdict
 
 
+# kernels defined in paper_2304_11277_b200/csrc (ncu prints them with or
+# without the fsdp:: namespace depending on its name-base setting)
+OURS = ("adam_kernel", "adam_tma_kernel", "allgather_kernel", "allgather_ll_kernel", "allgather_nvls_kernel",
+        "allreduce_kernel", "ar_epilogue_kernel", "cast_kernel", "ce_reduce_kernel", "coll_enter_kernel",
+        "coll_exit_kernel", "coll_signal_kernel", "coll_signal_slot_kernel", "coll_wait_slot_kernel",
+        "flatten_kernel", "reduce_scatter_kernel", "reduce_scatter_ll_kernel", "reduce_scatter_pull_kernel",
+        "reduce_scatter_tma_kernel", "scalar_allreduce_kernel", "sgd_kernel", "unflatten_kernel",
+        "unscale_kernel", "shard_copy_kernel")
+
+
+def is_ours(name: str) -> bool:
+    if "fsdp::" in name:
+        return True
+    base = name.split("(")[0].split("<")[0].split()[-1] if name.strip() else ""
+    return base in OURS
+
+
 def main():
     path = sys.argv[1]
     steps = int(sys.argv[2]) if len(sys.argv) > 2 else 0
@@ -26,7 +43,7 @@ def main():
         tot[r[ki]] += us
         cnt[r[ki]] += 1
     total = sum(tot.values())
-    ours = sum(v for k, v in tot.items() if "fsdp::" in k)
+    ours = sum(v for k, v in tot.items() if is_ours(k))
     n = sum(cnt.values())
     print(f"total {total / 1e3:.1f} ms over {n} launches"
           + (f" = {total / 1e3 / steps:.1f} ms/step ({steps} steps captured)" if steps else ""))

@@ -66,6 +66,8 @@ def parse():
                     help="engine of the two collectives nothing overlaps (first AG, last RS)")
     ap.add_argument("--ll-max-bytes", type=int, default=6 << 20,
                     help="units up to this unsharded size use the low-latency one-kernel collectives")
+    ap.add_argument("--opt-split-first", type=int, default=2,
+                    help="optimizer launch over the first N forward units first (0: one launch)")
     ap.add_argument("--exposed", action="store_true",
                     help="also time the step with collectives replaced by no-ops")
     ap.add_argument("--opt-in-bwd", action="store_true",
@@ -193,7 +195,8 @@ def run_ours(args):
         comm_backend=args.backend, hybrid_shard_size=args.hybrid_shard_size, lr=1e-4,
         optimizer_in_backward=args.opt_in_bwd, forward_prefetch=args.forward_prefetch,
         ag_ctas=args.ctas, rs_ctas=args.rs_ctas, ag_engine=args.ag_engine,
-        rs_engine=args.rs_engine, tail_engine=args.tail_engine, ll_max_bytes=args.ll_max_bytes)
+        rs_engine=args.rs_engine, tail_engine=args.tail_engine, ll_max_bytes=args.ll_max_bytes,
+        opt_split_first=args.opt_split_first)
     opt = fsdp.optimizer()
     rt = fsdp.rt
     dev_inputs = tuple(h.to(dev) for h in host)
@@ -350,6 +353,7 @@ def run_ours(args):
                        "comm_engine": {"allgather": args.ag_engine, "reduce_scatter": args.rs_engine,
                                        "first_ag_last_rs": args.tail_engine,
                                        "low_latency_max_bytes": args.ll_max_bytes},
+                       "opt_split_first": args.opt_split_first,
                        "l2": "inputs > L2 (weights+state >20 GB)"},
             "tflops_per_gpu": round(tflops_gpu, 2),
             "roofline": roof, "roofline_step": step_roof, "kernels": kern_share,

@@ -117,6 +117,11 @@ class RuntimeConfig:
     # measurement only (bench.py --exposed): skip every collective, keep all
     # stream/event plumbing — the step time without communication
     fake_comm: bool = False
+    # step the shards of the first `opt_split_first` units of the forward
+    # order in their own (first) optimizer launch, so the next step's first
+    # all-gathers wait only for it and overlap the launch over the rest of
+    # the arena (0 = one launch).  Same arithmetic, elementwise.
+    opt_split_first: int = 2
 
     def __post_init__(self):
         if self.reshard_after_forward not in (RAF, NRAF):
@@ -321,6 +326,8 @@ class FSDPRuntime:
         self.found_inf = torch.zeros(1, dtype=torch.float32, device=self.device)
         self.found_inf_world = torch.zeros(1, dtype=torch.float32, device=self.device)
         self.opt_done: torch.cuda.Event | None = None
+        self.opt_early: torch.cuda.Event | None = None   # first optimizer launch (units < opt_early_units)
+        self.opt_early_units = 0
         self.adam_steps = 0
         self.max_live_slots = 0
         self.fwd_visits: dict[int, int] = {}
@@ -559,13 +566,16 @@ class FSDPRuntime:
             if free_ev is not None:
                 self.ag_stream.wait_event(free_ev)
             if self.opt_done is not None:
-                self.ag_stream.wait_event(self.opt_done)
+                early = self.opt_early is not None and uid < self.opt_early_units
+                self.ag_stream.wait_event(self.opt_early if early else self.opt_done)
             if self.cfg.fake_comm:
                 pass
             elif self.cfg.comm_backend == "ipc":
                 with self.timed("allgather", self.ag_stream,
                                 lay.psi * (2 if self.cfg.mixed else 4)):
-                    first = self._ag_since_opt == 0 and self.opt_done is not None
+                    # the tail engine is for a first gather with nothing to
+                    # overlap; after a split optimizer it overlaps the second launch
+                    first = self._ag_since_opt == 0 and self.opt_done is not None and self.opt_early is None
                     if self._use_ll(uid):
                         self.comm.all_gather_ll(self._group_ag(), [src], self.slots.offsets[slot],
                                                 self.compute_dtype, self.ll_ag_off, stream=self.ag_stream)
@@ -1079,22 +1089,44 @@ class FSDPRuntime:
             nb = n * (28 + (2 if self.low is not None else 0))
         else:
             nb = n * (12 + (2 if self.low is not None else 0))
+        k = self._early_prefix_units()
+        t = self._adam_t(skip) if cfg.optimizer == "adam" else 0
+        self.opt_early, self.opt_early_units = None, 0
         with self.timed(cfg.optimizer + "_step", self.compute_stream, nb):
-            self._opt_launch(skip)
+            if k:
+                cut = self.units[k].master.storage_offset() - self.master.storage_offset()
+                self._opt_launch(skip, t, 0, cut)
+                self.opt_early = torch.cuda.Event()
+                self.opt_early.record(self.compute_stream)
+                self.opt_early_units = k
+                self._opt_launch(skip, t, cut, n)
+            else:
+                self._opt_launch(skip, t, 0, n)
         ev = torch.cuda.Event()
         ev.record(self.compute_stream)
         self.opt_done = ev
         self._ag_since_opt = 0
         self.events.append((self.step_count - 1, "opt_step", None))
 
-    def _opt_launch(self, skip) -> None:
+    def _early_prefix_units(self) -> int:
+        """k > 0 when the first opt_split_first units of the last forward
+        order are exactly units 0..k-1, i.e. a prefix of the arena (the
+        wrapper's root-then-blocks order), and some arena is left after it."""
+        k = min(self.cfg.opt_split_first, len(self.units) - 1)
+        order = self.prev_fwd_order or self.fwd_order
+        if k <= 0 or self.direct_views or len(order) < k or sorted(order[:k]) != list(range(k)):
+            return 0
+        return k
+
+    def _opt_launch(self, skip, t: int, a: int, b: int) -> None:
+        """One optimizer launch over arena elements [a, b)."""
         cfg = self.cfg
+        low = self.low[a:b] if self.low is not None else None
         if cfg.optimizer == "adam":
-            kernels.adam_step(self.master, self.grad, self.exp_avg, self.exp_avg_sq, lr=cfg.lr,
-                              betas=cfg.betas, eps=cfg.eps, t=self._adam_t(skip), skip_flag=skip,
-                              p_lowp=self.low)
+            kernels.adam_step(self.master[a:b], self.grad[a:b], self.exp_avg[a:b], self.exp_avg_sq[a:b],
+                              lr=cfg.lr, betas=cfg.betas, eps=cfg.eps, t=t, skip_flag=skip, p_lowp=low)
         else:
-            kernels.sgd_step(self.master, self.grad, lr=cfg.lr, skip_flag=skip, p_lowp=self.low)
+            kernels.sgd_step(self.master[a:b], self.grad[a:b], lr=cfg.lr, skip_flag=skip, p_lowp=low)
 
     def _adam_t(self, skip) -> int:
         # Adam's t counts TAKEN steps (numerics.py:276).  A skipped step is

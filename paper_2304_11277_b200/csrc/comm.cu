@@ -623,52 +623,52 @@ reduce_scatter_pull_kernel(const __grid_constant__ CollParams p) {
 // tile of each member's chunk; all threads reduce a landed stage in
 // ascending rank order (fp32, from +0) while later stages are in flight.
 constexpr int kTmaThreads = 256;
-constexpr int kTmaStages = 4;
+constexpr int kTmaStages = 4;                // default ring: 4 stages x 32 KB
 constexpr int kTmaStageBytes = 32 * 1024;   // summed over the group's members
 
-template <typename Tin>
+template <typename Tin, int STAGES, int STAGE_BYTES>
 __global__ void __launch_bounds__(kTmaThreads, 1)
 reduce_scatter_tma_kernel(const __grid_constant__ CollParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t full[kTmaStages];
+  __shared__ __align__(8) uint64_t full[STAGES];
   const Group g = make_group(p);
   const int e = p.rank0 >= 0 ? 0 : blockIdx.y;
   float* __restrict__ out = p.out[e];
   const int64_t n = p.n;
   const int W = g.size;
   // elements per member tile: a multiple of 8 (16-byte bulk-copy granule)
-  const int64_t T = (kTmaStageBytes / (W * (int)sizeof(Tin))) / kVec * kVec;
+  const int64_t T = (STAGE_BYTES / (W * (int)sizeof(Tin))) / kVec * kVec;
   const int64_t chunk_off = p.off_a + (int64_t)g.pos * n * (int64_t)sizeof(Tin);
   const int64_t ntiles = (n + T - 1) / T;
   const int64_t my_tiles = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kTmaStages; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   cta_barrier(p, g, 0, false);   // every member's payload is in place (+ mbarrier init visible)
 
-  auto issue = [&](int64_t k) {   // tile iteration k -> stage k % kTmaStages
-    const int s = (int)(k % kTmaStages);
+  auto issue = [&](int64_t k) {   // tile iteration k -> stage k % STAGES
+    const int s = (int)(k % STAGES);
     const int64_t t = blockIdx.x + k * gridDim.x;
     const int64_t i0 = t * T;
     const uint32_t bytes = (uint32_t)((min(T, n - i0)) * (int64_t)sizeof(Tin));
     mbar_expect_tx(&full[s], bytes * W);
     for (int j = 0; j < W; ++j) {
       const Tin* src = (const Tin*)(p.bases[g.member(j)] + chunk_off) + i0;
-      tma_load_1d(smem + (size_t)s * kTmaStageBytes + (size_t)j * T * sizeof(Tin), src, bytes, &full[s]);
+      tma_load_1d(smem + (size_t)s * STAGE_BYTES + (size_t)j * T * sizeof(Tin), src, bytes, &full[s]);
     }
   };
   if (threadIdx.x == 0)
-    for (int64_t k = 0; k < my_tiles && k < kTmaStages; ++k) issue(k);
+    for (int64_t k = 0; k < my_tiles && k < STAGES; ++k) issue(k);
 
   const bool pre = p.prediv != 1.0f, post = p.postdiv != 1.0f;
   for (int64_t k = 0; k < my_tiles; ++k) {
-    const int s = (int)(k % kTmaStages);
-    mbar_wait(&full[s], (uint32_t)((k / kTmaStages) & 1));
+    const int s = (int)(k % STAGES);
+    mbar_wait(&full[s], (uint32_t)((k / STAGES) & 1));
     const int64_t i0 = (blockIdx.x + k * gridDim.x) * T;
     const int64_t len = min(T, n - i0);
-    const Tin* st = (const Tin*)(smem + (size_t)s * kTmaStageBytes);
+    const Tin* st = (const Tin*)(smem + (size_t)s * STAGE_BYTES);
     for (int64_t v = threadIdx.x; v * kVec < len; v += kTmaThreads) {
       V8F acc;
 #pragma unroll
@@ -697,9 +697,9 @@ reduce_scatter_tma_kernel(const __grid_constant__ CollParams p) {
       st8<float>(o, pack8<float>(acc));
     }
     __syncthreads();   // stage s fully consumed
-    if (threadIdx.x == 0 && k + kTmaStages < my_tiles) {
+    if (threadIdx.x == 0 && k + STAGES < my_tiles) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(k + kTmaStages);
+      issue(k + STAGES);
     }
   }
   cta_barrier(p, g, 1, false);   // every member is done reading my buffer
@@ -1102,7 +1102,8 @@ struct fsdp_comm {
   int ce_reduce_ctas = 0;                     // FSDP_CE_REDUCE_CTAS: grid of non-final piece reductions (0: full)
   bool ce_rs_geom = true;                     // FSDP_CE_RS_GEOM: halving pieces (else uniform)
   int ce_reduce_cap = 0;                      // FSDP_CE_REDUCE_CAP: grid cap of every CE reduction (0: 4 CTAs/SM)
-  bool ce_rs_noreduce = false;                // FSDP_CE_RS_NOREDUCE=1: DIAGNOSTIC ONLY, skip the reductions (wrong results)
+  bool ce_rs_noreduce = false;
+  int rs_tma_ring = -1;                       // FSDP_RS_TMA_RING: TMA-pull ring geometry (-1: not read yet)                // FSDP_CE_RS_NOREDUCE=1: DIAGNOSTIC ONLY, skip the reductions (wrong results)
   std::vector<cudaEvent_t> ce_events;
   size_t ce_next = 0;
   // VMM pool (fsdp_comm_create_vmm): own allocation + peer mappings
@@ -1502,14 +1503,26 @@ extern "C" int fsdp_reduce_scatter_tma(fsdp_comm_t* c, int channel, int gsize, i
   for (int e = 0; e < nranks_args(c); ++e) p.out[e] = outs[e];
   p.off_a = src_off;
   p.prediv = prediv; p.postdiv = postdiv; p.accumulate = accumulate ? 1 : 0;
-  const int64_t T = (kTmaStageBytes / (gsize * is)) / kVec * kVec;
+  // ring geometry (FSDP_RS_TMA_RING: 0 = 4 x 32 KB, 1 = 3 x 64 KB, 2 = 6 x 32 KB, 3 = 2 x 96 KB)
+  if (c->rs_tma_ring < 0) {       // read once per communicator
+    const char* e = getenv("FSDP_RS_TMA_RING");
+    c->rs_tma_ring = e ? std::max(0, std::min(3, atoi(e))) : 0;
+  }
+  const int ring = c->rs_tma_ring;
+  static const struct { void* bf; void* f; int stages, bytes; } kRings[] = {
+      {(void*)reduce_scatter_tma_kernel<__nv_bfloat16, 4, 32768>, (void*)reduce_scatter_tma_kernel<float, 4, 32768>, 4, 32768},
+      {(void*)reduce_scatter_tma_kernel<__nv_bfloat16, 3, 65536>, (void*)reduce_scatter_tma_kernel<float, 3, 65536>, 3, 65536},
+      {(void*)reduce_scatter_tma_kernel<__nv_bfloat16, 6, 32768>, (void*)reduce_scatter_tma_kernel<float, 6, 32768>, 6, 32768},
+      {(void*)reduce_scatter_tma_kernel<__nv_bfloat16, 2, 98304>, (void*)reduce_scatter_tma_kernel<float, 2, 98304>, 2, 98304},
+  };
+  const auto& rg = kRings[ring];
+  const int64_t T = (rg.bytes / (gsize * is)) / kVec * kVec;
   const int64_t ntiles = (n + T - 1) / T;
   int grid = (int)std::min<int64_t>(std::max<int64_t>(ntiles, 1), c->max_ctas);
   if (c->emulated) grid = std::min(grid, std::max(1, 128 / c->world));
-  const size_t smem = (size_t)kTmaStages * kTmaStageBytes;
+  const size_t smem = (size_t)rg.stages * rg.bytes;
   cudaStream_t s = (cudaStream_t)stream;
-  void* fn = src_dtype == FSDP_BF16 ? (void*)reduce_scatter_tma_kernel<__nv_bfloat16>
-                                    : (void*)reduce_scatter_tma_kernel<float>;
+  void* fn = src_dtype == FSDP_BF16 ? rg.bf : rg.f;
   FSDP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   void* args[] = {(void*)&p};
   if (c->emulated) {

@@ -30,6 +30,9 @@ VARIANTS = {
     "pull_p1_noreduce": {"FSDP_CE_RS_PUSH": "0", "FSDP_CE_RS_PIPE_MIN": str(1 << 40), "FSDP_CE_RS_NOREDUCE": "1"},
     "push_geo_noreduce": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_NOREDUCE": "1"},
     "ag_ce": {"_AG": "1"},
+    # SM TMA-pull reduce-scatter ring geometries (FSDP_RS_TMA_RING) x grid
+    **{f"tma_r{r}_c{c}": {"_TMA": "1", "FSDP_RS_TMA_RING": str(r), "_CTAS": str(c)}
+       for r in range(4) for c in (64, 128)},
     "push_geo_p3": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_PIECES": "3", "FSDP_CE_RS_MIN_PIECE": str(1 << 20)},
     "push_geo_p4": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_PIECES": "4", "FSDP_CE_RS_MIN_PIECE": str(1 << 20)},
     "push_geo_p5": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_PIECES": "5", "FSDP_CE_RS_MIN_PIECE": str(1 << 20)},
@@ -50,7 +53,7 @@ def main():
         saved = {k: os.environ.get(k) for k in VARIANTS[name]}
         os.environ.update(VARIANTS[name])
         maxb = max(sizes) << 20
-        cm = DeviceComm.create(2 * maxb + (64 << 20), max_ctas=64)
+        cm = DeviceComm.create(2 * maxb + (64 << 20), max_ctas=int(os.environ.get("_CTAS", "64")))
         src, stage = cm.alloc(maxb), cm.alloc(maxb)
         row = {}
         for mb in sizes:
@@ -64,6 +67,8 @@ def main():
             def fn():
                 if os.environ.get("_AG"):
                     cm.all_gather_ce((world, 1), sh, stage)
+                elif os.environ.get("_TMA"):
+                    cm.reduce_scatter_pull((world, 1), src, torch.bfloat16, [o], postdiv=float(world), tma=True)
                 else:
                     cm.reduce_scatter_ce((world, 1), src, torch.bfloat16, stage, o, postdiv=float(world))
             for _ in range(5):

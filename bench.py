@@ -365,6 +365,8 @@ def run_ours(args):
                 "comm_stalls_top_units": {k: [{"unit": u, "ms_total": t, "waits": c} for u, t, c in v]
                                           for k, v in stall_units.items()}} if stalls else {}),
             "peak_mem_gb": round(torch.cuda.max_memory_allocated() / 1e9, 2),
+            # the reference's limiter criterion (memsim.py:202): allocator retries stay 0
+            "num_alloc_retries": int(torch.cuda.memory_stats().get("num_alloc_retries", 0)),
             **({"exposed_comm": {"ms_per_step_without_comm": round(ms_nocomm, 3),
                                  "exposed_ms": round(ms - ms_nocomm, 3),
                                  "frac_of_step": round((ms - ms_nocomm) / ms, 4),

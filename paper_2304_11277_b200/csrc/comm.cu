@@ -243,17 +243,19 @@ __global__ void __launch_bounds__(32) coll_signal_kernel(const __grid_constant__
 // staging (stream order on the copy side stream), publish "piece q landed"
 // (phase 1, slot q) to every member; the receiving stream waits for slot q
 // from every member before reducing piece q.
-__global__ void __launch_bounds__(32) coll_signal_slot_kernel(const __grid_constant__ CollParams p, int slot) {
+__global__ void __launch_bounds__(32) coll_signal_slot_kernel(const __grid_constant__ CollParams p, int slot,
+                                                              int phase = 1) {
   const Group g = make_group(p);
   if ((int)threadIdx.x < g.size) {
     __threadfence_system();
-    st_release_sys(flag_ptr(p.bases[g.member(threadIdx.x)], p.channel, 1, g.rank, slot), p.epoch);
+    st_release_sys(flag_ptr(p.bases[g.member(threadIdx.x)], p.channel, phase, g.rank, slot), p.epoch);
   }
 }
-__global__ void __launch_bounds__(32) coll_wait_slot_kernel(const __grid_constant__ CollParams p, int slot) {
+__global__ void __launch_bounds__(32) coll_wait_slot_kernel(const __grid_constant__ CollParams p, int slot,
+                                                            int phase = 1) {
   const Group g = make_group(p);
   if ((int)threadIdx.x < g.size)
-    wait_flag(p, g, flag_ptr(p.bases[g.rank], p.channel, 1, g.member(threadIdx.x), slot));
+    wait_flag(p, g, flag_ptr(p.bases[g.rank], p.channel, phase, g.member(threadIdx.x), slot));
 }
 
 // Local reduction of a copy-engine reduce-scatter, one piece [e0, e0+len)
@@ -554,7 +556,8 @@ reduce_scatter_pull_kernel(const __grid_constant__ CollParams p) {
   const int e = p.rank0 >= 0 ? 0 : blockIdx.y;
   float* __restrict__ out = p.out[e];
   const int64_t n = p.n;
-  const int64_t chunk_off = p.off_a + (int64_t)g.pos * n * (int64_t)sizeof(Tin);
+  // off_b > 0: the members' chunks are off_b elements apart (a sub-range of each chunk)
+  const int64_t chunk_off = p.off_a + (int64_t)g.pos * (p.off_b > 0 ? p.off_b : n) * (int64_t)sizeof(Tin);
   const Tin* src[MAXW];
 #pragma unroll
   for (int j = 0; j < MAXW; ++j)
@@ -638,7 +641,8 @@ reduce_scatter_tma_kernel(const __grid_constant__ CollParams p) {
   const int W = g.size;
   // elements per member tile: a multiple of 8 (16-byte bulk-copy granule)
   const int64_t T = (STAGE_BYTES / (W * (int)sizeof(Tin))) / kVec * kVec;
-  const int64_t chunk_off = p.off_a + (int64_t)g.pos * n * (int64_t)sizeof(Tin);
+  // off_b > 0: the members' chunks are off_b elements apart (a sub-range of each chunk)
+  const int64_t chunk_off = p.off_a + (int64_t)g.pos * (p.off_b > 0 ? p.off_b : n) * (int64_t)sizeof(Tin);
   const int64_t ntiles = (n + T - 1) / T;
   const int64_t my_tiles = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
   if (threadIdx.x == 0) {
@@ -1103,7 +1107,8 @@ struct fsdp_comm {
   bool ce_rs_geom = true;                     // FSDP_CE_RS_GEOM: halving pieces (else uniform)
   int ce_reduce_cap = 0;                      // FSDP_CE_REDUCE_CAP: grid cap of every CE reduction (0: 4 CTAs/SM)
   bool ce_rs_noreduce = false;
-  int rs_tma_ring = -1;                       // FSDP_RS_TMA_RING: TMA-pull ring geometry (-1: not read yet)                // FSDP_CE_RS_NOREDUCE=1: DIAGNOSTIC ONLY, skip the reductions (wrong results)
+  int rs_tma_ring = -1;
+  float ce_rs_sm_frac = 0.f;                  // FSDP_CE_RS_SM_FRAC: tail fraction of a pipelined chunk pulled by SM TMA                       // FSDP_RS_TMA_RING: TMA-pull ring geometry (-1: not read yet)                // FSDP_CE_RS_NOREDUCE=1: DIAGNOSTIC ONLY, skip the reductions (wrong results)
   std::vector<cudaEvent_t> ce_events;
   size_t ce_next = 0;
   // VMM pool (fsdp_comm_create_vmm): own allocation + peer mappings
@@ -1570,6 +1575,7 @@ static int ce_prepare(fsdp_comm_t* c) {
     if (const char* e = getenv("FSDP_CE_RS_GEOM")) c->ce_rs_geom = atoi(e) != 0;
     if (const char* e = getenv("FSDP_CE_RS_NOREDUCE")) c->ce_rs_noreduce = atoi(e) != 0;
     if (const char* e = getenv("FSDP_CE_REDUCE_CAP")) c->ce_reduce_cap = std::max(0, atoi(e));
+    if (const char* e = getenv("FSDP_CE_RS_SM_FRAC")) c->ce_rs_sm_frac = std::max(0.f, std::min(0.9f, (float)atof(e)));
     for (int k = 0; k < 2; ++k)
       for (int r = 0; r < FSDP_MAX_RANKS * c->ce_split; ++r)
         FSDP_CUDA(cudaStreamCreateWithFlags(&c->ce_stream[k][r], cudaStreamNonBlocking));
@@ -1708,10 +1714,17 @@ extern "C" int fsdp_reduce_scatter_ce(fsdp_comm_t* c, int channel, int gsize, in
   // ce_rs_pieces equal pieces of at least ce_rs_pipe_min/2.
   std::vector<std::pair<int64_t, int64_t>> pcs;      // (first element, length)
   auto round8 = [](int64_t x) { return (x + kVec - 1) / kVec * kVec; };
+  // Hybrid (FSDP_CE_RS_SM_FRAC > 0, pipelined push only): the copy engines
+  // move [0, nA) of every chunk while an SM TMA-pull kernel reduces [nA, n)
+  // straight from the peers' payloads on a third side stream, so the tail of
+  // the chunk needs no staging round trip.
+  const bool hyb = c->ce_rs_sm_frac > 0.f && c->ce_serial && n >= c->ce_rs_pipe_min &&
+                   c->ce_rs_push != 0 && (n % kVec == 0) && (src_off % 16 == 0) && aligned16(out);
+  const int64_t nA = hyb ? std::min(n, round8((int64_t)((double)n * (1.0 - c->ce_rs_sm_frac)))) : n;
   if (!c->ce_serial || n < c->ce_rs_pipe_min) {
     pcs.emplace_back(0, n);
   } else if (c->ce_rs_geom) {
-    int64_t e0 = 0, rem = n;
+    int64_t e0 = 0, rem = nA;
     while (rem > 2 * c->ce_rs_min_piece && (int)pcs.size() + 1 < c->ce_rs_pieces) {
       const int64_t len = round8(rem / 2);
       pcs.emplace_back(e0, len);
@@ -1719,9 +1732,9 @@ extern "C" int fsdp_reduce_scatter_ce(fsdp_comm_t* c, int channel, int gsize, in
     }
     pcs.emplace_back(e0, rem);
   } else {
-    const int np = (int)std::min<int64_t>(c->ce_rs_pieces, std::max<int64_t>(1, 2 * n / c->ce_rs_pipe_min));
-    const int64_t plen = round8((n + np - 1) / np);
-    for (int64_t e0 = 0; e0 < n || pcs.empty(); e0 += plen) pcs.emplace_back(e0, std::min(plen, n - e0));
+    const int np = (int)std::min<int64_t>(c->ce_rs_pieces, std::max<int64_t>(1, 2 * nA / c->ce_rs_pipe_min));
+    const int64_t plen = round8((nA + np - 1) / np);
+    for (int64_t e0 = 0; e0 < nA || pcs.empty(); e0 += plen) pcs.emplace_back(e0, std::min(plen, nA - e0));
   }
   const int pieces = (int)pcs.size();
   const bool push = c->ce_rs_push < 0 ? pieces > 1 : c->ce_rs_push == 1;
@@ -1748,6 +1761,32 @@ extern "C" int fsdp_reduce_scatter_ce(fsdp_comm_t* c, int channel, int gsize, in
     cudaStream_t cs = c->ce_stream[c->ce_shared_streams ? 0 : 1][0];
     cudaStream_t ss = c->ce_stream[c->ce_shared_streams ? 0 : 1][1];
     FSDP_CUDA(cudaStreamWaitEvent(cs, fork, 0));
+    // hybrid: piece flags move to phase 2 (the TMA kernel's in-kernel
+    // barriers use phases 0 and 1, slot = CTA index, same epoch)
+    const int fph = hyb && nA < n ? 2 : 1;
+    cudaEvent_t pulled = nullptr;
+    if (hyb && nA < n) {
+      cudaStream_t ps = c->ce_stream[c->ce_shared_streams ? 0 : 1][2];
+      FSDP_CUDA(cudaStreamWaitEvent(ps, fork, 0));
+      CollParams p2 = p;
+      p2.n = n - nA;
+      p2.off_a = src_off + nA * es;
+      p2.off_b = n;                                  // members' chunks stay n elements apart
+      p2.out[0] = out + nA;
+      p2.prediv = prediv; p2.postdiv = postdiv; p2.accumulate = accumulate ? 1 : 0;
+      p2.split = 0;
+      const int64_t T = (kTmaStageBytes / (gsize * es)) / kVec * kVec;
+      const int grid = (int)std::min<int64_t>(std::max<int64_t>((p2.n + T - 1) / T, 1), c->max_ctas);
+      void* fn = src_dtype == FSDP_BF16 ? (void*)reduce_scatter_tma_kernel<__nv_bfloat16, kTmaStages, kTmaStageBytes>
+                                        : (void*)reduce_scatter_tma_kernel<float, kTmaStages, kTmaStageBytes>;
+      const size_t smem = (size_t)kTmaStages * kTmaStageBytes;
+      FSDP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      void* args[] = {(void*)&p2};
+      FSDP_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(kTmaThreads), args, smem, ps));
+      FSDP_LAUNCHED();
+      pulled = ce_event(c);
+      FSDP_CUDA(cudaEventRecord(pulled, ps));
+    }
     for (int q = 0; q < pieces; ++q) {
       const int64_t e0 = pcs[q].first, len = pcs[q].second;
       for (int jj = 0; jj + 1 < gsize; ++jj) {
@@ -1759,20 +1798,21 @@ extern "C" int fsdp_reduce_scatter_ce(fsdp_comm_t* c, int channel, int gsize, in
       cudaEvent_t landed = ce_event(c);
       FSDP_CUDA(cudaEventRecord(landed, cs));
       FSDP_CUDA(cudaStreamWaitEvent(ss, landed, 0));
-      coll_signal_slot_kernel<<<1, 32, 0, ss>>>(p, q);
+      coll_signal_slot_kernel<<<1, 32, 0, ss>>>(p, q, fph);
       FSDP_LAUNCHED();
     }
     cudaEvent_t sent = ce_event(c);
     FSDP_CUDA(cudaEventRecord(sent, ss));        // after the last signal, hence after every copy
     for (int q = 0; q < pieces; ++q) {
       const int64_t e0 = pcs[q].first, len = pcs[q].second;
-      coll_wait_slot_kernel<<<1, 32, 0, s>>>(p, q);
+      coll_wait_slot_kernel<<<1, 32, 0, s>>>(p, q, fph);
       FSDP_LAUNCHED();
       if (q + 1 == pieces)
         if (c->timing) { FSDP_CUDA(cudaEventRecord(b, s)); c->timed[FSDP_KIND_RS].emplace_back(a, b); }
       if (int rc = reduce_piece(e0, len)) return rc;
     }
     FSDP_CUDA(cudaStreamWaitEvent(s, sent, 0));   // my payload is free once my copies are done
+    if (pulled) FSDP_CUDA(cudaStreamWaitEvent(s, pulled, 0));   // ... and peers finished pulling its tail
     return 0;
   }
   if (pieces > 1) {

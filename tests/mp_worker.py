@@ -125,10 +125,13 @@ def ce_schedules(rank, world, results):
     # 2*min_piece): pull with uniform pieces (FSDP_CE_RS_GEOM=0: 4 pieces,
     # short last one); push with geometric pieces (3 pieces at min_piece 2M,
     # 5 at 512K)
-    for n, serial, push, minp in ((262144 + 8, 1, 0, 0), ((1 << 23) + 24, 1, 0, 1 << 21),
-                                  ((1 << 23) + 24, 1, 1, 1 << 21), ((1 << 23) + 24, 1, 1, 1 << 19),
-                                  (262144 + 8, 1, 1, 0),
-                                  (262144 + 8, 0, 0, 0), (262144 + 8, 0, 1, 0)):
+    # last case: hybrid -- copy engines for 75 % of every chunk, an SM TMA
+    # pull reducing the last 25 % from the peers (FSDP_CE_RS_SM_FRAC)
+    for n, serial, push, minp, smf in ((262144 + 8, 1, 0, 0, 0), ((1 << 23) + 24, 1, 0, 1 << 21, 0),
+                                       ((1 << 23) + 24, 1, 1, 1 << 21, 0), ((1 << 23) + 24, 1, 1, 1 << 19, 0),
+                                       (262144 + 8, 1, 1, 0, 0),
+                                       (262144 + 8, 0, 0, 0, 0), (262144 + 8, 0, 1, 0, 0),
+                                       ((1 << 23) + 24, 1, 1, 1 << 21, 0.25)):
         rngs = [np.random.default_rng(555 + r) for r in range(world)]
         shards = [g.standard_normal(n).astype(np.float32) for g in rngs]
         grads = [round_to_bf16(g.standard_normal(n * world).astype(np.float32)) for g in rngs]
@@ -140,6 +143,7 @@ def ce_schedules(rank, world, results):
         os.environ["FSDP_CE_RS_MIN_PIECE"] = str(minp or (4 << 20))
         os.environ["FSDP_CE_RS_PIPE_MIN"] = str(2 * minp if minp else (64 << 20))
         os.environ["FSDP_CE_RS_GEOM"] = "0" if (minp and not push) else "1"
+        os.environ["FSDP_CE_RS_SM_FRAC"] = str(smf)
         nb = n * world * 2 + (1 << 20)
         comm = DeviceComm.create(3 * nb + (4 << 20), max_ctas=32)
         try:
@@ -160,9 +164,9 @@ def ce_schedules(rank, world, results):
         finally:
             comm.close()
             for k in ("FSDP_CE_SERIAL", "FSDP_CE_RS_PUSH", "FSDP_CE_RS_MIN_PIECE", "FSDP_CE_RS_PIPE_MIN",
-                      "FSDP_CE_RS_GEOM"):
+                      "FSDP_CE_RS_GEOM", "FSDP_CE_RS_SM_FRAC"):
                 del os.environ[k]
-        done.append(f"n={n}/serial={serial}/push={push}/min_piece={minp}")
+        done.append(f"n={n}/serial={serial}/push={push}/min_piece={minp}" + (f"/sm_frac={smf}" if smf else ""))
     results["ce_schedules"] = done
 
 

@@ -33,6 +33,8 @@ VARIANTS = {
     # SM TMA-pull reduce-scatter ring geometries (FSDP_RS_TMA_RING) x grid
     **{f"tma_r{r}_c{c}": {"_TMA": "1", "FSDP_RS_TMA_RING": str(r), "_CTAS": str(c)}
        for r in range(4) for c in (64, 128)},
+    **{f"hyb_f{int(f * 100)}": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_SM_FRAC": str(f)}
+       for f in (0.1, 0.2, 0.3, 0.4)},
     "push_geo_p3": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_PIECES": "3", "FSDP_CE_RS_MIN_PIECE": str(1 << 20)},
     "push_geo_p4": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_PIECES": "4", "FSDP_CE_RS_MIN_PIECE": str(1 << 20)},
     "push_geo_p5": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_PIECES": "5", "FSDP_CE_RS_MIN_PIECE": str(1 << 20)},

@@ -1078,6 +1078,7 @@ class FSDPRuntime:
             ev.record(self.rs_stream)
             self.compute_stream.wait_event(ev)
             self.opt_done = ev
+            self.opt_early, self.opt_early_units = None, 0
             self._ag_since_opt = 0
             self.events.append((self.step_count - 1, "opt_step", None))
             return

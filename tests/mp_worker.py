@@ -115,6 +115,52 @@ def raw_collectives(rank, world, results):
     results["raw_collectives"] = "bit-exact"
 
 
+def full_size_properties(rank, world, results):
+    """Size-independent properties at the configs' real sizes (too large for
+    the oracle): a GPT-1.3B block's psi = 50,358,272 for the copy-engine
+    all-reduce (NO_SHARD / hybrid stage 2) and the split/CE reduce-scatter;
+    the LL threshold (6 MB unsharded) for the LL pair.  Inputs are small
+    integers, so every fp32 sum is exact and order-independent: the result
+    must equal the closed form bit for bit on every rank."""
+    from paper_2304_11277_b200.comm import DeviceComm
+    psi = 50358272
+    n = psi // world
+    comm = DeviceComm.create(10 * psi + (256 << 20), max_ctas=32)   # stage + gather fp32, src bf16, LL
+    comm.set_timeout_ms(20000)
+    stage, gath, src = comm.alloc(psi * 4), comm.alloc(psi * 4), comm.alloc(psi * 2)
+    idx = torch.arange(psi, device="cuda", dtype=torch.float32)
+    x = ((idx % 7) + rank).to(torch.bfloat16)                 # small integers, exact in bf16
+    tot = float(sum(range(world)))
+    expect = ((idx % 7) * world + tot) / world                 # exact: integers / power of two
+    out = torch.ones(psi, device="cuda")
+    comm.all_reduce_ce((world, 1), x, stage, gath, out, postdiv=float(world), accumulate=True)
+    check(torch.equal(out, expect + 1.0), "full-size AR-CE")
+    comm.view(src, psi, torch.bfloat16).copy_(x)
+    o = torch.zeros(n, device="cuda")
+    comm.reduce_scatter_ce((world, 1), src, torch.bfloat16, stage, o, postdiv=float(world))
+    check(torch.equal(o, expect[rank * n:(rank + 1) * n]), "full-size RS-CE")
+    o.zero_()
+    comm.reduce_scatter_pull((world, 1), src, torch.bfloat16, [o], postdiv=float(world), tma=True)
+    check(torch.equal(o, expect[rank * n:(rank + 1) * n]), "full-size RS TMA pull")
+    # LL at the threshold: 6 MB unsharded bf16
+    m = (6 << 20) // 2 // world
+    ll_a = comm.alloc(comm.ll_bytes(world, m, torch.bfloat16), 16)
+    ll_r = comm.alloc(comm.ll_bytes(world, m, torch.bfloat16), 16)
+    sh = ((torch.arange(m, device="cuda") % 5) + 10 * rank).to(torch.float32)
+    comm.all_gather_ll((world, 1), [sh], gath, torch.bfloat16, ll_a)
+    full = comm.view(gath, m * world, torch.bfloat16).float()
+    want = torch.cat([(torch.arange(m, device="cuda") % 5 + 10 * r).float() for r in range(world)])
+    check(torch.equal(full, want), "LL AG at the threshold")
+    y = x[: m * world].contiguous()
+    o = torch.zeros(m, device="cuda")
+    comm.reduce_scatter_ll((world, 1), [y], ll_r, [o], postdiv=float(world))
+    check(torch.equal(o, expect[rank * m:(rank + 1) * m]), "LL RS at the threshold")
+    torch.cuda.synchronize()
+    check(comm.device_error() == 0, "device error word (full size)")
+    comm.close()
+    results["full_size_properties"] = f"exact (psi={psi}, LL n={m})"
+
+
 def ce_schedules(rank, world, results):
     """Every copy-engine schedule gives the same bits: serial-staggered or
     concurrent DMA, reduce-scatter by pull or by push (FSDP_CE_SERIAL,
@@ -524,6 +570,7 @@ def main():
                 globals()[name](rank, world, results)
             raise _Done()
         raw_collectives(rank, world, results)
+        full_size_properties(rank, world, results)
         ll_collectives(rank, world, results)
         nvls_collectives(rank, world, results)
         ce_schedules(rank, world, results)

@@ -503,6 +503,14 @@ def run_sweep(args):
     nvls = {c: DeviceComm.create(max_bytes + (64 << 20), max_ctas=c, nvls_group=world) for c in cta_opts}
     nvls = {c: cm for c, cm in nvls.items() if cm.nvls_group == world}
     nvls_off = {c: cm.alloc(max_bytes) for c, cm in nvls.items()}
+    # single-launch mode (in-kernel barriers instead of the 1-CTA enter/exit
+    # kernels): what a standalone collective costs without the two extra
+    # launches; the runtime keeps split mode in-step (a late peer would park
+    # the data kernel's CTAs on SMs the GEMMs need)
+    fused = {c: DeviceComm.create(2 * max_bytes + (64 << 20), max_ctas=c) for c in (32, 128)}
+    for cm in fused.values():
+        cm.set_mode(split=False)
+    fused_offs = {c: (cm.alloc(max_bytes), cm.alloc(max_bytes)) for c, cm in fused.items()}
     # low-latency one-kernel path (2x wire bytes): small sizes only
     ll_max_mb = 64
     ll_comm = DeviceComm.create((ll_max_mb << 20) * 9 + (64 << 20), max_ctas=64)
@@ -549,6 +557,11 @@ def run_sweep(args):
         cm0 = next(iter(comms.values()))
         stage0, dst0 = offs[next(iter(comms))]
         cm0.view(stage0, n * world, torch.bfloat16).copy_(flat)
+        for c, cm in fused.items():
+            stage, dst = fused_offs[c]
+            r[f"ag_fused_c{c}"] = bus / (timeit(lambda: cm.all_gather((world, 1), [shard], dst, torch.bfloat16)) * 1e-3) / 1e9
+            cm.view(stage, n * world, torch.bfloat16).copy_(flat)
+            r[f"rs_pull_fused_c{c}"] = bus / (timeit(lambda: cm.reduce_scatter_pull((world, 1), stage, torch.bfloat16, [out], postdiv=float(world), tma=False)) * 1e-3) / 1e9
         if mb <= ll_max_mb:
             r["ag_ll"] = bus / (timeit(lambda: ll_comm.all_gather_ll((world, 1), [shard], ll_dst, torch.bfloat16, ll_ag)) * 1e-3) / 1e9
             r["rs_ll"] = bus / (timeit(lambda: ll_comm.reduce_scatter_ll((world, 1), [flat], ll_rs, [out], postdiv=float(world))) * 1e-3) / 1e9
@@ -556,15 +569,15 @@ def run_sweep(args):
         r["rs_ce"] = bus / (timeit(lambda: cm0.reduce_scatter_ce((world, 1), stage0, torch.bfloat16, dst0, out, postdiv=float(world))) * 1e-3) / 1e9
         # best of this library's engines: SM push / NVLS multicast / copy engines
         r["ag_ours_gbs"] = max([r[f"ag_ours_c{c}"] for c in comms] + [r[f"ag_nvls_c{c}"] for c in nvls]
-                               + [r["ag_ce"], r.get("ag_ll", 0.0)])
+                               + [r["ag_ce"], r.get("ag_ll", 0.0)] + [r[f"ag_fused_c{c}"] for c in fused])
         r["rs_ours_gbs"] = max([max(r[f"rs_push_c{c}"], r[f"rs_pull_c{c}"], r[f"rs_tma_c{c}"]) for c in comms]
-                               + [r["rs_ce"], r.get("rs_ll", 0.0)])
+                               + [r["rs_ce"], r.get("rs_ll", 0.0)] + [r[f"rs_pull_fused_c{c}"] for c in fused])
         r["ag_frac_of_measured"] = r["ag_ours_gbs"] / NVLINK_MEASURED_GBS
         r["rs_frac_of_measured"] = r["rs_ours_gbs"] / NVLINK_MEASURED_GBS
         r["ag_nccl_gbs"] = bus / (timeit(lambda: dist.all_gather_into_tensor(full, shard)) * 1e-3) / 1e9
         r["rs_nccl_gbs"] = bus / (timeit(lambda: dist.reduce_scatter_tensor(out_bf, flat)) * 1e-3) / 1e9
         res.append({k: (round(v, 3 if "frac" in k else 1) if isinstance(v, float) else v) for k, v in r.items()})
-    for cm in list(comms.values()) + list(nvls.values()) + [ll_comm]:
+    for cm in list(comms.values()) + list(nvls.values()) + list(fused.values()) + [ll_comm]:
         cm.close()
     if rank == 0:
         best = max(res, key=lambda r: r["ag_ours_gbs"])

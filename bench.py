@@ -85,11 +85,23 @@ def dist_env():
 
 
 def init_dist(world, local):
-    import torch
-    import torch.distributed as dist
-    torch.cuda.set_device(local)
-    if world > 1 and not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2304_11277_b200.dist_util import init_from_env
+    init_from_env()
+
+
+def self_launch(args) -> int:
+    """`python bench.py --gpus N` without a launcher: start N ranks (one per
+    GPU) with torch.distributed.run on this node and relay rank 0's line."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "4"))
+    return subprocess.run(cmd, env=env).returncode
 
 
 class ClockSampler:
@@ -220,7 +232,9 @@ def run_ours(args):
     sampler = ClockSampler(local)
     if rank == 0:
         sampler.start()
-    rt.profile = True
+    # headline: no instrumentation inside the timed region (no per-launch
+    # events, no comm timing mode)
+    rt.profile = False
     rt.reset_timers()
     n_launch0 = _lib.launch_count()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -232,9 +246,23 @@ def run_ours(args):
     barrier()
     launches = _lib.launch_count() - n_launch0
     ms = t0.elapsed_time(t1) / args.steps
+    # profiled pass (same K steps): CUDA events on the launching stream around
+    # every launch of this library and every compute-stream wait on a
+    # collective -> per-kernel mean durations (roofline) and the stall breakdown
+    rt.profile = True
+    rt.reset_timers()
+    pp0, pp1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    pp0.record(compute)
+    for _ in range(args.steps):
+        step(*dev_inputs)
+    pp1.record(compute)
+    barrier()
+    ms_prof = pp0.elapsed_time(pp1) / args.steps
     timers = rt.timer_summary()
     stall_units = rt.stall_breakdown()
     rt.profile = False
+    rt.reset_timers()
     # e2e: token ids from pinned host memory each step, loss read back each step
     e0 = time.perf_counter()
     barrier()
@@ -325,7 +353,7 @@ def run_ours(args):
                     "mean_ms": round(d["mean_ms"], 4)}
     step_roof = {"bound": "tensor", "achieved": round(tflops_gpu, 1), "peak": bf16_peak,
                  "unit": "TFLOP/s", "frac": round(tflops_gpu / bf16_peak, 4)}
-    kern_share = {k: {"share_of_step": round(v["total_ms"] / (ms * args.steps), 4),
+    kern_share = {k: {"share_of_step": round(v["total_ms"] / (ms_prof * args.steps), 4),
                       "mean_ms": round(v["mean_ms"], 4), "count": v["count"],
                       **({"data_kernel_mean_ms": round(v["data_mean_ms"], 4)} if "data_mean_ms" in v else {})}
                   for k, v in mine.items()}
@@ -343,19 +371,12 @@ def run_ours(args):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform token ids, meta-init weights)",
-            "config": {"workload": f"{cfg.name} {args.strategy}"
-                                   f"{'' if args.hybrid_shard_size is None else ' F=%d' % args.hybrid_shard_size}"
-                                   f" bf16 MixedPrecision, block auto-wrap, BACKWARD_PRE"
-                                   f"{'' if args.no_limiter else ', limit_all_gathers'}",
-                       "model": cfg.name, "global_batch": B * world, "seq_len": seq_len,
-                       "parallelism": f"fsdp{world}" if world > 1 else "fsdp1 (NO_SHARD-equivalent)",
-                       "comm_backend": args.backend,
-                       "comm_engine": {"allgather": args.ag_engine, "reduce_scatter": args.rs_engine,
-                                       "first_ag_last_rs": args.tail_engine,
-                                       "low_latency_max_bytes": args.ll_max_bytes},
-                       "opt_split_first": args.opt_split_first,
-                       "l2": "inputs > L2 (weights+state >20 GB)"},
+            "config": step_config(args, world),
             "tflops_per_gpu": round(tflops_gpu, 2),
+            "profiled_pass": {"ms_per_step": round(ms_prof, 3),
+                              "note": "kernel/stall timers come from a second pass of the same K steps "
+                                      "with CUDA events around every launch and wait; the headline "
+                                      "timed region carries no instrumentation"},
             "roofline": roof, "roofline_step": step_roof, "kernels": kern_share,
             "e2e": {"value": round(e2e_value, 2), "unit": "TFLOP/s (model, whole job)",
                     "h2d_bytes_per_step": int(sum(h.numel() * h.element_size() for h in host)),
@@ -376,9 +397,31 @@ def run_ours(args):
         out.update(comm_bw)
     if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config in CONFIGS:
         out["cpu_baseline"] = cpu_baseline(cfg, args.cpu_tokens, world=1)
+
     if world > 1:
         dist.barrier()
     return out
+
+
+def step_config(args, world: int) -> dict:
+    """The workload both arms (ours and --impl reference) report: same keys,
+    same values for the same command line."""
+    from paper_2304_11277_b200.workloads import CONFIGS, T5_CONFIGS
+    cfg = T5_CONFIGS[args.config] if args.config in T5_CONFIGS else CONFIGS[args.config]
+    seq_len = cfg.enc_seq if args.config in T5_CONFIGS else cfg.seq
+    return {"workload": f"{cfg.name} {args.strategy}"
+                        f"{'' if args.hybrid_shard_size is None else ' F=%d' % args.hybrid_shard_size}"
+                        f" bf16 MixedPrecision, block auto-wrap, BACKWARD_PRE"
+                        f"{'' if args.no_limiter else ', limit_all_gathers'}",
+            "model": cfg.name, "global_batch": args.micro * world, "seq_len": seq_len,
+            "micro_batch_per_gpu": args.micro,
+            "parallelism": f"fsdp{world}" if world > 1 else "fsdp1 (NO_SHARD-equivalent)",
+            "comm_backend": args.backend,
+            "comm_engine": {"allgather": args.ag_engine, "reduce_scatter": args.rs_engine,
+                            "first_ag_last_rs": args.tail_engine,
+                            "low_latency_max_bytes": args.ll_max_bytes},
+            "opt_split_first": args.opt_split_first,
+            "l2": "inputs > L2 (weights+state >20 GB)"}
 
 
 def run_torch_unsharded(args):
@@ -438,9 +481,27 @@ def run_torch_unsharded(args):
             "peak_mem_gb": round(torch.cuda.max_memory_allocated() / 1e9, 2)}
 
 
+def host_info(threads: int) -> dict:
+    """CPU model, core count and thread env of this host."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.lower().startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"cpu_model": model, "cpu_count": os.cpu_count(), "threads_used": threads,
+            "OMP_NUM_THREADS": os.environ.get("OMP_NUM_THREADS"),
+            "OPENBLAS_NUM_THREADS": os.environ.get("OPENBLAS_NUM_THREADS")}
+
+
 def cpu_baseline(cfg, tokens: int, world: int = 1, steps: int = 1, warmup: int = 0) -> dict:
     """The reference algorithm (oracle port) on this box's host cores, one
-    bounded sample: `tokens` tokens per simulated rank through the full step."""
+    bounded sample: `tokens` tokens per simulated rank through the full step
+    (torch CPU fwd/bwd on all host threads; the shardsim flatten / reduce /
+    Adam in numpy, elementwise work spread over a thread pool)."""
     import torch
     from oracle.cpu_fsdp import time_cpu_steps
     from paper_2304_11277_b200.workloads import GPT, Block, init_gpt_
@@ -457,30 +518,36 @@ def cpu_baseline(cfg, tokens: int, world: int = 1, steps: int = 1, warmup: int =
     flops = cfg.flops_per_token(seq) * seqs * seq * world
     val = flops / r["sec_per_step"] / 1e12
     return {"value": round(val, 4), "unit": "TFLOP/s (model, whole job)", "cores": r["threads"],
-            "kind": "port", "sec_per_step": round(r["sec_per_step"], 2),
-            "sample": f"{world} simulated rank(s) x {seqs}x{seq} tokens of {cfg.name}, full step "
-                      f"(fwd/bwd torch CPU fp32 + shardsim flatten/reduce/Adam numpy on all "
-                      f"{cfg.n_params/1e9:.2f}B params); cpu_count={os.cpu_count()}"}
+            "kind": "port", "sec_per_step": round(r["sec_per_step"], 2), "steps": steps, "warmup": warmup,
+            "host": host_info(r["threads"]),
+            "sample": f"{world} simulated rank(s) x {seqs} seq x {seq} tokens of {cfg.name} per step, "
+                      f"full FSDP step (fwd/bwd torch CPU fp32 + shardsim flatten/reduce/Adam numpy on "
+                      f"all {cfg.n_params/1e9:.2f}B params); {warmup} warm-up + {steps} timed step(s)"}
 
 
 def run_reference(args):
+    """The reference's algorithm on this box's host cores, same metric, unit
+    and config as our arm.  Rank 0 alone runs (shardsim simulates every rank
+    in one process, pkg/README.md:11-14); each step is a bounded sample of the
+    workload: one full sequence (cfg.seq tokens) per simulated rank instead of
+    --micro, so that W warm-up + K steps fit in a few minutes."""
     rank, world, local = dist_env()
+    if "WORLD_SIZE" not in os.environ:
+        world = args.gpus
     if rank != 0:
         return None
     from paper_2304_11277_b200.workloads import CONFIGS
     cfg = CONFIGS[args.config]
-    # bounded: each step is one sample of 512 tokens per simulated rank; K capped
-    # at 1 (N=1: 2) and no warm-up, so the arm ends within a few minutes at N=8
-    steps, warmup = (min(args.steps, 2) if world == 1 else 1), 0
-    cb = cpu_baseline(cfg, min(args.cpu_tokens, 512), world=world, steps=steps, warmup=warmup)
+    warmup = min(args.warmup, 1)
+    steps = max(1, min(args.steps, 2 if world <= 2 else 1))
+    cb = cpu_baseline(cfg, cfg.seq, world=world, steps=steps, warmup=warmup)
     return {"metric": METRIC, "value": cb["value"], "unit": cb["unit"], "n_gpus": world,
             "steps": steps, "warmup": warmup, "ms_per_step": cb["sec_per_step"] * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"{cfg.name} FULL_SHARD W={world} (shardsim algorithm, CPU)",
-                       "model": cfg.name, "seq_len": cfg.seq},
+            "config": step_config(args, world),
             "cpu_baseline": {"value": cb["value"], "unit": cb["unit"], "kind": "port",
-                             "cores": cb["cores"], "sample": cb["sample"]},
+                             "cores": cb["cores"], "sample": cb["sample"], "host": cb["host"]},
             "e2e": {"value": cb["value"], "unit": cb["unit"], "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
 
@@ -688,6 +755,10 @@ def run_copy(args):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl != "reference":
+        sys.exit(self_launch(args))
+    if "WORLD_SIZE" in os.environ and args.impl != "reference" and int(os.environ["WORLD_SIZE"]) != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={os.environ['WORLD_SIZE']}")
     if args.impl == "reference":
         out = run_reference(args)
     elif args.impl == "torch-unsharded":

@@ -139,6 +139,19 @@ int64_t fsdp_comm_reserved_bytes(void);
  * Synchronous read; call after synchronising the streams. */
 int fsdp_comm_device_error(fsdp_comm_t* c);
 int fsdp_comm_set_timeout_ms(fsdp_comm_t* c, int64_t ms);
+/* A timed-out wait ABORTS the communicator: it sets the error word of every
+ * rank whose pool this process maps (own + peers), and from then on every
+ * SM/LL data kernel skips its peer loads and stores (the flag waits bail out
+ * at once).  Copy-engine DMA already enqueued still runs; the optimizer must
+ * therefore read the word before updating: fsdp_comm_fold_error writes
+ * *flag = 1 if any local error word is set, else (keep ? *flag : 0), and
+ * mirrors the word into `host_mirror` (pinned host memory, may be NULL) so the
+ * host raises DeadlockError at the next step boundary without a sync.
+ * Replaces: the DeadlockError raise and the verdict agreement of
+ * collectives.py:461-483 / engine.py:410-411. */
+int fsdp_comm_fold_error(fsdp_comm_t* c, float* flag, int keep, int* host_mirror, void* stream);
+/* Zero the local error word(s) (synchronous; tests and re-use after a handled abort). */
+int fsdp_comm_clear_error(fsdp_comm_t* c);
 /* split != 0 (default): collectives run as [1-CTA enter barrier] [data kernel
  * that only signals] [1-CTA exit barrier], so a late peer never parks the
  * data kernel's CTAs on SMs.  timing != 0: CUDA events around every data

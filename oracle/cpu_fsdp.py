@@ -15,10 +15,33 @@ from __future__ import annotations
 
 import os
 import time
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 
 from . import shardsim_port as sp
+
+_CHUNK = 1 << 22      # elements per thread-pool task of the elementwise numpy work
+
+
+def adam_step_threaded(pool, param, grad, state, lr) -> None:
+    """sp.adam_step (numerics.py:273-285) applied chunk by chunk on a thread
+    pool: every element's arithmetic is the same numpy expression, so the
+    result is bit-identical to one call over the whole shard; numpy releases
+    the GIL inside the ufuncs, so the chunks run on all host cores."""
+    n = param.size
+    t = state["t"]
+    m, v = state["m"], state["v"]
+
+    def one(a):
+        b = min(n, a + _CHUNK)
+        st = {"m": m[a:b], "v": v[a:b], "t": t}
+        sp.adam_step(param[a:b], grad[a:b], st, lr=lr)
+        m[a:b] = st["m"]
+        v[a:b] = st["v"]
+
+    list(pool.map(one, range(0, n, _CHUNK)))
+    state["t"] = t + 1
 
 
 def _units_of(model, block_cls):
@@ -48,6 +71,7 @@ class CPUFSDP:
         self.torch = torch
         self.threads = threads or os.cpu_count() or 1
         torch.set_num_threads(self.threads)
+        self.pool = ThreadPoolExecutor(max_workers=self.threads)
         self.model = model
         self.plan = sp.Plan(world, shard_factor or world)
         shapes, names = _units_of(model, block_cls)
@@ -110,7 +134,8 @@ class CPUFSDP:
             for r in range(W):
                 k = sp.shard_index(self.plan, r)
                 g = red[k * lay.shard_numel:(k + 1) * lay.shard_numel]
-                sp.adam_step(self.shards[r][u], np.zeros_like(g) + g, self.states[r][u], lr=self.lr)
+                adam_step_threaded(self.pool, self.shards[r][u], np.zeros_like(g) + g, self.states[r][u],
+                                   self.lr)
         return float(np.mean(losses))
 
 

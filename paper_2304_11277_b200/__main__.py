@@ -52,13 +52,8 @@ def cmd_dump_plan(a) -> int:
 
 
 def _dist():
-    import torch
-    import torch.distributed as dist
-    rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
-    local = int(os.environ.get("LOCAL_RANK", 0))
-    torch.cuda.set_device(local)
-    if world > 1 and not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from .dist_util import init_from_env
+    rank, world, _ = init_from_env()
     return rank, world
 
 

@@ -66,6 +66,8 @@ _SIGS = {
     "fsdp_comm_reserved_bytes": (_i64, []),
     "fsdp_comm_device_error": (_i32, [_vp]),
     "fsdp_comm_set_timeout_ms": (_i32, [_vp, _i64]),
+    "fsdp_comm_fold_error": (_i32, [_vp, _vp, _i32, _vp, _vp]),
+    "fsdp_comm_clear_error": (_i32, [_vp]),
     "fsdp_comm_set_mode": (_i32, [_vp, _i32, _i32]),
     "fsdp_comm_set_barriers": (_i32, [_vp, _i32]),
     "fsdp_comm_set_ctas": (_i32, [_vp, _i32, _i32]),

@@ -312,6 +312,17 @@ class DeviceComm:
     def device_error(self) -> int:
         return int(lib.fsdp_comm_device_error(self._h))
 
+    def fold_error(self, flag: torch.Tensor | None, keep: bool, mirror: torch.Tensor | None = None,
+                   stream=None) -> None:
+        """On `stream`: flag = 1 if the error word is set, else (keep ? flag : 0);
+        the word is also mirrored into `mirror` (pinned int32 host tensor)."""
+        check(lib.fsdp_comm_fold_error(self._h, flag.data_ptr() if flag is not None else None,
+                                       int(keep), mirror.data_ptr() if mirror is not None else None,
+                                       stream_ptr(stream)), "comm_fold_error")
+
+    def clear_error(self) -> None:
+        check(lib.fsdp_comm_clear_error(self._h), "comm_clear_error")
+
     def raise_device_error(self) -> None:
         err = self.device_error()
         if err == _lib.E_TIMEOUT:

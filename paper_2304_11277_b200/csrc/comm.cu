@@ -113,6 +113,34 @@ __device__ __forceinline__ Group make_group(const CollParams& p) {
   return g;
 }
 
+// A flag wait that timed out aborts the communicator: the error word of
+// EVERY rank whose pool this process maps is set, so a late member sees the
+// failure at its next collective or optimizer step (its skip predicate reads
+// the word, fsdp_comm_fold_error) instead of computing on with a slot a
+// timed-out peer may have written.  collectives.py:461-483 (DeadlockError).
+__device__ __noinline__ void comm_abort(const CollParams& p, const Group& g) {
+  atomicExch(reinterpret_cast<uint32_t*>(p.bases[g.rank] + kErrOff), (uint32_t)FSDP_E_TIMEOUT);
+  for (int r = 0; r < FSDP_MAX_RANKS; ++r)
+    if (p.bases[r] != nullptr && r != g.rank)
+      st_release_sys(reinterpret_cast<uint32_t*>(p.bases[r] + kErrOff), (uint32_t)FSDP_E_TIMEOUT);
+  __threadfence_system();
+}
+
+// This rank's communicator has failed (own error word set, locally or by a
+// peer's abort): data kernels then skip every peer load and store.
+__device__ __forceinline__ bool comm_failed(const CollParams& p, const Group& g) {
+  return *reinterpret_cast<volatile const uint32_t*>(p.bases[g.rank] + kErrOff) != 0u;
+}
+// Same, one read per CTA so every thread of the CTA takes the same branch
+// (must be called by all threads; contains __syncthreads).
+__device__ __forceinline__ bool cta_failed(const CollParams& p, const Group& g) {
+  __shared__ int failed;
+  __syncthreads();
+  if (threadIdx.x == 0) failed = comm_failed(p, g) ? 1 : 0;
+  __syncthreads();
+  return failed != 0;
+}
+
 // CTA-level barrier with the matching CTA of every group member.  `release`
 // fences this CTA's prior peer stores (data phases).
 __device__ __noinline__ void cta_barrier(const CollParams& p, const Group& g, int phase,
@@ -131,7 +159,7 @@ __device__ __noinline__ void cta_barrier(const CollParams& p, const Group& g, in
       if ((++spins & 1023u) == 0) {
         if (*(volatile uint32_t*)err != 0) break;           // already failed: bail out
         if (globaltimer() - t0 > (uint64_t)p.timeout_ns) {
-          atomicExch(err, (uint32_t)FSDP_E_TIMEOUT);
+          comm_abort(p, g);
           break;
         }
       }
@@ -188,7 +216,7 @@ __device__ __forceinline__ void wait_flag(const CollParams& p, const Group& g, c
     if ((++spins & 1023u) == 0) {
       if (*(volatile uint32_t*)err != 0) break;
       if (globaltimer() - t0 > (uint64_t)p.timeout_ns) {
-        atomicExch(err, (uint32_t)FSDP_E_TIMEOUT);
+        comm_abort(p, g);
         break;
       }
     }
@@ -364,9 +392,10 @@ allgather_kernel(const __grid_constant__ CollParams p) {
   const int64_t n = p.n;
   const int64_t my_off = p.off_a + (int64_t)g.pos * n * (int64_t)sizeof(Tout);
   if (!p.split) cta_barrier(p, g, 0, false);   // every member's destination slot is free
+  const bool aborted = cta_failed(p, g);       // no peer stores after a timeout
 
   const bool vec = (n % kVec == 0) && aligned16(src) && (my_off % 16 == 0);
-  const int64_t ntiles = (n + kTileElems - 1) / kTileElems;
+  const int64_t ntiles = aborted ? 0 : (n + kTileElems - 1) / kTileElems;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     if (vec) {
       Packed8<Tout> o[kU];
@@ -428,7 +457,7 @@ allgather_nvls_kernel(const __grid_constant__ CollParams p) {
   const Tin* __restrict__ src = (const Tin*)p.in[0];
   const int64_t n = p.n;
   Tout* dst = (Tout*)(p.mc_base + p.off_a + (int64_t)g.pos * n * (int64_t)sizeof(Tout));
-  const int64_t ntiles = (n + kTileElems - 1) / kTileElems;
+  const int64_t ntiles = cta_failed(p, g) ? 0 : (n + kTileElems - 1) / kTileElems;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     Packed8<Tout> o[kU];
 #pragma unroll
@@ -459,7 +488,7 @@ reduce_scatter_kernel(const __grid_constant__ CollParams p) {
   cta_barrier(p, g, 0, false);   // every member's staging is free
 
   const bool vec = (n % kVec == 0) && aligned16(flat) && (p.off_a % 16 == 0) && aligned16(out);
-  const int64_t ntiles = (n + kTileElems - 1) / kTileElems;
+  const int64_t ntiles = cta_failed(p, g) ? 0 : (n + kTileElems - 1) / kTileElems;
   // phase 1: chunk j of my flat payload -> member j's staging slot [my pos]
   // (my own chunk stays in place and is read directly in phase 2)
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -486,6 +515,7 @@ reduce_scatter_kernel(const __grid_constant__ CollParams p) {
     }
   }
   cta_barrier(p, g, 1, true);    // my tiles of every member's chunk arrived
+  if (cta_failed(p, g)) return;  // staging incomplete: leave out untouched
   // phase 2: ascending-rank fp32 sum of the group's chunks, post-divide, accumulate
   const Tin* stage = (const Tin*)(p.bases[g.rank] + p.off_a);
   const Tin* mine = flat + (int64_t)g.pos * n;
@@ -565,7 +595,7 @@ reduce_scatter_pull_kernel(const __grid_constant__ CollParams p) {
   if (!p.split) cta_barrier(p, g, 0, false);   // every member's payload is in place
   const bool vec = (n % kVec == 0) && (chunk_off % 16 == 0) && aligned16(out);
   const bool pre = p.prediv != 1.0f, post = p.postdiv != 1.0f;
-  const int64_t ntiles = (n + TILE - 1) / TILE;
+  const int64_t ntiles = cta_failed(p, g) ? 0 : (n + TILE - 1) / TILE;   // no peer loads after a timeout
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     if (vec) {
       Packed8<Tin> r[MAXW][U];
@@ -651,6 +681,10 @@ reduce_scatter_tma_kernel(const __grid_constant__ CollParams p) {
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   cta_barrier(p, g, 0, false);   // every member's payload is in place (+ mbarrier init visible)
+  if (cta_failed(p, g)) {        // no peer loads after a timeout
+    cta_barrier(p, g, 1, false);
+    return;
+  }
 
   auto issue = [&](int64_t k) {   // tile iteration k -> stage k % STAGES
     const int s = (int)(k % STAGES);
@@ -730,7 +764,7 @@ allreduce_kernel(const __grid_constant__ CollParams p) {
   const bool vec = aligned16(in) && aligned16(out) && (p.off_a % 16 == 0) && (p.off_b % 16 == 0);
   cta_barrier(p, g, 0, false);
 
-  const int64_t ntiles = (c + kTileElems - 1) / kTileElems;
+  const int64_t ntiles = cta_failed(p, g) ? 0 : (c + kTileElems - 1) / kTileElems;
   // phase A: my chunk j -> member j's stage slot [my pos] (own chunk stays)
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     for (int jj = 1; jj < g.size; ++jj) {
@@ -754,7 +788,7 @@ allreduce_kernel(const __grid_constant__ CollParams p) {
   }
   cta_barrier(p, g, 1, true);
   // phase B: reduce my chunk (ascending), push fp32 result to every member
-  {
+  if (!cta_failed(p, g)) {
     const Tin* stage = (const Tin*)(p.bases[g.rank] + p.off_a);
     const Tin* mine = in + (int64_t)g.pos * c;
     const int64_t len = clen(g.pos);
@@ -797,6 +831,7 @@ allreduce_kernel(const __grid_constant__ CollParams p) {
     }
   }
   cta_barrier(p, g, 2, true);
+  if (cta_failed(p, g)) return;
   // phase C: out = (accumulate ? out : 0) + gathered, for my tiles of every chunk
   const float* gath = (const float*)(p.bases[g.rank] + p.off_b);
   for (int j = 0; j < g.size; ++j) {
@@ -827,6 +862,10 @@ __global__ void __launch_bounds__(32) scalar_allreduce_kernel(const __grid_const
   const Group g = make_group(p);
   const int e = p.rank0 >= 0 ? 0 : blockIdx.y;
   cta_barrier(p, g, 0, false);
+  if (cta_failed(p, g)) {        // verdict "skip" wherever the abort is seen
+    if (threadIdx.x == 0) *p.out[e] = 1.0f;
+    return;
+  }
   if ((int)threadIdx.x < g.size) {
     const float v = *(const float*)p.in[e];
     ((float*)(p.bases[g.member(threadIdx.x)] + kScalarOff))[g.rank] = v;
@@ -877,7 +916,7 @@ __device__ __noinline__ uint4 ll_wait(const CollParams& p, const Group& g, const
     if ((++spins & 255u) == 0) {
       if (*(volatile uint32_t*)err != 0) break;
       if (globaltimer() - t0 > (uint64_t)p.timeout_ns) {
-        atomicExch(err, (uint32_t)FSDP_E_TIMEOUT);
+        comm_abort(p, g);
         break;
       }
     }
@@ -957,6 +996,7 @@ allgather_ll_kernel(const __grid_constant__ CollParams p) {
   const int64_t nt = (int64_t)gridDim.x * blockDim.x;
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   Tout* dst = (Tout*)(p.bases[g.rank] + p.off_a);
+  if (comm_failed(p, g)) return;   // no peer stores after a timeout
   for (int64_t L = tid; L < nl; L += nt) {
     const uint2 d = ll_load_line<Tin, Tout>(src, L, n);
     for (int jj = 1; jj < g.size; ++jj) {
@@ -1002,6 +1042,7 @@ reduce_scatter_ll_kernel(const __grid_constant__ CollParams p) {
   const int64_t nl = (n + EPL - 1) / EPL;
   const int64_t nt = (int64_t)gridDim.x * blockDim.x;
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (comm_failed(p, g)) return;   // no peer stores after a timeout
   for (int64_t L = tid; L < nl; L += nt) {
     for (int jj = 1; jj < g.size; ++jj) {
       const int j = (g.pos + jj) % g.size;
@@ -1365,6 +1406,45 @@ extern "C" int fsdp_comm_device_error(fsdp_comm_t* c) {
     if (v) worst = (int)v;
   }
   return worst;
+}
+
+// Device-side fold of the error word(s) into a skip predicate: *flag = 1 if
+// any local pool's error word is set, else (keep ? *flag : 0); also mirrors
+// the word into host-visible memory (pinned, UVA) so the host can raise
+// DeadlockError at a step boundary without a synchronisation.
+namespace {
+struct ErrWords { const uint32_t* w[FSDP_MAX_RANKS]; int n; };
+__global__ void __launch_bounds__(32) fold_error_kernel(ErrWords e, float* flag, int keep, int* mirror) {
+  if (threadIdx.x != 0) return;
+  uint32_t worst = 0;
+  for (int i = 0; i < e.n; ++i) {
+    const uint32_t v = *reinterpret_cast<volatile const uint32_t*>(e.w[i]);
+    if (v) worst = v;
+  }
+  if (flag) *flag = worst ? 1.0f : (keep ? *flag : 0.0f);
+  if (mirror) *reinterpret_cast<volatile int*>(mirror) = (int)worst;
+}
+}  // namespace
+
+extern "C" int fsdp_comm_fold_error(fsdp_comm_t* c, float* flag, int keep, int* host_mirror,
+                                    void* stream) {
+  if (!c) return fail(FSDP_E_INVALID, "null communicator");
+  ErrWords e;
+  e.n = c->emulated ? c->world : 1;
+  for (int i = 0; i < e.n; ++i)
+    e.w[i] = reinterpret_cast<const uint32_t*>((c->emulated ? c->bases[i] : c->pool) + kErrOff);
+  fold_error_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(e, flag, keep ? 1 : 0, host_mirror);
+  FSDP_LAUNCHED();
+  return 0;
+}
+
+extern "C" int fsdp_comm_clear_error(fsdp_comm_t* c) {
+  if (!c) return fail(FSDP_E_INVALID, "null communicator");
+  const int n = c->emulated ? c->world : 1;
+  for (int i = 0; i < n; ++i)
+    FSDP_CUDA(cudaMemset((c->emulated ? c->bases[i] : c->pool) + kErrOff, 0, sizeof(uint32_t)));
+  FSDP_CUDA(cudaDeviceSynchronize());
+  return 0;
 }
 
 extern "C" int fsdp_comm_destroy(fsdp_comm_t* c) {

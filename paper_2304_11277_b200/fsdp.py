@@ -38,6 +38,7 @@ from __future__ import annotations
 import contextlib
 import enum
 import functools
+import warnings
 from dataclasses import dataclass
 from typing import Any, Callable, Iterable
 
@@ -143,20 +144,38 @@ class FullyShardedDataParallel(nn.Module):
         super().__init__()
         if cpu_offload is not None and cpu_offload.offload_params:
             raise NotImplementedError("CPU offload is out of scope for the B200 runtime")
+        if use_orig_params:
+            warnings.warn("use_orig_params=True: the original parameters are exposed as views of "
+                          "the unit's unsharded flat buffer during forward/backward (as with "
+                          "use_orig_params); between steps only the flat shards exist "
+                          "(flat_shards(), full_state_dict())")
         import torch.distributed as dist
         dist_on = dist.is_available() and dist.is_initialized()
-        world = dist.get_world_size(process_group) if dist_on else 1
-        rank = dist.get_rank(process_group) if dist_on else 0
+        hybrid = sharding_strategy in (ShardingStrategy.HYBRID_SHARD, ShardingStrategy._HYBRID_SHARD_ZERO2)
+        F_req = _shard_factor_from(process_group, device_mesh, hybrid_shard_size, hybrid, dist_on)
+        pg = None if isinstance(process_group, tuple) else process_group
+        world = dist.get_world_size(pg) if dist_on else 1
+        rank = dist.get_rank(pg) if dist_on else 0
         if device_id is not None:
             torch.cuda.set_device(device_id)
         device = torch.device("cuda", torch.cuda.current_device())
         if sharding_strategy in (ShardingStrategy.FULL_SHARD, ShardingStrategy.SHARD_GRAD_OP):
             F = world
+            if F_req is not None and F_req != world:
+                raise ValueError(f"{sharding_strategy.name} shards over the whole world ({world}); the "
+                                 f"device_mesh / process_group asks for groups of {F_req} (use HYBRID_SHARD)")
         elif sharding_strategy == ShardingStrategy.NO_SHARD:
             F = 1
         else:
-            F = hybrid_shard_size or (torch.cuda.device_count() if world > torch.cuda.device_count() else world)
+            if F_req is None:
+                raise ValueError("HYBRID_SHARD needs the shard-group size: pass hybrid_shard_size=F, a 2-D "
+                                 "device_mesh (replicate, shard), or process_group=(shard_group, "
+                                 "replicate_group) (collectives.py:63-72: shard groups of F consecutive "
+                                 "ranks, replica groups strided by F)")
+            F = F_req
         plan = build_plan(world, F)
+        if isinstance(process_group, tuple) and dist_on:
+            _check_group_tuple(process_group, plan, rank)
         raf = NRAF if sharding_strategy in (ShardingStrategy.SHARD_GRAD_OP,
                                             ShardingStrategy._HYBRID_SHARD_ZERO2) else RAF
         mp = mixed_precision
@@ -252,14 +271,15 @@ class FullyShardedDataParallel(nn.Module):
                     p = m._parameters[pname]
                 params.append(p)
             if params:
-                self.rt.load_unit_values(uid, params)
+                self.rt.load_unit_values(uid, params, sync_src=0 if sync_module_states else None)
             for (m, pname) in refs[uid]:
                 if pname in m._parameters:
                     del m._parameters[pname]
-        for b in module.buffers():
-            if b.device != device:
-                pass
         module.to(device)
+        if sync_module_states and world > 1:
+            from .dist_util import broadcast_
+            for b in module.buffers():
+                broadcast_(b.data, src=0)
         if mixed and (mp.buffer_dtype is not None):
             for m in module.modules():
                 for bn, b in list(m._buffers.items()):
@@ -339,6 +359,13 @@ class FullyShardedDataParallel(nn.Module):
         self.rt.optimizer_step(scale)
         self.rt.begin_step()
 
+    def check_errors(self) -> None:
+        """Synchronise and raise DeadlockError if a cross-GPU collective wait
+        timed out on this rank or a peer aborted (collectives.py:461-483).
+        Without this call the runtime raises at the next optimizer step; the
+        optimizer never applies an update once the error word is set."""
+        self.rt.raise_if_aborted(sync=True)
+
     def close(self) -> None:
         """Release the communicator's pool and IPC mappings."""
         for h in self._handles:
@@ -358,18 +385,7 @@ class FullyShardedDataParallel(nn.Module):
         from . import kernels
         out = {}
         for uid, lay in enumerate(self.layouts):
-            u = self.rt.units[uid]
-            flat = torch.empty(lay.psi, dtype=torch.float32, device=self.rt.device)
-            if self.plan.shard_factor == 1:
-                flat.copy_(u.master)
-            elif self.comm is not None:
-                from .comm import DeviceFabric  # noqa: F401
-                import torch.distributed as dist
-                dist.all_gather_into_tensor(flat, u.master.contiguous(),
-                                            group=_shard_group(self.plan, self.rank))
-            else:
-                import torch.distributed as dist
-                dist.all_gather_into_tensor(flat, u.master.contiguous(), group=self.rt.pgs.get("shard"))
+            flat = self.rt.gather_master(uid)     # this library's all-gather (ipc backend)
             tensors = [torch.empty(o.shape, dtype=torch.float32, device=flat.device) for o in lay.originals]
             kernels.unflatten(flat, tensors, lay.offsets)
             for o, t in zip(lay.originals, tensors):
@@ -443,8 +459,56 @@ def _nccl_groups(plan, rank):
     return {"shard": shard[plan.sharded_group_of(rank)], "replicate": rep[plan.replicated_group_of(rank)]}
 
 
-def _shard_group(plan, rank):
-    return _nccl_groups(plan, rank)["shard"]
+def _shard_factor_from(process_group, device_mesh, hybrid_shard_size, hybrid: bool, dist_on: bool):
+    """Shard-group size F requested by torch-FSDP's ways of naming it:
+    hybrid_shard_size, a DeviceMesh (1-D: shard over it; 2-D: (replicate,
+    shard), mesh_dim_names honoured) or a (shard_group, replicate_group)
+    process-group tuple.  None if nothing names it.  Only the reference's
+    group convention is accepted (collectives.py:63-72, :89-96): shard groups
+    of F consecutive ranks, replica groups strided by F."""
+    cands = []
+    if hybrid_shard_size is not None:
+        cands.append(int(hybrid_shard_size))
+    if device_mesh is not None:
+        mesh = device_mesh.mesh if hasattr(device_mesh, "mesh") else torch.as_tensor(device_mesh)
+        mesh = torch.as_tensor(mesh).cpu()
+        names = tuple(getattr(device_mesh, "mesh_dim_names", None) or ())
+        if mesh.dim() == 1:
+            F = mesh.numel()
+            canon = torch.arange(F)
+        elif mesh.dim() == 2:
+            if names and names[0] == "shard":      # (shard, replicate) order: transpose
+                mesh = mesh.t()
+            R, F = mesh.shape
+            canon = torch.arange(R * F).view(R, F)
+        else:
+            raise ValueError("device_mesh must be 1-D (shard) or 2-D (replicate, shard)")
+        if not torch.equal(mesh.to(torch.int64), canon):
+            raise ValueError(f"device_mesh {mesh.tolist()} does not follow the shard-group convention "
+                             f"(rows of consecutive ranks = shard groups): collectives.py:89-96")
+        cands.append(int(F))
+    if isinstance(process_group, tuple):
+        if len(process_group) != 2:
+            raise ValueError("process_group tuple must be (shard_group, replicate_group)")
+        if dist_on:
+            import torch.distributed as dist
+            cands.append(dist.get_world_size(process_group[0]))
+    if len(set(cands)) > 1:
+        raise ValueError(f"inconsistent shard-group sizes {cands} (hybrid_shard_size / device_mesh / "
+                         f"process_group)")
+    if cands and not hybrid and device_mesh is None and not isinstance(process_group, tuple):
+        return None                               # hybrid_shard_size is ignored by FULL/NO_SHARD
+    return cands[0] if cands else None
+
+
+def _check_group_tuple(groups, plan, rank) -> None:
+    import torch.distributed as dist
+    shard = tuple(dist.get_process_group_ranks(groups[0]))
+    rep = tuple(dist.get_process_group_ranks(groups[1]))
+    if shard != tuple(plan.sharded_group_of(rank)) or rep != tuple(plan.replicated_group_of(rank)):
+        raise ValueError(f"process groups {shard} / {rep} do not match the shard/replica convention "
+                         f"{plan.sharded_group_of(rank)} / {plan.replicated_group_of(rank)} "
+                         f"(collectives.py:89-96)")
 
 
 class ShardedGradScaler:
@@ -485,6 +549,9 @@ class ShardedGradScaler:
         rt = self._pending.rt
         found = bool(rt.found_inf_world.item() > 0.0)
         if found:
+            # an aborted communicator also forces the verdict: surface it as
+            # DeadlockError (collectives.py:476-482), not as an inf step
+            rt.raise_if_aborted(sync=True)
             rt.undo_adam_t()
             self.scale_value *= self.backoff_factor
             self._tracker = 0

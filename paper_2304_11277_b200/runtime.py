@@ -45,7 +45,7 @@ import torch
 
 from . import _lib, kernels
 from .layout import UnitLayout
-from .plan import ShardingPlan
+from .plan import DeadlockError, ShardingPlan
 
 RAF = "RAF"
 NRAF = "NRAF"
@@ -325,6 +325,13 @@ class FSDPRuntime:
         self.inject_inf: set[int] = set()                     # steps to poison (test hook)
         self.found_inf = torch.zeros(1, dtype=torch.float32, device=self.device)
         self.found_inf_world = torch.zeros(1, dtype=torch.float32, device=self.device)
+        # abort handling (collectives.py:461-483): the optimizer's skip
+        # predicate folds in the communicator's error word on device, and the
+        # word is mirrored into pinned host memory for a sync-free check at
+        # the next step boundary
+        self.abort_flag = torch.zeros(1, dtype=torch.float32, device=self.device)
+        self.abort_flag_bwd = torch.zeros(1, dtype=torch.float32, device=self.device)
+        self.err_mirror = torch.zeros(1, dtype=torch.int32).pin_memory() if comm is not None else None
         self.opt_done: torch.cuda.Event | None = None
         self.opt_early: torch.cuda.Event | None = None   # first optimizer launch (units < opt_early_units)
         self.opt_early_units = 0
@@ -460,18 +467,65 @@ class FSDPRuntime:
         return total + (1 << 20)
 
     # ------------------------------------------------------- parameters ---
-    def load_unit_values(self, uid: int, tensors: Sequence[torch.Tensor]) -> None:
+    def load_unit_values(self, uid: int, tensors: Sequence[torch.Tensor], sync_src: int | None = None) -> None:
         """Materialise a unit: flatten its original tensors (declaration order)
         into an unsharded fp32 buffer, copy this rank's shard, refresh the bf16
-        copy (deferred_init.py:156-176 — flatten + shard)."""
+        copy (deferred_init.py:156-176 — flatten + shard).  sync_src=r
+        (sync_module_states) first replaces the unsharded buffer with rank r's."""
         u = self.units[uid]
         lay = u.layout
         srcs = [t.detach().to(self.device, torch.float32).contiguous() for t in tensors]
         flat = torch.empty(lay.psi, dtype=torch.float32, device=self.device)
         kernels.flatten(srcs, lay.offsets, flat)
+        if sync_src is not None and self.plan.world_size > 1:
+            from .dist_util import broadcast_
+            broadcast_(flat, src=sync_src)
         kernels.shard_copy(flat, u.master, self.plan.shard_index(self.rank))
         if u.low is not None:
             kernels.cast(u.master, u.low)
+
+    def gather_master(self, uid: int) -> torch.Tensor:
+        """The unit's fp32 unsharded flat parameter (engine.py:824-834,
+        gather_full_params), gathered within the shard group by this library's
+        all-gather: on the all-gather stream, through a free symmetric slot, in
+        pieces of the slot's capacity (fp32 chunks of every member land
+        side by side in the slot and are copied to their flat offsets)."""
+        u = self.units[uid]
+        lay = u.layout
+        F = self.plan.shard_factor
+        n = lay.shard_numel
+        flat = torch.empty(lay.psi, dtype=torch.float32, device=self.device)
+        if F == 1:
+            flat.copy_(u.master)
+            return flat
+        if n == 0:
+            return flat
+        if self.cfg.comm_backend != "ipc":
+            import torch.distributed as dist
+            dist.all_gather_into_tensor(flat, u.master.contiguous(), group=self.pgs.get("shard"))
+            return flat
+        cap = self.slots.slot_elems * self.compute_dtype.itemsize // (4 * F)
+        cap = cap // 8 * 8 if cap >= 8 else cap
+        if cap < 1:
+            raise EngineError("symmetric slot too small for an fp32 gather piece")
+        slot, free_ev = self.slots.acquire(-1)
+        off = self.slots.offsets[slot]
+        s = self.ag_stream
+        s.wait_stream(self.compute_stream)            # master is current on compute
+        if free_ev is not None:
+            s.wait_event(free_ev)
+        with torch.cuda.stream(s):
+            rows = flat.view(F, n)
+            for a in range(0, n, cap):
+                m = min(cap, n - a)
+                self.comm.all_gather(self.plan.sharded_desc, [u.master[a:a + m]], off, torch.float32, stream=s)
+                rows[:, a:a + m].copy_(self.comm.view(off, F * m, torch.float32).view(F, m))
+            ev = torch.cuda.Event()
+            ev.record(s)
+        self.slots.release(slot, ev)
+        self.compute_stream.wait_event(ev)
+        flat.record_stream(s)
+        return flat
 
     def full_unit_values(self, uid: int) -> list[torch.Tensor]:
         """This rank's view of the full unit (requires F == 1) — helper."""
@@ -728,20 +782,49 @@ class FSDPRuntime:
     def _step_in_backward(self) -> bool:
         return (self.cfg.optimizer_in_backward and self.final_micro and not self.defer_reduce)
 
+    def _abort_skip(self, stream: torch.cuda.Stream, flag: torch.Tensor | None = None):
+        """Skip predicate for an optimizer launch on `stream`: `flag` (the
+        scaler verdict, kept) or-ed with the communicator's error word; None
+        when there is no communicator."""
+        if self.comm is None or self.cfg.comm_backend != "ipc" or self.cfg.fake_comm:
+            return flag
+        out = flag if flag is not None else (self.abort_flag if stream is self.compute_stream
+                                             else self.abort_flag_bwd)
+        self.comm.fold_error(out, keep=flag is not None, mirror=self.err_mirror, stream=stream)
+        return out
+
+    def aborted(self) -> bool:
+        """Sync-free: the error word as of the last completed optimizer fold."""
+        return self.err_mirror is not None and int(self.err_mirror[0]) != 0
+
+    def raise_if_aborted(self, sync: bool = False) -> None:
+        """DeadlockError if a cross-GPU wait timed out on this rank or a peer
+        aborted (collectives.py:476-482).  sync=True reads the device word now."""
+        if self.comm is None:
+            return
+        if sync:
+            torch.cuda.synchronize(self.device)
+            self.comm.raise_device_error()
+        elif self.aborted():
+            raise DeadlockError("a cross-GPU collective wait timed out on device (this rank or a "
+                                "group member never entered the matching collective); no optimizer "
+                                "update was applied after the abort")
+
     def _step_unit(self, uid: int, stream: torch.cuda.Stream) -> None:
         """Optimizer on one unit's shard slice (same arithmetic as the arena
         launch, t = the step about to be taken)."""
         u = self.units[uid]
         cfg = self.cfg
         n = u.layout.shard_numel
+        skip = self._abort_skip(stream)
         with self.timed(cfg.optimizer + "_step", stream, n * (28 if cfg.optimizer == "adam" else 12)
                         + (2 * n if u.low is not None else 0)):
             if cfg.optimizer == "adam":
                 kernels.adam_step(u.master, u.grad, u.exp_avg, u.exp_avg_sq, lr=cfg.lr,
                                   betas=cfg.betas, eps=cfg.eps, t=self.adam_steps + 1,
-                                  p_lowp=u.low, stream=stream)
+                                  skip_flag=skip, p_lowp=u.low, stream=stream)
             else:
-                kernels.sgd_step(u.master, u.grad, lr=cfg.lr, p_lowp=u.low, stream=stream)
+                kernels.sgd_step(u.master, u.grad, lr=cfg.lr, skip_flag=skip, p_lowp=u.low, stream=stream)
         u.stepped = True
 
     def begin_micro(self, final: bool) -> None:
@@ -1041,7 +1124,10 @@ class FSDPRuntime:
     # --------------------------------------------------------- optimizer ---
     def optimizer_step(self, scale: float | None = None) -> None:
         """engine.py:563-594: unscale + world verdict + optimizer on the arena.
-        The verdict stays on device (skip flag) — no host sync."""
+        The verdict stays on device (skip flag) — no host sync.  An abort seen
+        by an earlier step's fold raises DeadlockError here; this step's own
+        launch is skipped on device if the error word is set by then."""
+        self.raise_if_aborted()
         for u in self.units:          # gathered copies would be stale after the update
             if u.unsharded is not None:
                 if u.pending:
@@ -1069,6 +1155,8 @@ class FSDPRuntime:
                 self.found_inf_world.copy_(self.found_inf)
             skip = self.found_inf_world
         self.step_count += 1
+        if not all(u.stepped for u in self.units) or skip is not None:
+            skip = self._abort_skip(self.compute_stream, skip)
         cfg = self.cfg
         if skip is None and self.units and all(u.stepped for u in self.units):
             # every shard was already stepped in backward, right behind its

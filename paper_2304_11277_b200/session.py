@@ -404,11 +404,13 @@ class Session:
         cvec = torch.tensor([counts.get(c, 0) for c in ("AG", "RS", "AR")], device=self.device,
                             dtype=torch.float32)
         torch.cuda.synchronize()
+        rt.raise_if_aborted(sync=True)          # DeadlockError (collectives.py:476-482)
         ms = torch.tensor([t0.elapsed_time(t1)], device=self.device)
         if W > 1:
-            dist.all_reduce(losses)
-            dist.all_reduce(cvec)
-            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+            from .dist_util import all_reduce_
+            all_reduce_(losses)
+            all_reduce_(cvec)
+            all_reduce_(ms, op=dist.ReduceOp.MAX)
         self._makespan += ms.item()
         rl = losses.tolist()
         counts = {c: int(v) for c, v in zip(("AG", "RS", "AR"), cvec.tolist()) if v > 0}
@@ -428,11 +430,10 @@ class Session:
 
     # -- inspection ---------------------------------------------------------
     def _all_gather_shard(self, t: torch.Tensor, group_ranks) -> torch.Tensor:
-        import torch.distributed as dist
+        from .dist_util import all_gather
         if len(group_ranks) == 1:
             return t.clone()
-        out = [torch.empty_like(t) for _ in range(dist.get_world_size())]
-        dist.all_gather(out, t.contiguous())
+        out = all_gather(t)
         return torch.cat([out[r] for r in group_ranks])
 
     def gather_full_params(self) -> dict[str, np.ndarray]:
@@ -451,14 +452,13 @@ class Session:
 
     def replica_divergence(self) -> float:
         """engine.py:836-846: max |shard difference| across replicas."""
-        import torch.distributed as dist
+        from .dist_util import all_gather
         if self.plan.world_size == 1:
             return 0.0
         worst = 0.0
         for u in range(self.num_units):
             t = self.rt.units[u].master
-            allv = [torch.empty_like(t) for _ in range(self.plan.world_size)]
-            dist.all_gather(allv, t.contiguous())
+            allv = all_gather(t)
             for grp in self.plan.replicated_groups:
                 for r in grp[1:]:
                     if t.numel():

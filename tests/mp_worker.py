@@ -1,6 +1,13 @@
 """Multi-GPU parity worker (launched by tests/test_multigpu.py via torchrun,
 one process per GPU, NCCL only for bootstrap/ground truth).
 
+Shared mode: when the box has fewer GPUs than ranks (the 1-GPU CI box), the
+ranks share devices round-robin and bootstrap over gloo.  The CUDA-IPC
+communicator, the copy-engine collectives, the symmetric slots, limiter,
+prefetch and every strategy run unchanged between processes on one device
+(the contexts time-slice the GPU); only the NVLS and NCCL-backend scenarios
+are skipped (multicast needs distinct devices; NCCL refuses duplicates).
+
 1. raw IPC collectives (AG with fused cast, RS with fp32 accumulation and
    /W, AR, hybrid RS->AR, scalar AR) vs the oracle — bit-exact;
 2. a full FSDP training step of the tiny GPT for every strategy available at
@@ -29,8 +36,13 @@ from oracle import shardsim_port as sp  # noqa: E402
 from oracle.bf16 import round_to_bf16  # noqa: E402
 
 
+SHARED = False       # ranks share a GPU (set in main)
+
+
 def gather_np(x: np.ndarray) -> list[np.ndarray]:
-    t = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    t = torch.from_numpy(np.ascontiguousarray(x))
+    if not SHARED:
+        t = t.cuda()
     out = [torch.empty_like(t) for _ in range(dist.get_world_size())]
     dist.all_gather(out, t)
     return [o.cpu().numpy() for o in out]
@@ -80,8 +92,7 @@ def raw_collectives(rank, world, results):
         exp = sp.reduce_unit(grads, sp.Plan(world, 1), reduce_dtype=sp.BF16, full_dtype=np.float32,
                              acc_dtype=np.float32, mean=True, accum=acc_full)
         check(out_ce.cpu().numpy().tobytes() == exp[rank].tobytes(), f"AR-CE bf16 accumulate n={n}")
-        if world == 4:
-            f = 2
+        for f in [f for f in (2, 4) if f < world and world % f == 0]:
             part = torch.empty(n * world // f, device="cuda")
             comm.reduce_scatter((f, 1), [torch.from_numpy(grads[rank]).cuda().to(torch.bfloat16)], a, [part])
             out = torch.from_numpy(acc0[rank]).cuda().repeat(world // f)[: n * world // f].contiguous()
@@ -267,6 +278,9 @@ def nvls_collectives(rank, world, results):
     checked against NCCL's all-gather of the same bf16 shards."""
     from paper_2304_11277_b200 import _lib
     from paper_2304_11277_b200.comm import DeviceComm
+    if SHARED:
+        results["nvls"] = "skipped: ranks share one GPU (multicast needs distinct devices)"
+        return
     if not _lib.lib.fsdp_nvls_supported(torch.cuda.current_device()):
         results["nvls"] = "unsupported on this device: " + _lib.last_error()
         return
@@ -407,6 +421,56 @@ def deadlock_detection(rank, world, results):
     dist.barrier()
     comm.close()
     results["deadlock_detection"] = "ok (split and LL)"
+
+
+def abort_in_step(rank, world, results):
+    """A member stalls past the timeout INSIDE a wrapped training step (its
+    compute stream sleeps before the step's first all-gather): the waiting
+    members' flag waits time out and abort the communicator on every rank;
+    the data kernels stop touching peer memory, the optimizer launch of the
+    step is skipped on device (the error word is folded into its predicate),
+    and every rank raises DeadlockError (collectives.py:461-483) -- with its
+    shards and optimizer state bit-identical to before the step."""
+    from paper_2304_11277_b200.fsdp import FullyShardedDataParallel, MixedPrecision, ModuleWrapPolicy
+    from paper_2304_11277_b200.plan import DeadlockError
+    from paper_2304_11277_b200.workloads import CONFIGS, GPT, Block, init_gpt_, synthetic_batch
+    cfg = CONFIGS["tiny"]
+    fsdp = FullyShardedDataParallel(init_gpt_(GPT(cfg), seed=0), auto_wrap_policy=ModuleWrapPolicy({Block}),
+                                    mixed_precision=MixedPrecision(param_dtype=torch.bfloat16), lr=1e-3)
+    opt = fsdp.optimizer()
+    x, y = synthetic_batch(cfg, 2, seed=300 + rank, device="cuda")
+    fsdp(x, y).backward()
+    opt.step()
+    fsdp.check_errors()                               # healthy step: no error
+    torch.cuda.synchronize()
+    rt = fsdp.rt
+    before = [t.clone() for t in (rt.master, rt.exp_avg, rt.exp_avg_sq, rt.low)]
+    fsdp.comm.set_timeout_ms(1500)
+    dist.barrier()
+    if rank == world - 1:
+        torch.cuda._sleep(6_000_000_000)              # ~3 s on the compute stream: misses the timeout
+    raised = False
+    try:
+        fsdp(x, y).backward()
+        opt.step()
+        fsdp.check_errors()
+    except DeadlockError:
+        raised = True
+    torch.cuda.synchronize()
+    check(raised, f"rank {rank}: DeadlockError not raised after a peer stalled past the timeout")
+    after = [rt.master, rt.exp_avg, rt.exp_avg_sq, rt.low]
+    for name, a, b in zip(("master", "exp_avg", "exp_avg_sq", "low"), before, after):
+        check(torch.equal(a, b), f"rank {rank}: {name} changed by an aborted step")
+    # the next step refuses to run on an aborted communicator
+    again = False
+    try:
+        opt.step()
+    except DeadlockError:
+        again = True
+    check(again, "optimizer step on an aborted communicator did not raise")
+    dist.barrier()
+    fsdp.close()
+    results["abort_in_step"] = "DeadlockError on every rank; shards and Adam state unchanged"
 
 
 def _sess(w, f, spec=None, seed=0, **kw):
@@ -556,12 +620,12 @@ class _Done(Exception):
 
 
 def main():
-    rank = int(os.environ["RANK"])
+    global SHARED
+    from paper_2304_11277_b200.dist_util import init_from_env, shared_gpu
     world = int(os.environ["WORLD_SIZE"])
-    local = int(os.environ["LOCAL_RANK"])
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    results = {"world": world}
+    SHARED = shared_gpu(world)
+    rank, world, _ = init_from_env()
+    results = {"world": world, "shared_gpu": SHARED, "backend": dist.get_backend()}
     ok = True
     only = os.environ.get("MP_ONLY")       # debugging: a comma list of scenario functions
     try:
@@ -569,38 +633,38 @@ def main():
             for name in only.split(","):
                 globals()[name](rank, world, results)
             raise _Done()
-        raw_collectives(rank, world, results)
-        full_size_properties(rank, world, results)
-        ll_collectives(rank, world, results)
-        nvls_collectives(rank, world, results)
-        ce_schedules(rank, world, results)
-        session_parity(rank, world, results)
-        cases =[("FULL_SHARD", None), ("SHARD_GRAD_OP", None), ("NO_SHARD", None)]
-        if world == 4:
-            cases.append(("HYBRID_SHARD", 2))
-        for strat, hyb in cases:
-            fsdp_step_parity(rank, world, strat, hyb, results)
-        fsdp_step_parity(rank, world, "FULL_SHARD", None, results, opt_in_bwd=True)
-        fsdp_step_parity(rank, world, "FULL_SHARD", None, results, ll=True)
-        fsdp_step_parity(rank, world, "SHARD_GRAD_OP", None, results, ll=True)
-        if world == 4:
-            fsdp_step_parity(rank, world, "HYBRID_SHARD", 2, results, ll=True)
-        fsdp_step_parity(rank, world, "FULL_SHARD", None, results, engine="sm")
-        fsdp_step_parity(rank, world, "FULL_SHARD", None, results, engine="nvls")
-        if world == 4:
-            fsdp_step_parity(rank, world, "HYBRID_SHARD", 2, results, engine="nvls")
-        if world == 4:
-            fsdp_step_parity(rank, world, "HYBRID_SHARD", 2, results, engine="sm")
-        if world == 4:
-            fsdp_step_parity(rank, world, "HYBRID_SHARD", 2, results, opt_in_bwd=True)
-        fsdp_step_parity(rank, world, "FULL_SHARD", None, results, backend="nccl")
-        deadlock_detection(rank, world, results)
+        hybrids = [f for f in (2, 4) if f < world and world % f == 0]
+        steps = [("FULL_SHARD", None, {}), ("SHARD_GRAD_OP", None, {}), ("NO_SHARD", None, {})]
+        steps += [("HYBRID_SHARD", f, {}) for f in hybrids]
+        steps += [("FULL_SHARD", None, {"opt_in_bwd": True}), ("FULL_SHARD", None, {"ll": True}),
+                  ("SHARD_GRAD_OP", None, {"ll": True})]
+        steps += [("HYBRID_SHARD", f, {"ll": True}) for f in hybrids]
+        steps += [("FULL_SHARD", None, {"engine": "sm"})]
+        if not SHARED:
+            steps += [("FULL_SHARD", None, {"engine": "nvls"})]
+            steps += [("HYBRID_SHARD", f, {"engine": "nvls"}) for f in hybrids]
+        steps += [("HYBRID_SHARD", f, {"engine": "sm"}) for f in hybrids]
+        steps += [("HYBRID_SHARD", f, {"opt_in_bwd": True}) for f in hybrids]
+        if not SHARED:
+            steps += [("FULL_SHARD", None, {"backend": "nccl"})]
+        scen = [("raw_collectives", raw_collectives), ("full_size_properties", full_size_properties),
+                ("ll_collectives", ll_collectives), ("nvls_collectives", nvls_collectives),
+                ("ce_schedules", ce_schedules), ("session_parity", session_parity)]
+        scen += [("fsdp_step", lambda r, w, res, s=s, h=h, kw=kw: fsdp_step_parity(r, w, s, h, res, **kw))
+                 for s, h, kw in steps]
+        scen += [("deadlock_detection", deadlock_detection), ("abort_in_step", abort_in_step)]
+        # MP_SCENARIOS: comma list of scenario names to run (default: all)
+        pick = os.environ.get("MP_SCENARIOS")
+        pick = set(pick.split(",")) if pick else None
+        for name, fn in scen:
+            if pick is None or name in pick:
+                fn(rank, world, results)
     except _Done:
         pass
     except Exception:
         ok = False
         traceback.print_exc()
-    flag = torch.tensor([0.0 if ok else 1.0], device="cuda")
+    flag = torch.tensor([0.0 if ok else 1.0], device="cpu" if SHARED else "cuda")
     dist.all_reduce(flag)
     if rank == 0:
         results["ok"] = flag.item() == 0.0

@@ -150,8 +150,17 @@ int fsdp_comm_set_timeout_ms(fsdp_comm_t* c, int64_t ms);
  * Replaces: the DeadlockError raise and the verdict agreement of
  * collectives.py:461-483 / engine.py:410-411. */
 int fsdp_comm_fold_error(fsdp_comm_t* c, float* flag, int keep, int* host_mirror, void* stream);
+/* Diagnostics of the first local timeout (synchronous read): out[0..5] =
+ * {set, polled word index in the pool, last value seen, epoch, channel,
+ * group size << 8 | stride}.  A word index below the flag area's size decodes
+ * as ((channel * 3 + phase) * FSDP_MAX_RANKS + src) * FSDP_MAX_CTAS + cta. */
+int fsdp_comm_timeout_info(fsdp_comm_t* c, uint32_t* out);
 /* Zero the local error word(s) (synchronous; tests and re-use after a handled abort). */
 int fsdp_comm_clear_error(fsdp_comm_t* c);
+/* Fault injection for verify-sensitivity (collectives.py:176, :296; cli.py:568-574):
+ * misorder_reduce_scatter != 0 makes every reduce-scatter hand member k the
+ * reduced chunk (k + 1) % size instead of chunk k (all engines).  Test use only. */
+int fsdp_comm_set_fault(fsdp_comm_t* c, int misorder_reduce_scatter);
 /* split != 0 (default): collectives run as [1-CTA enter barrier] [data kernel
  * that only signals] [1-CTA exit barrier], so a late peer never parks the
  * data kernel's CTAs on SMs.  timing != 0: CUDA events around every data

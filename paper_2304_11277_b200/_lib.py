@@ -68,6 +68,8 @@ _SIGS = {
     "fsdp_comm_set_timeout_ms": (_i32, [_vp, _i64]),
     "fsdp_comm_fold_error": (_i32, [_vp, _vp, _i32, _vp, _vp]),
     "fsdp_comm_clear_error": (_i32, [_vp]),
+    "fsdp_comm_timeout_info": (_i32, [_vp, C.POINTER(C.c_uint32)]),
+    "fsdp_comm_set_fault": (_i32, [_vp, _i32]),
     "fsdp_comm_set_mode": (_i32, [_vp, _i32, _i32]),
     "fsdp_comm_set_barriers": (_i32, [_vp, _i32]),
     "fsdp_comm_set_ctas": (_i32, [_vp, _i32, _i32]),

@@ -320,14 +320,47 @@ class DeviceComm:
                                        int(keep), mirror.data_ptr() if mirror is not None else None,
                                        stream_ptr(stream)), "comm_fold_error")
 
+    def set_fault(self, misorder_reduce_scatter: bool) -> None:
+        """Verify-sensitivity fault hook (collectives.py:296): member k of every
+        reduce-scatter receives chunk (k + 1) % size."""
+        check(lib.fsdp_comm_set_fault(self._h, int(misorder_reduce_scatter)), "comm_set_fault")
+
     def clear_error(self) -> None:
         check(lib.fsdp_comm_clear_error(self._h), "comm_clear_error")
+
+    _CH_NAMES = {0: "AG", 1: "RS", 2: "AR", 3: "SCALAR"}
+
+    def timeout_info(self) -> dict | None:
+        """Where this rank's first local timeout happened (None if none here:
+        the abort came from a peer)."""
+        buf = (C.c_uint32 * 6)()
+        check(lib.fsdp_comm_timeout_info(self._h, buf), "comm_timeout_info")
+        v = list(buf)
+        if not v[0]:
+            return None
+        info = {"epoch": v[3], "channel": self._CH_NAMES.get(v[4], v[4]), "group": (v[5] >> 8, v[5] & 255),
+                "seen": v[2]}
+        flag_words = 4 * 3 * _lib.MAX_RANKS * _lib.MAX_CTAS
+        w = v[1]
+        if w < flag_words:
+            cta = w % _lib.MAX_CTAS
+            src = (w // _lib.MAX_CTAS) % _lib.MAX_RANKS
+            ph = (w // (_lib.MAX_CTAS * _lib.MAX_RANKS)) % 3
+            info.update(waiting_for_rank=src, phase=("enter", "data/exit", "phase2")[ph] if cta != _lib.MAX_CTAS - 1
+                        else "enter", slot=cta)
+        else:
+            info.update(ll_line_byte_offset=w * 4)
+        return info
 
     def raise_device_error(self) -> None:
         err = self.device_error()
         if err == _lib.E_TIMEOUT:
+            info = self.timeout_info()
+            where = (f" (here: channel {info['channel']} epoch {info['epoch']} group {info['group']}, "
+                     f"{ {k: v for k, v in info.items() if k not in ('channel', 'epoch', 'group')} })"
+                     if info else " (aborted by a peer)")
             raise DeadlockError("a cross-GPU collective wait timed out on device: some group member "
-                                "never entered the matching collective")
+                                "never entered the matching collective" + where)
         if err:
             raise RuntimeError(f"device error word = {err}")
 

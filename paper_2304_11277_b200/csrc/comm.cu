@@ -36,6 +36,7 @@ constexpr int kPhases = 3;
 constexpr int64_t kFlagBytes =
     (int64_t)FSDP_NUM_CH * kPhases * FSDP_MAX_RANKS * FSDP_MAX_CTAS * sizeof(uint32_t);
 constexpr int64_t kErrOff = kFlagBytes;                 // uint32 error word
+constexpr int64_t kDiagOff = kFlagBytes + 64;           // uint32[6]: first local timeout (diagnostics)
 constexpr int64_t kScalarOff = kFlagBytes + 256;        // float[FSDP_MAX_RANKS]
 constexpr int64_t kReserved = 65536;
 static_assert(kScalarOff + 4 * FSDP_MAX_RANKS <= kReserved, "reserved region too small");
@@ -60,7 +61,14 @@ struct CollParams {
   int split;        // 1: waits live in 1-CTA enter/exit kernels, data kernels only signal
   int data_ctas;    // exit kernel: grid of the data kernel it waits for
   char* mc_base;    // NVLS multicast VA of the pool (shard group), or null
+  int rot;          // reduce-scatter fault hook: member k receives chunk (k + rot) % size
 };
+
+// chunk of the payload that member position `pos` reduces (rot = 0 except
+// under the misorder fault, collectives.py:296)
+__device__ __forceinline__ int rs_chunk(const CollParams& p, int pos, int size) {
+  return (pos + p.rot) % size;
+}
 
 // flag slot (CTA index) reserved for the whole-collective enter barrier
 constexpr int kEnterSlot = FSDP_MAX_CTAS - 1;
@@ -118,7 +126,18 @@ __device__ __forceinline__ Group make_group(const CollParams& p) {
 // failure at its next collective or optimizer step (its skip predicate reads
 // the word, fsdp_comm_fold_error) instead of computing on with a slot a
 // timed-out peer may have written.  collectives.py:461-483 (DeadlockError).
-__device__ __noinline__ void comm_abort(const CollParams& p, const Group& g) {
+// `what` = the polled word (flag or LL line), `seen` = its last value: the
+// first local timeout records {1, word index in the pool, seen, epoch,
+// channel, group (size << 8 | stride)} at kDiagOff for the host's message.
+__device__ __noinline__ void comm_abort(const CollParams& p, const Group& g, const void* what, uint32_t seen) {
+  uint32_t* diag = reinterpret_cast<uint32_t*>(p.bases[g.rank] + kDiagOff);
+  if (atomicCAS(diag, 0u, 1u) == 0u) {
+    diag[1] = (uint32_t)(((const char*)what - p.bases[g.rank]) / 4);
+    diag[2] = seen;
+    diag[3] = p.epoch;
+    diag[4] = (uint32_t)p.channel;
+    diag[5] = (uint32_t)((g.size << 8) | g.stride);
+  }
   atomicExch(reinterpret_cast<uint32_t*>(p.bases[g.rank] + kErrOff), (uint32_t)FSDP_E_TIMEOUT);
   for (int r = 0; r < FSDP_MAX_RANKS; ++r)
     if (p.bases[r] != nullptr && r != g.rank)
@@ -159,7 +178,7 @@ __device__ __noinline__ void cta_barrier(const CollParams& p, const Group& g, in
       if ((++spins & 1023u) == 0) {
         if (*(volatile uint32_t*)err != 0) break;           // already failed: bail out
         if (globaltimer() - t0 > (uint64_t)p.timeout_ns) {
-          comm_abort(p, g);
+          comm_abort(p, g, mine, ld_acquire_sys(mine));
           break;
         }
       }
@@ -216,7 +235,7 @@ __device__ __forceinline__ void wait_flag(const CollParams& p, const Group& g, c
     if ((++spins & 1023u) == 0) {
       if (*(volatile uint32_t*)err != 0) break;
       if (globaltimer() - t0 > (uint64_t)p.timeout_ns) {
-        comm_abort(p, g);
+        comm_abort(p, g, f, ld_acquire_sys(f));
         break;
       }
     }
@@ -495,7 +514,7 @@ reduce_scatter_kernel(const __grid_constant__ CollParams p) {
     for (int jj = 1; jj < g.size; ++jj) {
       const int j = (g.pos + jj) % g.size;
       Tin* dst = (Tin*)(p.bases[g.member(j)] + p.off_a + (int64_t)g.pos * slot_bytes);
-      const Tin* s = flat + (int64_t)j * n;
+      const Tin* s = flat + (int64_t)rs_chunk(p, j, g.size) * n;
       if (vec) {
         Packed8<Tin> r[kU];
 #pragma unroll
@@ -518,7 +537,7 @@ reduce_scatter_kernel(const __grid_constant__ CollParams p) {
   if (cta_failed(p, g)) return;  // staging incomplete: leave out untouched
   // phase 2: ascending-rank fp32 sum of the group's chunks, post-divide, accumulate
   const Tin* stage = (const Tin*)(p.bases[g.rank] + p.off_a);
-  const Tin* mine = flat + (int64_t)g.pos * n;
+  const Tin* mine = flat + (int64_t)rs_chunk(p, g.pos, g.size) * n;
   const bool pre = p.prediv != 1.0f, post = p.postdiv != 1.0f;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     if (vec) {
@@ -587,7 +606,7 @@ reduce_scatter_pull_kernel(const __grid_constant__ CollParams p) {
   float* __restrict__ out = p.out[e];
   const int64_t n = p.n;
   // off_b > 0: the members' chunks are off_b elements apart (a sub-range of each chunk)
-  const int64_t chunk_off = p.off_a + (int64_t)g.pos * (p.off_b > 0 ? p.off_b : n) * (int64_t)sizeof(Tin);
+  const int64_t chunk_off = p.off_a + (int64_t)rs_chunk(p, g.pos, g.size) * (p.off_b > 0 ? p.off_b : n) * (int64_t)sizeof(Tin);
   const Tin* src[MAXW];
 #pragma unroll
   for (int j = 0; j < MAXW; ++j)
@@ -672,7 +691,7 @@ reduce_scatter_tma_kernel(const __grid_constant__ CollParams p) {
   // elements per member tile: a multiple of 8 (16-byte bulk-copy granule)
   const int64_t T = (STAGE_BYTES / (W * (int)sizeof(Tin))) / kVec * kVec;
   // off_b > 0: the members' chunks are off_b elements apart (a sub-range of each chunk)
-  const int64_t chunk_off = p.off_a + (int64_t)g.pos * (p.off_b > 0 ? p.off_b : n) * (int64_t)sizeof(Tin);
+  const int64_t chunk_off = p.off_a + (int64_t)rs_chunk(p, g.pos, g.size) * (p.off_b > 0 ? p.off_b : n) * (int64_t)sizeof(Tin);
   const int64_t ntiles = (n + T - 1) / T;
   const int64_t my_tiles = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
   if (threadIdx.x == 0) {
@@ -916,7 +935,7 @@ __device__ __noinline__ uint4 ll_wait(const CollParams& p, const Group& g, const
     if ((++spins & 255u) == 0) {
       if (*(volatile uint32_t*)err != 0) break;
       if (globaltimer() - t0 > (uint64_t)p.timeout_ns) {
-        comm_abort(p, g);
+        comm_abort(p, g, line, v.y);
         break;
       }
     }
@@ -1046,12 +1065,12 @@ reduce_scatter_ll_kernel(const __grid_constant__ CollParams p) {
   for (int64_t L = tid; L < nl; L += nt) {
     for (int jj = 1; jj < g.size; ++jj) {
       const int j = (g.pos + jj) % g.size;
-      const uint2 d = ll_load_line<Tin, Tin>(flat + (int64_t)j * n, L, n);
+      const uint2 d = ll_load_line<Tin, Tin>(flat + (int64_t)rs_chunk(p, j, g.size) * n, L, n);
       st_ll(ll_region(p, p.bases[g.member(j)], g.pos, nl) + L * 16, d.x, d.y, p.epoch);
     }
   }
   const bool pre = p.prediv != 1.0f, post = p.postdiv != 1.0f;
-  const Tin* mine = flat + (int64_t)g.pos * n;
+  const Tin* mine = flat + (int64_t)rs_chunk(p, g.pos, g.size) * n;
   const char* reg[MAXW];
 #pragma unroll
   for (int j = 0; j < MAXW; ++j) reg[j] = j < g.size ? ll_region(p, p.bases[g.rank], j, nl) : nullptr;
@@ -1148,6 +1167,7 @@ struct fsdp_comm {
   bool ce_rs_geom = true;                     // FSDP_CE_RS_GEOM: halving pieces (else uniform)
   int ce_reduce_cap = 0;                      // FSDP_CE_REDUCE_CAP: grid cap of every CE reduction (0: 4 CTAs/SM)
   bool ce_rs_noreduce = false;
+  int misorder_rs = 0;                        // fault hook (fsdp_comm_set_fault)
   int rs_tma_ring = -1;
   float ce_rs_sm_frac = 0.f;                  // FSDP_CE_RS_SM_FRAC: tail fraction of a pipelined chunk pulled by SM TMA                       // FSDP_RS_TMA_RING: TMA-pull ring geometry (-1: not read yet)                // FSDP_CE_RS_NOREDUCE=1: DIAGNOSTIC ONLY, skip the reductions (wrong results)
   std::vector<cudaEvent_t> ce_events;
@@ -1438,11 +1458,30 @@ extern "C" int fsdp_comm_fold_error(fsdp_comm_t* c, float* flag, int keep, int* 
   return 0;
 }
 
+// First local timeout: out[0..5] = {set, word index, seen, epoch, channel,
+// size << 8 | stride}; word index < flag words decodes as
+// ((channel * 3 + phase) * MAX_RANKS + src) * MAX_CTAS + cta.
+extern "C" int fsdp_comm_timeout_info(fsdp_comm_t* c, uint32_t* out) {
+  if (!c || !out) return fail(FSDP_E_INVALID, "null argument");
+  const int n = c->emulated ? c->world : 1;
+  for (int i = 0; i < 6; ++i) out[i] = 0;
+  for (int i = 0; i < n && !out[0]; ++i)
+    FSDP_CUDA(cudaMemcpy(out, (c->emulated ? c->bases[i] : c->pool) + kDiagOff, 6 * sizeof(uint32_t),
+                         cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+extern "C" int fsdp_comm_set_fault(fsdp_comm_t* c, int misorder_reduce_scatter) {
+  if (!c) return fail(FSDP_E_INVALID, "null communicator");
+  c->misorder_rs = misorder_reduce_scatter ? 1 : 0;
+  return 0;
+}
+
 extern "C" int fsdp_comm_clear_error(fsdp_comm_t* c) {
   if (!c) return fail(FSDP_E_INVALID, "null communicator");
   const int n = c->emulated ? c->world : 1;
   for (int i = 0; i < n; ++i)
-    FSDP_CUDA(cudaMemset((c->emulated ? c->bases[i] : c->pool) + kErrOff, 0, sizeof(uint32_t)));
+    FSDP_CUDA(cudaMemset((c->emulated ? c->bases[i] : c->pool) + kErrOff, 0, kScalarOff - kErrOff));
   FSDP_CUDA(cudaDeviceSynchronize());
   return 0;
 }
@@ -1523,6 +1562,7 @@ extern "C" int fsdp_reduce_scatter(fsdp_comm_t* c, int channel, int gsize, int g
   if (int rc = check_range(c, stage_off, n * gsize * is, "fsdp_reduce_scatter")) return rc;
   CollParams p;
   fill_common(c, p, channel, gsize, gstride, n);
+  p.rot = c->misorder_rs && gsize > 1 ? 1 : 0;
   for (int e = 0; e < nranks_args(c); ++e) { p.in[e] = flats[e]; p.out[e] = outs[e]; }
   p.off_a = stage_off;
   p.prediv = prediv; p.postdiv = postdiv; p.accumulate = accumulate ? 1 : 0;
@@ -1545,6 +1585,7 @@ extern "C" int fsdp_reduce_scatter_pull(fsdp_comm_t* c, int channel, int gsize, 
   if (int rc = check_range(c, src_off, n * gsize * is, "fsdp_reduce_scatter_pull")) return rc;
   CollParams p;
   fill_common(c, p, channel, gsize, gstride, n);
+  p.rot = c->misorder_rs && gsize > 1 ? 1 : 0;
   for (int e = 0; e < nranks_args(c); ++e) p.out[e] = outs[e];
   p.off_a = src_off;
   p.prediv = prediv; p.postdiv = postdiv; p.accumulate = accumulate ? 1 : 0;
@@ -1585,6 +1626,7 @@ extern "C" int fsdp_reduce_scatter_tma(fsdp_comm_t* c, int channel, int gsize, i
                                     postdiv, accumulate, stream);
   CollParams p;
   fill_common(c, p, channel, gsize, gstride, n);
+  p.rot = c->misorder_rs && gsize > 1 ? 1 : 0;
   for (int e = 0; e < nranks_args(c); ++e) p.out[e] = outs[e];
   p.off_a = src_off;
   p.prediv = prediv; p.postdiv = postdiv; p.accumulate = accumulate ? 1 : 0;
@@ -1766,14 +1808,18 @@ extern "C" int fsdp_reduce_scatter_ce(fsdp_comm_t* c, int channel, int gsize, in
   if (int rc = ce_prepare(c)) return rc;
   CollParams p;
   fill_common(c, p, channel, gsize, gstride, n);
+  p.rot = c->misorder_rs && gsize > 1 ? 1 : 0;
   p.data_ctas = 1;
   cudaStream_t s = (cudaStream_t)stream;
   if (int rc = launch(c, coll_enter_kernel, p, 1, 32, s)) return rc;
   const int start = gstride == 1 ? (c->rank / gsize) * gsize : c->rank % gstride;
   const int pos = gstride == 1 ? c->rank - start : c->rank / gstride;
+  const int rot = p.rot;                           // misorder fault: chunk (k + rot) % gsize
+  auto chunk = [&](int k) { return (k + rot) % gsize; };
+  const int cpos = chunk(pos);
   char* mine = c->bases[c->rank];
   CeReduceArgs ra;
-  ra.own = mine + src_off + (int64_t)pos * n * es;
+  ra.own = mine + src_off + (int64_t)cpos * n * es;
   ra.stage = mine + stage_off;
   ra.stride = n;
   ra.out = out;
@@ -1872,7 +1918,7 @@ extern "C" int fsdp_reduce_scatter_ce(fsdp_comm_t* c, int channel, int gsize, in
       for (int jj = 0; jj + 1 < gsize; ++jj) {
         const int j = (pos + 1 + jj) % gsize;
         FSDP_CUDA(cudaMemcpyAsync(c->bases[start + j * gstride] + stage_off + ((int64_t)pos * n + e0) * es,
-                                  mine + src_off + ((int64_t)j * n + e0) * es,
+                                  mine + src_off + ((int64_t)chunk(j) * n + e0) * es,
                                   (size_t)len * es, cudaMemcpyDeviceToDevice, cs));
       }
       cudaEvent_t landed = ce_event(c);
@@ -1905,7 +1951,7 @@ extern "C" int fsdp_reduce_scatter_ce(fsdp_comm_t* c, int channel, int gsize, in
       for (int jj = 0; jj + 1 < gsize; ++jj) {
         const int j = (pos + 1 + jj) % gsize;
         FSDP_CUDA(cudaMemcpyAsync(mine + stage_off + ((int64_t)j * n + e0) * es,
-                                  c->bases[start + j * gstride] + src_off + ((int64_t)pos * n + e0) * es,
+                                  c->bases[start + j * gstride] + src_off + ((int64_t)cpos * n + e0) * es,
                                   (size_t)len * es, cudaMemcpyDeviceToDevice, cs));
       }
       cudaEvent_t landed = ce_event(c);
@@ -1926,10 +1972,10 @@ extern "C" int fsdp_reduce_scatter_ce(fsdp_comm_t* c, int channel, int gsize, in
     if (j == pos) continue;   // own chunk is reduced in place
     if (push) {               // my chunk j -> member j's staging, slot pos (NVLink writes)
       dst[j] = c->bases[start + j * gstride] + stage_off + (int64_t)pos * n * es;
-      src[j] = mine + src_off + (int64_t)j * n * es;
+      src[j] = mine + src_off + (int64_t)chunk(j) * n * es;
     } else {                  // member j's chunk pos -> my staging, slot j (NVLink reads)
       dst[j] = mine + stage_off + (int64_t)j * n * es;
-      src[j] = c->bases[start + j * gstride] + src_off + (int64_t)pos * n * es;
+      src[j] = c->bases[start + j * gstride] + src_off + (int64_t)cpos * n * es;
     }
   }
   if (int rc = ce_fork_join(c, 1, s, gsize, pos, dst, src, (size_t)n * es)) return rc;
@@ -2115,6 +2161,7 @@ extern "C" int fsdp_reduce_scatter_ll(fsdp_comm_t* c, int channel, int gsize, in
   if (int rc = check_range(c, ll_off, fsdp_ll_bytes(gsize, n, src_dtype), "fsdp_reduce_scatter_ll")) return rc;
   CollParams p;
   fill_common(c, p, channel, gsize, gstride, n);
+  p.rot = c->misorder_rs && gsize > 1 ? 1 : 0;
   for (int e = 0; e < nranks_args(c); ++e) { p.in[e] = flats[e]; p.out[e] = outs[e]; }
   p.off_b = ll_off;
   p.prediv = prediv; p.postdiv = postdiv; p.accumulate = accumulate ? 1 : 0;

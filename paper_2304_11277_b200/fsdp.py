@@ -22,7 +22,8 @@ Mapping to the reference engine (`engine.py:165-207`, EngineConfig):
                                     (the reference's point, engine.py:544-545)
   backward_prefetch=None            backward_prefetch=False
   forward_prefetch                  forward_prefetch
-  limit_all_gathers                 rate_limit = 2 (else None)
+  limit_all_gathers                 rate_limit = 2 (else None); rate_limit=k overrides
+  keep_outermost_unsharded=         keep_outermost_unsharded (default True, as torch)
   MixedPrecision(param_dtype=bf16)  PrecisionPolicy(mixed=True)
   MixedPrecision(reduce_dtype=fp32) PrecisionPolicy(reduce_in_low=False)
   no_sync()                         accumulation = no_comm (engine.py:547-556)
@@ -140,7 +141,8 @@ class FullyShardedDataParallel(nn.Module):
                  comm_backend: str = "ipc", num_slots: int | None = None, ag_ctas: int = 32, rs_ctas: int = 64,
                  optimizer: str = "adam", lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-8,
                  optimizer_in_backward: bool = False, ag_engine: str = "ce", rs_engine: str = "ce",
-                 tail_engine: str = "sm", ll_max_bytes: int = 6 << 20, opt_split_first: int = 2):
+                 tail_engine: str = "sm", ll_max_bytes: int = 6 << 20, opt_split_first: int = 2,
+                 rate_limit: int | None | str = "auto", keep_outermost_unsharded: bool = True):
         super().__init__()
         if cpu_offload is not None and cpu_offload.offload_params:
             raise NotImplementedError("CPU offload is out of scope for the B200 runtime")
@@ -187,8 +189,8 @@ class FullyShardedDataParallel(nn.Module):
               BackwardPrefetch.BACKWARD_POST: PREFETCH_POST}[backward_prefetch]
         cfg = RuntimeConfig(mixed=mixed, reduce_in_low=reduce_low, reshard_after_forward=raf,
                             backward_prefetch=bp, forward_prefetch=forward_prefetch,
-                            rate_limit=2 if limit_all_gathers else None,
-                            keep_outermost_unsharded=True, accumulation=ACCUM_OFF,
+                            rate_limit=(2 if limit_all_gathers else None) if rate_limit == "auto" else rate_limit,
+                            keep_outermost_unsharded=keep_outermost_unsharded, accumulation=ACCUM_OFF,
                             comm_backend=comm_backend, num_slots=num_slots, ag_ctas=ag_ctas, rs_ctas=rs_ctas,
                             optimizer=optimizer, lr=lr, betas=tuple(betas), eps=eps,
                             optimizer_in_backward=optimizer_in_backward,
@@ -323,6 +325,7 @@ class FullyShardedDataParallel(nn.Module):
         rt = self.rt
         rt.post_order.append(uid)
         rt.close_window(uid)
+        rt.sample_activations()
         if torch.is_grad_enabled():
             output = _map_tensors(lambda ts: PreBackward.apply(rt, uid, *ts), output)
             rt.release_use(uid, "forward", 0)
@@ -433,6 +436,32 @@ class FullyShardedDataParallel(nn.Module):
                 kernels.cast(u.master, u.low)
         rt.adam_steps = int(sd["adam_steps"])
         torch.cuda.synchronize()
+
+    def memory_ledger(self) -> dict:
+        """Per-category residency and peaks of this rank (memsim.py:113-185),
+        with torch's allocator statistics and the symmetric pool size beside it."""
+        st = torch.cuda.memory_stats(self.rt.device)
+        out = self.rt.ledger.snapshot()
+        out["torch"] = {"allocated_peak_bytes": int(st.get("allocated_bytes.all.peak", 0)),
+                        "reserved_peak_bytes": int(st.get("reserved_bytes.all.peak", 0)),
+                        "num_alloc_retries": int(st.get("num_alloc_retries", 0))}
+        out["symmetric_pool_bytes"] = self.comm.pool_bytes if self.comm is not None else 0
+        return out
+
+    def inject_fault(self, kind: str, step: int | None = None) -> None:
+        """Verify-sensitivity faults (cli.py:568-574): "misordered-reduction"
+        hands every reduce-scatter member the neighbouring chunk
+        (collectives.py:296); "inf-grad" writes inf into unit 0's gradient on
+        this rank at optimizer step `step` (engine.py:541-543)."""
+        if kind == "misordered-reduction":
+            if self.comm is not None:
+                self.comm.set_fault(True)
+            elif self.plan.shard_factor > 1:
+                raise NotImplementedError("misordered-reduction needs the ipc backend")
+        elif kind == "inf-grad":
+            self.rt.inject_inf.add(self.rt.step_count if step is None else int(step))
+        else:
+            raise ValueError(f"unknown fault {kind!r} (misordered-reduction, inf-grad)")
 
     def trace_lines(self) -> list[str]:
         """The reference's trace format (memsim.py:50-61) for this rank."""

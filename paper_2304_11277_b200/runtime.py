@@ -45,6 +45,7 @@ import torch
 
 from . import _lib, kernels
 from .layout import UnitLayout
+from .ledger import MemoryLedger
 from .plan import DeadlockError, ShardingPlan
 
 RAF = "RAF"
@@ -306,6 +307,7 @@ class FSDPRuntime:
         self.compute_stream = torch.cuda.current_stream(self.device)
         self.ag_stream = torch.cuda.Stream(self.device)
         self.rs_stream = torch.cuda.Stream(self.device)
+        self.ledger = MemoryLedger()           # memsim.py:113-185 on the real runtime
         self._alloc_arenas()
         self._alloc_pool_regions()
         # per-step state
@@ -358,8 +360,15 @@ class FSDPRuntime:
         self.exp_avg = torch.zeros(total, **f32) if self.cfg.optimizer == "adam" else None
         self.exp_avg_sq = torch.zeros(total, **f32) if self.cfg.optimizer == "adam" else None
         self.low = torch.zeros(total, dtype=torch.bfloat16, device=self.device) if self.cfg.mixed else None
+        self._resident_torch_bytes = sum(t.numel() * t.element_size() for t in
+                                         (self.master, self.grad, self.exp_avg, self.exp_avg_sq, self.low)
+                                         if t is not None)
         for u, o in zip(self.units, offs):
             n = u.layout.shard_numel
+            self.ledger.alloc("sharded_params", n * 4 + (2 * n if self.low is not None else 0), n)
+            self.ledger.alloc("grads", n * 4, n)
+            if self.exp_avg is not None:
+                self.ledger.alloc("optimizer_state", 2 * n * 4, 2 * n)
             u.master = self.master[o:o + n]
             u.grad = self.grad[o:o + n]
             if self.exp_avg is not None:
@@ -612,6 +621,7 @@ class FSDPRuntime:
         lay = u.layout
         slot, free_ev = self.slots.acquire(uid)
         self.max_live_slots = max(self.max_live_slots, len(self.slots.owner))
+        self.ledger.alloc("unsharded_params", lay.psi * self.compute_dtype.itemsize, lay.psi)
         u.slot = slot
         views = self.slots.views[slot]
         u.unsharded = views[0][: lay.psi]
@@ -705,6 +715,13 @@ class FSDPRuntime:
         self._issue_unshard(uid)
         u.pending = True
 
+    def sample_activations(self) -> None:
+        """After a unit's forward: torch-allocator bytes above the resident
+        shard/optimizer arenas (the reference books activations per unit,
+        engine.py:489; here they are measured)."""
+        self.ledger.set_level("activations",
+                              torch.cuda.memory_allocated(self.device) - self._resident_torch_bytes)
+
     def close_window(self, uid: int) -> None:
         """The unit's first consuming compute has been issued: its completion
         (an event on the compute stream) retires the limiter window."""
@@ -738,6 +755,7 @@ class FSDPRuntime:
         ev = torch.cuda.Event()
         ev.record(self.compute_stream)
         self.slots.release(u.slot, ev)
+        self.ledger.free("unsharded_params", u.layout.psi * self.compute_dtype.itemsize, u.layout.psi)
         u.slot = None
         u.unsharded = None
         u.uses = 0
@@ -806,9 +824,13 @@ class FSDPRuntime:
             torch.cuda.synchronize(self.device)
             self.comm.raise_device_error()
         elif self.aborted():
-            raise DeadlockError("a cross-GPU collective wait timed out on device (this rank or a "
-                                "group member never entered the matching collective); no optimizer "
-                                "update was applied after the abort")
+            torch.cuda.synchronize(self.device)
+            try:
+                self.comm.raise_device_error()
+            except DeadlockError as exc:
+                raise DeadlockError(f"{exc}; no optimizer update was applied after the abort") from None
+            raise DeadlockError("the communicator was aborted (a cross-GPU collective wait timed out); "
+                                "no optimizer update was applied after the abort")
 
     def _step_unit(self, uid: int, stream: torch.cuda.Stream) -> None:
         """Optimizer on one unit's shard slice (same arithmetic as the arena
@@ -929,6 +951,8 @@ class FSDPRuntime:
             u.gslot, u.flat_grad = self._acquire_gslot(lay.psi)
         elif first:
             u.flat_grad = torch.empty(lay.psi, dtype=gdt, device=self.device)
+        if first:
+            self.ledger.alloc("grads", lay.psi * u.flat_grad.element_size(), lay.psi)   # engine.py:530
         with self.timed("flatten_grad", self.compute_stream,
                         sum(g.numel() for g in srcs if g is not None) * 2 * u.flat_grad.element_size()):
             kernels.flatten(srcs, lay.offsets, u.flat_grad, accumulate=not first,
@@ -956,9 +980,11 @@ class FSDPRuntime:
             self._accumulate_local(uid)
             if not self.defer_reduce:
                 self._reduce_unit(uid, u.accum_unsharded)
+                self.ledger.free("grads", u.layout.psi * 4, u.layout.psi)
                 u.accum_unsharded = None
         else:
             self._reduce_unit(uid, u.flat_grad)
+        self.ledger.free("grads", u.layout.psi * u.flat_grad.element_size(), u.layout.psi)
         u.flat_grad = None
 
     def _accumulate_local(self, uid: int) -> None:
@@ -966,6 +992,7 @@ class FSDPRuntime:
         first = u.accum_unsharded is None
         if first:
             u.accum_unsharded = torch.empty(u.layout.psi, dtype=torch.float32, device=self.device)
+            self.ledger.alloc("grads", u.layout.psi * 4, u.layout.psi)        # engine.py:761
         kernels.flatten([u.flat_grad], [0], u.accum_unsharded, accumulate=not first,
                         stream=self.compute_stream)
 
@@ -1032,7 +1059,9 @@ class FSDPRuntime:
         ready = torch.cuda.Event()
         ready.record(self.compute_stream)
         self.events.append((self.step_count, "reduce_issue", uid))
-        self.trace.record("RS_issue", uid, grad.numel() * self.payload_dtype.itemsize)
+        # F = 1 with W > 1 (NO_SHARD) reduces with one all-reduce (engine.py:811-816)
+        self.trace.record("AR_issue" if (F == 1 and W > 1) else "RS_issue", uid,
+                          grad.numel() * self.payload_dtype.itemsize)
         n = u.layout.shard_numel
         tail = (not self.defer_reduce and self.final_micro and bool(self.bwd_order)
                 and uid == self.bwd_order[-1])
@@ -1106,6 +1135,7 @@ class FSDPRuntime:
                     warnings.warn(f"unit {uid}: no gradient for any parameter, zero-filled")
                 if u.flat_grad is None:
                     u.flat_grad = torch.empty(u.layout.psi, dtype=self.compute_dtype, device=self.device)
+                    self.ledger.alloc("grads", u.layout.psi * self.compute_dtype.itemsize, u.layout.psi)
                     kernels.flatten([None] * len(u.layout.originals), u.layout.offsets, u.flat_grad,
                                     stream=self.compute_stream)
                 u.grad_pending = 0

@@ -77,3 +77,39 @@ def test_multigpu_cli_verify():
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     last = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]
     assert json.loads(last)["verify"] == "PASS"
+
+
+@pytest.mark.parametrize("fault", ["misordered-reduction", "inf-grad"])
+def test_multigpu_cli_verify_detects_faults(fault):
+    """verify --inject-fault exits 1 (cli.py:568-590): the rotated
+    reduce-scatter chunk (collectives.py:296) and an inf gradient
+    (engine.py:541-543) are both caught by the parameter comparison."""
+    r = _torchrun(2, ["-m", "paper_2304_11277_b200", "verify", "--steps", "3", "--inject-fault", fault],
+                  timeout=900)
+    last = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]
+    assert r.returncode == 1, r.stdout[-3000:] + r.stderr[-3000:]
+    assert json.loads(last)["verify"] == "FAIL"
+
+
+def test_multigpu_cli_verify_serialized_memory_formula():
+    """verify --serialized: one unit materialised at a time; the ledger's
+    peak parameter bytes equal the closed form (flatparam.py:198-235)."""
+    r = _torchrun(2, ["-m", "paper_2304_11277_b200", "verify", "--steps", "2", "--serialized"], timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    last = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    assert last["verify"] == "PASS" and last["memory"]["ok"], last
+
+
+def test_multigpu_cli_sweep():
+    """sweep (cli.py:623-706): F x RAF grid, one TSV row per point."""
+    r = _torchrun(2, ["-m", "paper_2304_11277_b200", "sweep", "--axis", "F=1,2", "--axis", "raf=RAF,NRAF",
+                      "--steps", "1"], timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if "\t" in l]
+    assert lines[0].startswith("sharding_factor\traf\tfinal_loss\tAG\tRS\tAR")
+    rows = [l.split("\t") for l in lines[1:]]
+    assert len(rows) == 4
+    by = {(a, b): row for a, b, *row in rows}
+    # F=1 (NO_SHARD): no gathers, all-reduce only; F=2 RAF re-gathers in backward, NRAF does not
+    assert int(by[("1", "RAF")][1]) == 0 and int(by[("1", "RAF")][3]) > 0
+    assert int(by[("2", "RAF")][1]) > int(by[("2", "NRAF")][1]) > 0

@@ -264,7 +264,10 @@ int fsdp_allreduce_scalar(fsdp_comm_t* c, const float* const* ins, float* const*
  * bytes, same offset on every member, one region per channel); the receiver
  * polls the flags and unpacks.  The region is double-buffered by epoch
  * parity, which is safe without barriers because a member running epoch e
- * has received every peer's epoch e-1 lines.
+ * has received every peer's epoch e-1 lines.  Lines are laid out in blocks of
+ * 32 as [block][member][parity], so a line's address does not depend on the
+ * message length: calls of different sizes may share the region (one region
+ * per channel sized for the largest call); fsdp_ll_bytes rounds to blocks.
  * fsdp_allgather_ll: same contract and destination as fsdp_allgather
  *   (collectives.py:288-291 + engine.py:661-671); the lines carry the
  *   dst-dtype (cast) payload.

@@ -995,9 +995,19 @@ __device__ __forceinline__ void ll_store_line(T* dst, int64_t L, int64_t n, uint
   }
 }
 
-// LL region of member `pos`'s lines at the receiver whose pool base is `base`
-__device__ __forceinline__ char* ll_region(const CollParams& p, char* base, int pos, int64_t nl) {
-  return base + p.off_b + ((int64_t)(p.epoch & 1u) * p.gsize + pos) * nl * 16;
+// Address of line L from member `pos` in the LL region of the receiver whose
+// pool base is `base`.  Lines go in blocks of kLLBlock (one warp's 512
+// contiguous bytes per store instruction), blocks interleaved as
+// [block][member][epoch parity]: a line's address depends on (L, pos,
+// parity) only, never on the message length, so consecutive calls of
+// different sizes on one channel can never overlap the other parity's lines
+// (a length-dependent layout let a large epoch e+1 overwrite a small epoch
+// e's lines before a slow receiver read them).
+constexpr int kLLBlock = 32;
+__device__ __forceinline__ char* ll_line(const CollParams& p, char* base, int pos, int64_t L) {
+  const int64_t blk = L / kLLBlock;
+  return base + p.off_b +
+         ((((blk * p.gsize + pos) * 2 + (int64_t)(p.epoch & 1u)) * kLLBlock) + (L % kLLBlock)) * 16;
 }
 
 // All-gather: member k sends cast(shard) as LL lines to every other member,
@@ -1020,26 +1030,25 @@ allgather_ll_kernel(const __grid_constant__ CollParams p) {
     const uint2 d = ll_load_line<Tin, Tout>(src, L, n);
     for (int jj = 1; jj < g.size; ++jj) {
       const int j = (g.pos + jj) % g.size;   // stagger destinations
-      st_ll(ll_region(p, p.bases[g.member(j)], g.pos, nl) + L * 16, d.x, d.y, p.epoch);
+      st_ll(ll_line(p, p.bases[g.member(j)], g.pos, L), d.x, d.y, p.epoch);
     }
     ll_store_line<Tout>(dst + (int64_t)g.pos * n, L, n, d.x, d.y);
   }
   for (int jj = 1; jj < g.size; ++jj) {
     const int j = (g.pos + jj) % g.size;
-    const char* reg = ll_region(p, p.bases[g.rank], j, nl);
     Tout* dj = dst + (int64_t)j * n;
     for (int64_t L0 = tid; L0 < nl; L0 += nt * kLLUnroll) {
       uint4 v[kLLUnroll];
 #pragma unroll
       for (int u = 0; u < kLLUnroll; ++u) {
         const int64_t L = L0 + u * nt;
-        if (L < nl) v[u] = ld_ll(reg + L * 16);
+        if (L < nl) v[u] = ld_ll(ll_line(p, p.bases[g.rank], j, L));
       }
 #pragma unroll
       for (int u = 0; u < kLLUnroll; ++u) {
         const int64_t L = L0 + u * nt;
         if (L >= nl) continue;
-        if (!ll_ready(v[u], p.epoch)) v[u] = ll_wait(p, g, reg + L * 16, v[u]);
+        if (!ll_ready(v[u], p.epoch)) v[u] = ll_wait(p, g, ll_line(p, p.bases[g.rank], j, L), v[u]);
         ll_store_line<Tout>(dj, L, n, v[u].x, v[u].z);
       }
     }
@@ -1066,19 +1075,16 @@ reduce_scatter_ll_kernel(const __grid_constant__ CollParams p) {
     for (int jj = 1; jj < g.size; ++jj) {
       const int j = (g.pos + jj) % g.size;
       const uint2 d = ll_load_line<Tin, Tin>(flat + (int64_t)rs_chunk(p, j, g.size) * n, L, n);
-      st_ll(ll_region(p, p.bases[g.member(j)], g.pos, nl) + L * 16, d.x, d.y, p.epoch);
+      st_ll(ll_line(p, p.bases[g.member(j)], g.pos, L), d.x, d.y, p.epoch);
     }
   }
   const bool pre = p.prediv != 1.0f, post = p.postdiv != 1.0f;
   const Tin* mine = flat + (int64_t)rs_chunk(p, g.pos, g.size) * n;
-  const char* reg[MAXW];
-#pragma unroll
-  for (int j = 0; j < MAXW; ++j) reg[j] = j < g.size ? ll_region(p, p.bases[g.rank], j, nl) : nullptr;
   for (int64_t L = tid; L < nl; L += nt) {
     uint4 v[MAXW];
 #pragma unroll
     for (int j = 0; j < MAXW; ++j)      // every peer's line in flight before any wait
-      if (j < g.size && j != g.pos) v[j] = ld_ll(reg[j] + L * 16);
+      if (j < g.size && j != g.pos) v[j] = ld_ll(ll_line(p, p.bases[g.rank], j, L));
     float acc[EPL];
 #pragma unroll
     for (int q = 0; q < EPL; ++q) acc[q] = 0.0f;
@@ -1089,7 +1095,7 @@ reduce_scatter_ll_kernel(const __grid_constant__ CollParams p) {
       if (j == g.pos) {
         d = ll_load_line<Tin, Tin>(mine, L, n);
       } else {
-        if (!ll_ready(v[j], p.epoch)) v[j] = ll_wait(p, g, reg[j] + L * 16, v[j]);
+        if (!ll_ready(v[j], p.epoch)) v[j] = ll_wait(p, g, ll_line(p, p.bases[g.rank], j, L), v[j]);
         d = make_uint2(v[j].x, v[j].z);
       }
       float x[EPL];
@@ -2112,7 +2118,8 @@ extern "C" int64_t fsdp_ll_bytes(int gsize, int64_t n, int dtype) {
   const int es = elem_size(dtype);
   if (gsize < 1 || n < 0 || !es) return -1;
   const int64_t nl = (n * es + 7) / 8;
-  return 2 * (int64_t)gsize * nl * 16;
+  const int64_t blocks = (nl + kLLBlock - 1) / kLLBlock;      // whole line blocks (ll_line layout)
+  return 2 * (int64_t)gsize * blocks * kLLBlock * 16;
 }
 
 static int ll_grid(fsdp_comm_t* c, int64_t nl, int kind) {

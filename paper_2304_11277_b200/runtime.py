@@ -465,9 +465,10 @@ class FSDPRuntime:
             total += nslots * pad(psi_max * es) + 3 * pad(psi_max * ps)
             if W > 1 and cfg.ll_max_bytes > 0:
                 ll_n = max((l.shard_numel for l in layouts if l.psi * es <= cfg.ll_max_bytes), default=0)
-                # LL lines carry 8 payload bytes in 16 (x2 epoch parities, per member)
+                # LL lines carry 8 payload bytes in 16 (x2 epoch parities, per
+                # member), in whole blocks of 32 lines (fsdp_ll_bytes)
                 for sz in (es, ps):
-                    total += pad(2 * F * (-(-ll_n * sz // 8)) * 16)
+                    total += pad(2 * F * (-(-(-(-ll_n * sz // 8)) // 32)) * 32 * 16)
         if W > 1 and F < W:
             n_ar = n_max if F > 1 else psi_max
             g = W // F

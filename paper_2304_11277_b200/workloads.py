@@ -55,6 +55,10 @@ CONFIGS = {
     "gpt30b": GPTConfig("gpt30b", 7168, 48, 50304, 2048, 56),
     # depth-reduced same-width variants (single-GPU references)
     "gpt1.3b-l4": GPTConfig("gpt1.3b-l4", 2048, 4, 50304, 2048, 16),
+    # GPT-30B width (block psi = 616,655,872) at reduced depth: HYBRID runs on
+    # 4 GPUs whose replica all-reduce moves the 30B config's per-unit shard sizes
+    "gpt30b-l12": GPTConfig("gpt30b-l12", 7168, 12, 50304, 2048, 56),
+    "gpt30b-l8": GPTConfig("gpt30b-l8", 7168, 8, 50304, 2048, 56),
 }
 
 

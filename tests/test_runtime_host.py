@@ -15,7 +15,8 @@ from paper_2304_11277_b200.runtime import FSDPRuntime, RuntimeConfig
 def test_ll_bytes_formula(gsize, n):
     for dt, es in ((F32, 4), (BF16, 2)):
         lines = -(-(n * es) // 8)                 # 8 payload bytes per 16-byte line
-        assert lib.fsdp_ll_bytes(gsize, n, dt) == 2 * gsize * lines * 16
+        blocks = -(-lines // 32)                  # whole 32-line blocks
+        assert lib.fsdp_ll_bytes(gsize, n, dt) == 2 * gsize * blocks * 32 * 16
     assert lib.fsdp_ll_bytes(0, 8, F32) == -1
     assert lib.fsdp_ll_bytes(2, 8, 7) == -1
 

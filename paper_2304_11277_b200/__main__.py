@@ -176,7 +176,8 @@ def cmd_verify(a) -> int:
     if a.serialized and fsdp.plan.shard_factor > 1:
         lays = fsdp.layouts
         pred = peak_param_bytes([l.psi for l in lays], [l.shard_numel for l in lays], fsdp.plan.shard_factor,
-                                k_full=4, k_low=2 if fsdp.mixed else None, low_copy=fsdp.mixed)
+                                k_full=4, k_low=2 if fsdp.mixed else None, low_copy=fsdp.mixed,
+                                nested_root=True)
         meas = fsdp.rt.ledger.peak_param_bytes
         mem = {"peak_param_bytes": meas, "predicted": pred, "ok": meas == pred}
         ok = ok and meas == pred

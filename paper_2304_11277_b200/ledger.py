@@ -83,15 +83,24 @@ class MemoryLedger:
 
 
 def peak_param_bytes(psis, shard_numels, shard_factor: int, k_full: int = 4, k_low: int | None = 2,
-                     low_copy: bool = True, variant: str = "serialized") -> int:
+                     low_copy: bool = True, variant: str = "serialized", nested_root: bool = False) -> int:
     """flatparam.py:198-235 (peak_param_memory) for this runtime's layout:
     resident shards in full precision (k_full per element, plus the k_low
     bf16 copy when `low_copy`), plus the gathered units in k_low (serialized:
-    the largest one; two_inflight: the two largest).  F = 1 gathers nothing."""
+    the largest one; two_inflight: the two largest).  F = 1 gathers nothing.
+
+    nested_root: unit 0 is the wrapper's root, whose forward encloses every
+    other unit (torch-FSDP nesting; the reference's units are sequential), so
+    it stays gathered while each child is: serialized peak = root + the
+    largest child (two_inflight: root + the two largest children)."""
     shards = sum(shard_numels)
     res = shards * k_full + (shards * k_low if (low_copy and k_low) else 0)
     if shard_factor == 1 or not psis:
         return res
+    k = k_low if k_low else k_full
+    if nested_root:
+        kids = sorted(psis[1:], reverse=True)
+        return res + (psis[0] + sum(kids[:1] if variant == "serialized" else kids[:2])) * k
     largest = sorted(psis, reverse=True)
     gathered = largest[:1] if variant == "serialized" else largest[:2]
-    return res + sum(gathered) * (k_low if k_low else k_full)
+    return res + sum(gathered) * k

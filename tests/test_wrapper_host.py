@@ -70,6 +70,12 @@ def test_peak_formula_matches_reference_shape():
     assert peak_param_bytes(psis, shards, F) == sum(shards) * 6 + 72 * 2
     assert peak_param_bytes(psis, shards, F, variant="two_inflight") == sum(shards) * 6 + (72 + 40) * 2
     assert peak_param_bytes(psis, psis, 1) == sum(psis) * 6                 # F = 1 gathers nothing
+    # wrapper nesting: the root (unit 0) stays gathered under every child
+    assert peak_param_bytes(psis, shards, F, nested_root=True) == sum(shards) * 6 + (40 + 72) * 2
+    # the tiny GPT fp32 verify case measured on the GPU: 8,090,624 bytes at F = 2
+    tiny = [295424, 789760, 789760]
+    assert peak_param_bytes(tiny, [p // 2 for p in tiny], 2, k_low=None, low_copy=False,
+                            nested_root=True) == 8090624
 
 
 def test_sweep_axis_parser():

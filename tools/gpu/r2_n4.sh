@@ -1,0 +1,27 @@
+#!/bin/bash
+# Round 2 on a 4-GPU box: real multi-GPU parity (W=2,4), self-launched bench
+# at N=1/2/4, GPT-30B-width HYBRID 2x2 (replica all-reduce at size), sweep, reference arm.
+O=gpurun_out/${OUT:-r2n4}; mkdir -p $O
+nvidia-smi --query-gpu=index,name,clocks.sm,clocks.max.sm,power.limit --format=csv > $O/gpus.txt 2>&1
+python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
+T0=$(date +%s)
+timeout 1800 python -m pytest tests/test_multigpu.py -q -m gpu > $O/pytest_multigpu.log 2>&1
+echo "multigpu rc=$? secs=$(( $(date +%s) - T0 ))" >> $O/times.txt
+for N in 1 2 4; do
+  T0=$(date +%s)
+  timeout 900 python bench.py --gpus $N --steps 20 --warmup 5 --exposed > $O/bench_n$N.json 2> $O/bench_n$N.err
+  echo "bench n=$N rc=$? secs=$(( $(date +%s) - T0 ))" >> $O/times.txt
+done
+T0=$(date +%s)
+timeout 1500 python bench.py --gpus 4 --config gpt30b-l12 --micro 1 --strategy HYBRID_SHARD --hybrid-shard-size 2 --steps 4 --warmup 3 --exposed > $O/bench_gpt30b_l12_hybrid2x2_n4.json 2> $O/bench_gpt30b_l12_hybrid2x2_n4.err
+echo "hybrid30b rc=$? secs=$(( $(date +%s) - T0 ))" >> $O/times.txt
+T0=$(date +%s)
+timeout 900 python bench.py --gpus 4 --strategy HYBRID_SHARD --hybrid-shard-size 2 --steps 10 --warmup 3 --exposed > $O/bench_gpt1.3b_hybrid2x2_n4.json 2> $O/bench_gpt1.3b_hybrid2x2_n4.err
+echo "hybrid1.3b rc=$? secs=$(( $(date +%s) - T0 ))" >> $O/times.txt
+T0=$(date +%s)
+FSDP_SWEEP_SIZES=1,16,64,128,256,1024,2048 timeout 1500 python bench.py --gpus 4 --mode sweep > $O/sweep_n4.json 2> $O/sweep_n4.err
+echo "sweep rc=$? secs=$(( $(date +%s) - T0 ))" >> $O/times.txt
+T0=$(date +%s)
+timeout 900 python bench.py --impl reference --gpus 4 --steps 20 --warmup 5 > $O/bench_ref_n4.json 2> $O/bench_ref_n4.err
+echo "ref n4 rc=$? secs=$(( $(date +%s) - T0 ))" >> $O/times.txt
+echo done

@@ -74,6 +74,9 @@ def parse():
                     help="step each unit's shard in backward (measured: slower at N=1, "
                          "Adam contends for HBM with the backward kernels)")
     ap.add_argument("--cpu-tokens", type=int, default=2048)
+    ap.add_argument("--fused-cast-ag", action="store_true",
+                    help="gather the fp32 master shard with the bf16 cast fused into the (SM/LL) "
+                         "all-gather instead of the bf16 copy Adam writes (copy engines)")
     return ap.parse_args()
 
 
@@ -208,7 +211,7 @@ def run_ours(args):
         optimizer_in_backward=args.opt_in_bwd, forward_prefetch=args.forward_prefetch,
         ag_ctas=args.ctas, rs_ctas=args.rs_ctas, ag_engine=args.ag_engine,
         rs_engine=args.rs_engine, tail_engine=args.tail_engine, ll_max_bytes=args.ll_max_bytes,
-        opt_split_first=args.opt_split_first)
+        opt_split_first=args.opt_split_first, fused_cast_ag=args.fused_cast_ag)
     opt = fsdp.optimizer()
     rt = fsdp.rt
     dev_inputs = tuple(h.to(dev) for h in host)
@@ -320,7 +323,8 @@ def run_ours(args):
     # dominant SM kernel of this library; collectives moved by copy engines
     # (DMA, no SM code) are reported separately as bus bandwidth
     dma = {k for k in ("allgather", "reduce_scatter")
-           if (k == "allgather" and args.ag_engine == "ce") or (k == "reduce_scatter" and args.rs_engine == "ce")}
+           if (k == "allgather" and args.ag_engine == "ce" and not args.fused_cast_ag)
+           or (k == "reduce_scatter" and args.rs_engine == "ce")}
     cands = {k: v for k, v in mine.items() if k not in dma}
     dom = max(cands, key=lambda k: cands[k]["total_ms"]) if cands else None
     roof = None
@@ -421,6 +425,7 @@ def step_config(args, world: int) -> dict:
                             "first_ag_last_rs": args.tail_engine,
                             "low_latency_max_bytes": args.ll_max_bytes},
             "opt_split_first": args.opt_split_first,
+            **({"fused_cast_ag": True} if args.fused_cast_ag else {}),
             "l2": "inputs > L2 (weights+state >20 GB)"}
 
 

@@ -142,7 +142,8 @@ class FullyShardedDataParallel(nn.Module):
                  optimizer: str = "adam", lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-8,
                  optimizer_in_backward: bool = False, ag_engine: str = "ce", rs_engine: str = "ce",
                  tail_engine: str = "sm", ll_max_bytes: int = 6 << 20, opt_split_first: int = 2,
-                 rate_limit: int | None | str = "auto", keep_outermost_unsharded: bool = True):
+                 rate_limit: int | None | str = "auto", keep_outermost_unsharded: bool = True,
+                 fused_cast_ag: bool = False):
         super().__init__()
         if cpu_offload is not None and cpu_offload.offload_params:
             raise NotImplementedError("CPU offload is out of scope for the B200 runtime")
@@ -195,7 +196,8 @@ class FullyShardedDataParallel(nn.Module):
                             optimizer=optimizer, lr=lr, betas=tuple(betas), eps=eps,
                             optimizer_in_backward=optimizer_in_backward,
                             ag_engine=ag_engine, rs_engine=rs_engine, tail_engine=tail_engine,
-                            ll_max_bytes=ll_max_bytes, opt_split_first=opt_split_first)
+                            ll_max_bytes=ll_max_bytes, opt_split_first=opt_split_first,
+                            fused_cast_ag=fused_cast_ag)
         self.module = module
         self.plan = plan
         self.rank = rank

@@ -123,6 +123,13 @@ class RuntimeConfig:
     # all-gathers wait only for it and overlap the launch over the rest of
     # the arena (0 = one launch).  Same arithmetic, elementwise.
     opt_split_first: int = 2
+    # the north star's fused path: gather the fp32 master shard with the
+    # fp32 -> bf16 cast fused into the all-gather kernel (SM push / NVLS / LL),
+    # instead of gathering the bf16 copy Adam's epilogue writes (copy
+    # engines need equal dtypes).  Saves the 2 B/elem bf16 write in Adam and
+    # the bf16 copy's memory; the gather reads 4 B/elem instead of 2 and runs
+    # on SMs.  Same bits either way (cast-then-gather == gather-then-cast).
+    fused_cast_ag: bool = False
 
     def __post_init__(self):
         if self.reshard_after_forward not in (RAF, NRAF):
@@ -359,7 +366,8 @@ class FSDPRuntime:
         self.grad = torch.zeros(total, **f32)
         self.exp_avg = torch.zeros(total, **f32) if self.cfg.optimizer == "adam" else None
         self.exp_avg_sq = torch.zeros(total, **f32) if self.cfg.optimizer == "adam" else None
-        self.low = torch.zeros(total, dtype=torch.bfloat16, device=self.device) if self.cfg.mixed else None
+        keep_low = self.cfg.mixed and not (self.cfg.fused_cast_ag and self.plan.shard_factor > 1)
+        self.low = torch.zeros(total, dtype=torch.bfloat16, device=self.device) if keep_low else None
         self._resident_torch_bytes = sum(t.numel() * t.element_size() for t in
                                          (self.master, self.grad, self.exp_avg, self.exp_avg_sq, self.low)
                                          if t is not None)
@@ -626,7 +634,7 @@ class FSDPRuntime:
         u.slot = slot
         views = self.slots.views[slot]
         u.unsharded = views[0][: lay.psi]
-        src = u.low if self.cfg.mixed else u.master
+        src = u.low if u.low is not None else u.master      # fp32 master: cast fused into the gather
         with torch.cuda.stream(self.ag_stream):
             if free_ev is not None:
                 self.ag_stream.wait_event(free_ev)

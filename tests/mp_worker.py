@@ -314,7 +314,7 @@ def nvls_collectives(rank, world, results):
 
 
 def fsdp_step_parity(rank, world, strategy, hybrid, results, backend="ipc", opt_in_bwd=False,
-                     engine="ce", ll=False):
+                     engine="ce", ll=False, fused=False):
     """ll=False pins every unit to `engine` (the tiny GPT's units are all
     small enough for the low-latency path, which ll=True exercises)."""
     from paper_2304_11277_b200 import kernels  # noqa: F401
@@ -329,7 +329,7 @@ def fsdp_step_parity(rank, world, strategy, hybrid, results, backend="ipc", opt_
                                     hybrid_shard_size=hybrid, comm_backend=backend, lr=1e-3,
                                     optimizer_in_backward=opt_in_bwd, ag_engine=engine,
                                     rs_engine="sm" if engine == "nvls" else engine,
-                                    ll_max_bytes=(6 << 20) if ll else 0)
+                                    ll_max_bytes=(6 << 20) if ll else 0, fused_cast_ag=fused)
     plan = fsdp.plan
     ref = init_gpt_(GPT(cfg), seed=0).cuda().to(torch.bfloat16)
     x, y = synthetic_batch(cfg, 2, seed=100 + rank, device="cuda")
@@ -338,7 +338,7 @@ def fsdp_step_parity(rank, world, strategy, hybrid, results, backend="ipc", opt_
     lref = ref(x, y)
     lref.backward()
     key = (f"{strategy}{'' if hybrid is None else hybrid}/{backend}/{'ll' if ll else engine}"
-           f"{'/opt-in-bwd' if opt_in_bwd else ''}")
+           f"{'/opt-in-bwd' if opt_in_bwd else ''}{'/fused-cast-ag' if fused else ''}")
     torch.cuda.synchronize()
     # initial shards from the oracle (flatten + shard of the same init)
     vals = {k: v.detach().float().cpu().numpy() for k, v in init_gpt_(GPT(cfg), seed=0).named_parameters()}
@@ -639,7 +639,9 @@ def main():
         steps += [("FULL_SHARD", None, {"opt_in_bwd": True}), ("FULL_SHARD", None, {"ll": True}),
                   ("SHARD_GRAD_OP", None, {"ll": True})]
         steps += [("HYBRID_SHARD", f, {"ll": True}) for f in hybrids]
-        steps += [("FULL_SHARD", None, {"engine": "sm"})]
+        steps += [("FULL_SHARD", None, {"engine": "sm"}), ("FULL_SHARD", None, {"fused": True}),
+                  ("FULL_SHARD", None, {"fused": True, "ll": True})]
+        steps += [("HYBRID_SHARD", f, {"fused": True}) for f in hybrids]
         if not SHARED:
             steps += [("FULL_SHARD", None, {"engine": "nvls"})]
             steps += [("HYBRID_SHARD", f, {"engine": "nvls"}) for f in hybrids]

@@ -721,6 +721,8 @@ class FSDPRuntime:
         limit = self.cfg.rate_limit
         if limit is not None and len(self.inflight) >= limit:
             return
+        if self.slots is not None and not self.slots.free:
+            return                      # every slot holds a live unit: prefetch is opportunistic
         self._issue_unshard(uid)
         u.pending = True
 

@@ -314,7 +314,7 @@ def nvls_collectives(rank, world, results):
 
 
 def fsdp_step_parity(rank, world, strategy, hybrid, results, backend="ipc", opt_in_bwd=False,
-                     engine="ce", ll=False, fused=False):
+                     engine="ce", ll=False, fused=False, num_slots=None):
     """ll=False pins every unit to `engine` (the tiny GPT's units are all
     small enough for the low-latency path, which ll=True exercises)."""
     from paper_2304_11277_b200 import kernels  # noqa: F401
@@ -329,7 +329,8 @@ def fsdp_step_parity(rank, world, strategy, hybrid, results, backend="ipc", opt_
                                     hybrid_shard_size=hybrid, comm_backend=backend, lr=1e-3,
                                     optimizer_in_backward=opt_in_bwd, ag_engine=engine,
                                     rs_engine="sm" if engine == "nvls" else engine,
-                                    ll_max_bytes=(6 << 20) if ll else 0, fused_cast_ag=fused)
+                                    ll_max_bytes=(6 << 20) if ll else 0, fused_cast_ag=fused,
+                                    num_slots=num_slots)
     plan = fsdp.plan
     ref = init_gpt_(GPT(cfg), seed=0).cuda().to(torch.bfloat16)
     x, y = synthetic_batch(cfg, 2, seed=100 + rank, device="cuda")
@@ -338,7 +339,8 @@ def fsdp_step_parity(rank, world, strategy, hybrid, results, backend="ipc", opt_
     lref = ref(x, y)
     lref.backward()
     key = (f"{strategy}{'' if hybrid is None else hybrid}/{backend}/{'ll' if ll else engine}"
-           f"{'/opt-in-bwd' if opt_in_bwd else ''}{'/fused-cast-ag' if fused else ''}")
+           f"{'/opt-in-bwd' if opt_in_bwd else ''}{'/fused-cast-ag' if fused else ''}"
+           f"{'' if num_slots is None else '/slots%d' % num_slots}")
     torch.cuda.synchronize()
     # initial shards from the oracle (flatten + shard of the same init)
     vals = {k: v.detach().float().cpu().numpy() for k, v in init_gpt_(GPT(cfg), seed=0).named_parameters()}
@@ -642,6 +644,11 @@ def main():
         steps += [("FULL_SHARD", None, {"engine": "sm"}), ("FULL_SHARD", None, {"fused": True}),
                   ("FULL_SHARD", None, {"fused": True, "ll": True})]
         steps += [("HYBRID_SHARD", f, {"fused": True}) for f in hybrids]
+        # slot-starved: 2 slots for 3 units (root kept + one block at a time;
+        # backward prefetch finds no free slot and is skipped).  The default 3
+        # slots already re-gather each block into a different slot in backward
+        # (saved tensors re-materialise against it, pack_hook)
+        steps += [("FULL_SHARD", None, {"num_slots": 2})]
         if not SHARED:
             steps += [("FULL_SHARD", None, {"engine": "nvls"})]
             steps += [("HYBRID_SHARD", f, {"engine": "nvls"}) for f in hybrids]

@@ -1154,7 +1154,7 @@ struct fsdp_comm {
   // copy-engine path: one side stream per (collective kind, peer, piece) —
   // all-gather and reduce-scatter copies never queue behind each other —
   // and an event pool
-  cudaStream_t ce_stream[2][FSDP_MAX_RANKS * 4] = {};
+  cudaStream_t ce_stream[3][FSDP_MAX_RANKS * 4] = {};   // [AG, RS, AR][...]
   int ce_split = 1;                           // pieces per peer copy (FSDP_CE_SPLIT, <= 4)
   bool ce_shared_streams = false;             // FSDP_CE_SHARED_STREAMS=1: AG and RS share side streams
   // one destination at a time, staggered (FSDP_CE_SERIAL=0: one side stream
@@ -1704,7 +1704,7 @@ static int ce_prepare(fsdp_comm_t* c) {
     if (const char* e = getenv("FSDP_CE_RS_NOREDUCE")) c->ce_rs_noreduce = atoi(e) != 0;
     if (const char* e = getenv("FSDP_CE_REDUCE_CAP")) c->ce_reduce_cap = std::max(0, atoi(e));
     if (const char* e = getenv("FSDP_CE_RS_SM_FRAC")) c->ce_rs_sm_frac = std::max(0.f, std::min(0.9f, (float)atof(e)));
-    for (int k = 0; k < 2; ++k)
+    for (int k = 0; k < 3; ++k)
       for (int r = 0; r < FSDP_MAX_RANKS * c->ce_split; ++r)
         FSDP_CUDA(cudaStreamCreateWithFlags(&c->ce_stream[k][r], cudaStreamNonBlocking));
     c->ce_events.resize(256);
@@ -2025,7 +2025,9 @@ extern "C" int fsdp_allreduce_ce(fsdp_comm_t* c, int channel, int gsize, int gst
   const int pos = gstride == 1 ? c->rank - start : c->rank / gstride;
   auto clen = [&](int j) -> int64_t { const int64_t b = (int64_t)j * ch; return b >= n ? 0 : std::min(ch, n - b); };
   char* mine = c->bases[c->rank];
-  cudaStream_t cs = c->ce_stream[c->ce_shared_streams ? 0 : 1][0];
+  // own side stream: a HYBRID stage-2 all-reduce of unit u overlaps the
+  // reduce-scatter of unit u+1 (caller streams differ), DMA included
+  cudaStream_t cs = c->ce_stream[c->ce_shared_streams ? 0 : 2][0];
   cudaEvent_t a = nullptr, b = nullptr;
   if (c->timing) { a = take_event(c); b = take_event(c); FSDP_CUDA(cudaEventRecord(a, s)); }
   // 1. reduce-scatter push: chunk j -> member j's staging slot pos

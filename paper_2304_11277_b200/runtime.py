@@ -314,6 +314,11 @@ class FSDPRuntime:
         self.compute_stream = torch.cuda.current_stream(self.device)
         self.ag_stream = torch.cuda.Stream(self.device)
         self.rs_stream = torch.cuda.Stream(self.device)
+        # HYBRID stage 2 (replica all-reduce) runs on its own stream behind its
+        # reduce-scatter, so the reduce-scatter of the next unit (and the
+        # release of its gradient slot) does not queue behind it
+        W_, F_ = plan.world_size, plan.shard_factor
+        self.ar_stream = torch.cuda.Stream(self.device) if 1 < F_ < W_ else self.rs_stream
         self.ledger = MemoryLedger()           # memsim.py:113-185 on the real runtime
         self._alloc_arenas()
         self._alloc_pool_regions()
@@ -1031,15 +1036,17 @@ class FSDPRuntime:
                                           [out], prediv=pre, postdiv=post, accumulate=accumulate,
                                           stream=self.rs_stream, tma=False)
 
-    def _ar(self, inp: torch.Tensor, out: torch.Tensor, post: float, accumulate: bool) -> None:
+    def _ar(self, inp: torch.Tensor, out: torch.Tensor, post: float, accumulate: bool,
+            stream: torch.cuda.Stream | None = None) -> None:
         """All-reduce in the replicated group (hybrid stage 2 / NO_SHARD):
         copy engines with rs_engine="ce", else the two-shot SM kernel."""
+        s = stream if stream is not None else self.rs_stream
         if self.cfg.rs_engine == "ce":
             self.comm.all_reduce_ce(self.plan.replicated_desc, inp, self.ar_stage_off, self.ar_gather_off,
-                                    out, postdiv=post, accumulate=accumulate, stream=self.rs_stream)
+                                    out, postdiv=post, accumulate=accumulate, stream=s)
         else:
             self.comm.all_reduce(self.plan.replicated_desc, [inp], self.ar_stage_off, self.ar_gather_off,
-                                 [out], postdiv=post, accumulate=accumulate, stream=self.rs_stream)
+                                 [out], postdiv=post, accumulate=accumulate, stream=s)
 
     def _acquire_gslot(self, psi: int) -> tuple[int, torch.Tensor]:
         """Next symmetric gradient slot (alternating); compute waits until the
@@ -1104,16 +1111,19 @@ class FSDPRuntime:
                     self._rs(gslot, payload.dtype, tmp, pre, 1.0, False, tail)
                 self.events.append((self.step_count, "reduce_stage2", uid))
                 self.trace.record("AR_issue", uid, n * 4)
-                with self.timed("allreduce", self.rs_stream, n * 4):
-                    self._ar(tmp, u.grad, post, accumulate)
-                tmp.record_stream(self.rs_stream)
+                rs_done = torch.cuda.Event()
+                rs_done.record(self.rs_stream)
+                self.ar_stream.wait_event(rs_done)
+                with self.timed("allreduce", self.ar_stream, n * 4):
+                    self._ar(tmp, u.grad, post, accumulate, stream=self.ar_stream)
+                tmp.record_stream(self.ar_stream)
             payload.record_stream(self.rs_stream)
             if gslot is not None:
                 ev = torch.cuda.Event()
-                ev.record(self.rs_stream)
+                ev.record(self.rs_stream)          # free once the reduce-scatter read it
                 self.gslot_free[gslot] = ev
             if self._step_in_backward():
-                self._step_unit(uid, self.rs_stream)   # right behind its reduction
+                self._step_unit(uid, self.ar_stream)   # right behind its (last) reduction
         self.bytes_rs += grad.numel() * (2 if self.payload_dtype == torch.bfloat16 else 4)
         u.reduces_this_step += 1
 
@@ -1158,6 +1168,8 @@ class FSDPRuntime:
                     u.pending = False
                 self.reshard(u.uid)
         self._wait("reduce_scatter_end", stream=self.rs_stream)   # every reduction done
+        if self.ar_stream is not self.rs_stream:
+            self._wait("allreduce_end", stream=self.ar_stream)
         self.in_backward = False
         self.prev_fwd_order = list(self.fwd_order)
         self.micro_index += 1
@@ -1180,6 +1192,7 @@ class FSDPRuntime:
                 # reference zero-fills missing gradients, flatparam.py:181-185),
                 # never a stale one from an earlier step
                 self.compute_stream.wait_stream(self.rs_stream)
+                self.compute_stream.wait_stream(self.ar_stream)
                 u.grad.zero_()
         skip = None
         if scale is not None:
@@ -1204,7 +1217,7 @@ class FSDPRuntime:
             # reduction on the reduce stream
             self.adam_steps += 1
             ev = torch.cuda.Event()
-            ev.record(self.rs_stream)
+            ev.record(self.ar_stream)             # = rs_stream unless HYBRID
             self.compute_stream.wait_event(ev)
             self.opt_done = ev
             self.opt_early, self.opt_early_units = None, 0

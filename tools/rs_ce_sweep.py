@@ -38,6 +38,14 @@ VARIANTS = {
     "push_geo_p3": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_PIECES": "3", "FSDP_CE_RS_MIN_PIECE": str(1 << 20)},
     "push_geo_p4": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_PIECES": "4", "FSDP_CE_RS_MIN_PIECE": str(1 << 20)},
     "push_geo_p5": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_PIECES": "5", "FSDP_CE_RS_MIN_PIECE": str(1 << 20)},
+    # pipelining at unit sizes (GPT-1.3B block at W=4: 12.6 M-element chunks):
+    # geometric pieces down to 8 / 4 M elements (16 / 8 MB per member piece)
+    "push_geo_u8M": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_PIPE_MIN": str(8 << 20),
+                     "FSDP_CE_RS_MIN_PIECE": str(4 << 20)},
+    "push_geo_u4M": {"FSDP_CE_RS_PUSH": "1", "FSDP_CE_RS_PIPE_MIN": str(4 << 20),
+                     "FSDP_CE_RS_MIN_PIECE": str(2 << 20)},
+    "pull_uni_u8M": {"FSDP_CE_RS_PUSH": "0", "FSDP_CE_RS_GEOM": "0", "FSDP_CE_RS_PIECES": "4",
+                     "FSDP_CE_RS_PIPE_MIN": str(8 << 20)},
 }
 
 

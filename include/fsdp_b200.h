@@ -251,6 +251,16 @@ int fsdp_allreduce(fsdp_comm_t* c, int channel, int gsize, int gstride, const vo
 int fsdp_allreduce_ce(fsdp_comm_t* c, int channel, int gsize, int gstride, const void* in,
                       int src_dtype, int64_t n, int64_t stage_off, int64_t gather_off, float* out,
                       float postdiv, int accumulate, void* stream);
+/* Same, with the output itself a pool region: out = [out_off, +n fp32) at
+ * the same offset on every member (out_off 16-byte aligned).  The owner
+ * reduces its chunk straight into its own out slice and the DMA pushes that
+ * slice into every member's out: no gather buffer and no epilogue pass (HBM
+ * traffic per member drops by ~2n*4 bytes).  out = sum / postdiv
+ * (accumulate = 0 semantics; the runtime keeps its HYBRID / NO_SHARD fp32
+ * gradient arena in the pool to use this on the first micro-batch). */
+int fsdp_allreduce_ce_pool(fsdp_comm_t* c, int channel, int gsize, int gstride, const void* in,
+                           int src_dtype, int64_t n, int64_t stage_off, int64_t out_off, float postdiv,
+                           void* stream);
 
 /* 1-element world all-reduce of a float flag (engine.py:572-576):
  * *outs[e] = sum over ranks (ascending) of *ins[e]. */

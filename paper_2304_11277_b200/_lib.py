@@ -88,6 +88,7 @@ _SIGS = {
     "fsdp_allreduce": (_i32, [_vp, _i32, _i32, _i32, _vpp, _i32, _i64, _i64, _i64, _vpp, _f32,
                               _i32, _vp]),
     "fsdp_allreduce_ce": (_i32, [_vp, _i32, _i32, _i32, _vp, _i32, _i64, _i64, _i64, _vp, _f32, _i32, _vp]),
+    "fsdp_allreduce_ce_pool": (_i32, [_vp, _i32, _i32, _i32, _vp, _i32, _i64, _i64, _i64, _f32, _vp]),
     "fsdp_allreduce_scalar": (_i32, [_vp, _vpp, _vpp, _vp]),
     "fsdp_ll_bytes": (_i64, [_i32, _i64, _i32]),
     "fsdp_allgather_ll": (_i32, [_vp, _i32, _i32, _i32, _vpp, _i32, _i64, _i64, _i32, _i64, _vp]),

@@ -464,6 +464,14 @@ class DeviceComm:
                                     out.data_ptr(), float(postdiv), int(accumulate),
                                     stream_ptr(stream)), "allreduce_ce")
 
+    def all_reduce_ce_pool(self, gdesc, inp: torch.Tensor, stage_off: int, out_off: int,
+                           postdiv: float = 1.0, stream=None, channel: int = _lib.CH_AR) -> None:
+        """Copy-engine all-reduce whose output is the pool region at out_off
+        (same offset on every member): no gather buffer, no epilogue."""
+        check(lib.fsdp_allreduce_ce_pool(self._h, channel, gdesc[0], gdesc[1], inp.data_ptr(),
+                                         dtype_code(inp.dtype), inp.numel(), stage_off, out_off,
+                                         float(postdiv), stream_ptr(stream)), "allreduce_ce_pool")
+
     def scalar_all_reduce(self, ins: Sequence[torch.Tensor], outs: Sequence[torch.Tensor],
                           stream=None) -> None:
         check(lib.fsdp_allreduce_scalar(self._h, self._ptrs(ins), self._ptrs(outs),

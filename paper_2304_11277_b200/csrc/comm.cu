@@ -2004,22 +2004,21 @@ extern "C" int fsdp_reduce_scatter_ce(fsdp_comm_t* c, int channel, int gsize, in
 // every member's gather buffer + flag; out = (accumulate ? out : 0) +
 // gathered.  Peers read nothing of mine and the next call's enter barrier
 // guards the staging/gather buffers, so there is no exit barrier.
-extern "C" int fsdp_allreduce_ce(fsdp_comm_t* c, int channel, int gsize, int gstride, const void* in,
-                                 int src_dtype, int64_t n, int64_t stage_off, int64_t gather_off,
-                                 float* out, float postdiv, int accumulate, void* stream) {
-  if (int rc = validate_group(c, channel, gsize, gstride)) return rc;
-  if (c->emulated) return fail(FSDP_E_UNSUPPORTED, "copy-engine collectives need a real communicator");
+// out_off >= 0: `out` is the pool region [out_off, +n fp32) on every member
+// (same offset everywhere): the owner reduces its chunk straight into its own
+// out slice and the DMA pushes that slice into every member's out, so there
+// is no gather buffer and no epilogue (accumulate must be 0).
+static int allreduce_ce_impl(fsdp_comm_t* c, int channel, int gsize, int gstride, const void* in,
+                             int src_dtype, int64_t n, int64_t stage_off, int64_t gather_off, float* out,
+                             int64_t out_off, float postdiv, int accumulate, cudaStream_t s) {
   const int is = elem_size(src_dtype);
-  if (n < 0 || !in || !out || !is) return fail(FSDP_E_INVALID, "fsdp_allreduce_ce: bad args");
-  if (!(postdiv > 0.f)) return fail(FSDP_E_INVALID, "postdiv must be > 0");
+  if (int rc = ce_prepare(c)) return rc;
   int64_t ch = (n + gsize - 1) / gsize;
   ch = (ch + kVec - 1) / kVec * kVec;
-  if (int rc = check_range(c, stage_off, ch * gsize * is, "fsdp_allreduce_ce(stage)")) return rc;
-  if (int rc = check_range(c, gather_off, ch * gsize * 4, "fsdp_allreduce_ce(gather)")) return rc;
-  if (int rc = ce_prepare(c)) return rc;
+  const bool direct = out_off >= 0;
+  const int64_t res_off = direct ? out_off : gather_off;   // where results land on every member
   CollParams p;
   fill_common(c, p, channel, gsize, gstride, n);
-  cudaStream_t s = (cudaStream_t)stream;
   if (int rc = launch(c, coll_enter_kernel, p, 1, 32, s)) return rc;
   const int start = gstride == 1 ? (c->rank / gsize) * gsize : c->rank % gstride;
   const int pos = gstride == 1 ? c->rank - start : c->rank / gstride;
@@ -2045,12 +2044,12 @@ extern "C" int fsdp_allreduce_ce(fsdp_comm_t* c, int channel, int gsize, int gst
   FSDP_LAUNCHED();
   coll_wait_slot_kernel<<<1, 32, 0, s>>>(p, 0);
   FSDP_LAUNCHED();
-  // 2. owner reduction of my chunk -> my slot of the gather buffer
+  // 2. owner reduction of my chunk -> my slot of the result buffer
   CeReduceArgs ra;
   ra.own = (const char*)in + (int64_t)pos * ch * is;
   ra.stage = mine + stage_off;
   ra.stride = ch;
-  ra.out = (float*)(mine + gather_off) + (int64_t)pos * ch;
+  ra.out = (float*)(mine + res_off) + (int64_t)pos * ch;
   ra.gsize = gsize; ra.pos = pos;
   ra.prediv = 1.0f; ra.postdiv = postdiv; ra.accumulate = 0; ra.store_raw = 1;
   if (int rc = launch_ce_reduce(ra, 0, clen(pos), src_dtype, c->ce_reduce_cap, s)) return rc;
@@ -2061,8 +2060,8 @@ extern "C" int fsdp_allreduce_ce(fsdp_comm_t* c, int channel, int gsize, int gst
   for (int jj = 0; jj + 1 < gsize; ++jj) {
     const int j = (pos + 1 + jj) % gsize;
     if (clen(pos) > 0)
-      FSDP_CUDA(cudaMemcpyAsync(c->bases[start + j * gstride] + gather_off + (int64_t)pos * ch * 4,
-                                mine + gather_off + (int64_t)pos * ch * 4, (size_t)(clen(pos) * 4),
+      FSDP_CUDA(cudaMemcpyAsync(c->bases[start + j * gstride] + res_off + (int64_t)pos * ch * 4,
+                                mine + res_off + (int64_t)pos * ch * 4, (size_t)(clen(pos) * 4),
                                 cudaMemcpyDeviceToDevice, cs));
   }
   coll_signal_slot_kernel<<<1, 32, 0, cs>>>(p, 1);
@@ -2072,12 +2071,47 @@ extern "C" int fsdp_allreduce_ce(fsdp_comm_t* c, int channel, int gsize, int gst
   coll_wait_slot_kernel<<<1, 32, 0, s>>>(p, 1);
   FSDP_LAUNCHED();
   if (c->timing) { FSDP_CUDA(cudaEventRecord(b, s)); c->timed[FSDP_KIND_AR].emplace_back(a, b); }
-  // 4. out = (accumulate ? out : 0) + gathered
-  const int grid = (int)std::min<int64_t>(std::max<int64_t>((n / 4 + 255) / 256, 1), (int64_t)kNumSMs * 4);
-  ar_epilogue_kernel<<<grid, 256, 0, s>>>((const float*)(mine + gather_off), out, n, accumulate ? 1 : 0);
-  FSDP_LAUNCHED();
-  FSDP_CUDA(cudaStreamWaitEvent(s, sent, 0));   // my input and gather slot are free once my copies are done
+  if (!direct) {
+    // 4. out = (accumulate ? out : 0) + gathered
+    const int grid = (int)std::min<int64_t>(std::max<int64_t>((n / 4 + 255) / 256, 1), (int64_t)kNumSMs * 4);
+    ar_epilogue_kernel<<<grid, 256, 0, s>>>((const float*)(mine + gather_off), out, n, accumulate ? 1 : 0);
+    FSDP_LAUNCHED();
+  }
+  FSDP_CUDA(cudaStreamWaitEvent(s, sent, 0));   // my input and result slot are free once my copies are done
   return 0;
+}
+
+extern "C" int fsdp_allreduce_ce(fsdp_comm_t* c, int channel, int gsize, int gstride, const void* in,
+                                 int src_dtype, int64_t n, int64_t stage_off, int64_t gather_off,
+                                 float* out, float postdiv, int accumulate, void* stream) {
+  if (int rc = validate_group(c, channel, gsize, gstride)) return rc;
+  if (c->emulated) return fail(FSDP_E_UNSUPPORTED, "copy-engine collectives need a real communicator");
+  const int is = elem_size(src_dtype);
+  if (n < 0 || !in || !out || !is) return fail(FSDP_E_INVALID, "fsdp_allreduce_ce: bad args");
+  if (!(postdiv > 0.f)) return fail(FSDP_E_INVALID, "postdiv must be > 0");
+  int64_t ch = (n + gsize - 1) / gsize;
+  ch = (ch + kVec - 1) / kVec * kVec;
+  if (int rc = check_range(c, stage_off, ch * gsize * is, "fsdp_allreduce_ce(stage)")) return rc;
+  if (int rc = check_range(c, gather_off, ch * gsize * 4, "fsdp_allreduce_ce(gather)")) return rc;
+  return allreduce_ce_impl(c, channel, gsize, gstride, in, src_dtype, n, stage_off, gather_off, out, -1,
+                           postdiv, accumulate, (cudaStream_t)stream);
+}
+
+extern "C" int fsdp_allreduce_ce_pool(fsdp_comm_t* c, int channel, int gsize, int gstride, const void* in,
+                                      int src_dtype, int64_t n, int64_t stage_off, int64_t out_off,
+                                      float postdiv, void* stream) {
+  if (int rc = validate_group(c, channel, gsize, gstride)) return rc;
+  if (c->emulated) return fail(FSDP_E_UNSUPPORTED, "copy-engine collectives need a real communicator");
+  const int is = elem_size(src_dtype);
+  if (n < 0 || !in || !is) return fail(FSDP_E_INVALID, "fsdp_allreduce_ce_pool: bad args");
+  if (!(postdiv > 0.f)) return fail(FSDP_E_INVALID, "postdiv must be > 0");
+  if (out_off % 16) return fail(FSDP_E_INVALID, "fsdp_allreduce_ce_pool: out region must be 16-byte aligned");
+  int64_t ch = (n + gsize - 1) / gsize;
+  ch = (ch + kVec - 1) / kVec * kVec;
+  if (int rc = check_range(c, stage_off, ch * gsize * is, "fsdp_allreduce_ce_pool(stage)")) return rc;
+  if (int rc = check_range(c, out_off, n * 4, "fsdp_allreduce_ce_pool(out)")) return rc;
+  return allreduce_ce_impl(c, channel, gsize, gstride, in, src_dtype, n, stage_off, -1,
+                           (float*)(c->bases[c->rank] + out_off), out_off, postdiv, 0, (cudaStream_t)stream);
 }
 
 extern "C" int fsdp_allreduce(fsdp_comm_t* c, int channel, int gsize, int gstride,

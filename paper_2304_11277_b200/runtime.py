@@ -368,13 +368,23 @@ class FSDPRuntime:
         total = max(cur, _ALIGN)
         f32 = dict(dtype=torch.float32, device=self.device)
         self.master = torch.zeros(total, **f32)
-        self.grad = torch.zeros(total, **f32)
+        self.grad_pool_off = None
+        if self._grad_in_pool(self.plan, self.cfg) and self.comm is not None:
+            # the reduced-gradient arena lives in the symmetric pool (same
+            # offset on every rank): the replica all-reduce writes every
+            # member's result straight into it (fsdp_allreduce_ce_pool)
+            self.grad_pool_off = self.comm.alloc(total * 4, 256)
+            self.grad = self.comm.view(self.grad_pool_off, total, torch.float32)
+            self.grad.zero_()
+        else:
+            self.grad = torch.zeros(total, **f32)
         self.exp_avg = torch.zeros(total, **f32) if self.cfg.optimizer == "adam" else None
         self.exp_avg_sq = torch.zeros(total, **f32) if self.cfg.optimizer == "adam" else None
         keep_low = self.cfg.mixed and not (self.cfg.fused_cast_ag and self.plan.shard_factor > 1)
         self.low = torch.zeros(total, dtype=torch.bfloat16, device=self.device) if keep_low else None
         self._resident_torch_bytes = sum(t.numel() * t.element_size() for t in
-                                         (self.master, self.grad, self.exp_avg, self.exp_avg_sq, self.low)
+                                         (self.master, None if self.grad_pool_off is not None else self.grad,
+                                          self.exp_avg, self.exp_avg_sq, self.low)
                                          if t is not None)
         for u, o in zip(self.units, offs):
             n = u.layout.shard_numel
@@ -447,6 +457,13 @@ class FSDPRuntime:
                 self.ar_stage_off = c.alloc(el * 4)
                 self.ar_gather_off = c.alloc(el * 4)
 
+    @staticmethod
+    def _grad_in_pool(plan: ShardingPlan, cfg: RuntimeConfig) -> bool:
+        """HYBRID / NO_SHARD on the ipc copy-engine path: the fp32 gradient
+        arena is a pool region so the all-reduce lands in it directly."""
+        return (plan.world_size > 1 and plan.shard_factor < plan.world_size and cfg.comm_backend == "ipc"
+                and cfg.rs_engine == "ce")
+
     def _ll_shard_max(self, units, F: int, es: int) -> int:
         """Largest shard length among units small enough for the LL path."""
         lim = self.cfg.ll_max_bytes
@@ -474,6 +491,9 @@ class FSDPRuntime:
             nslots = min(len(layouts), cfg.rate_limit + 3)
         total = reserved
         pad = lambda b: -(-b // 256) * 256 + 256  # noqa: E731
+        if FSDPRuntime._grad_in_pool(plan, cfg):
+            arena = sum(-(-l.shard_numel // _ALIGN) * _ALIGN for l in layouts)
+            total += pad(max(arena, _ALIGN) * 4)
         if F > 1:
             total += nslots * pad(psi_max * es) + 3 * pad(psi_max * ps)
             if W > 1 and cfg.ll_max_bytes > 0:
@@ -1039,9 +1059,16 @@ class FSDPRuntime:
     def _ar(self, inp: torch.Tensor, out: torch.Tensor, post: float, accumulate: bool,
             stream: torch.cuda.Stream | None = None) -> None:
         """All-reduce in the replicated group (hybrid stage 2 / NO_SHARD):
-        copy engines with rs_engine="ce", else the two-shot SM kernel."""
+        copy engines with rs_engine="ce", else the two-shot SM kernel.  A
+        first reduction into the pool-resident gradient arena lands in place
+        on every member (no gather buffer, no epilogue)."""
         s = stream if stream is not None else self.rs_stream
-        if self.cfg.rs_engine == "ce":
+        if (self.cfg.rs_engine == "ce" and not accumulate and self.grad_pool_off is not None
+                and out.untyped_storage().data_ptr() == self.grad.untyped_storage().data_ptr()):
+            off = self.grad_pool_off + (out.storage_offset() - self.grad.storage_offset()) * 4
+            self.comm.all_reduce_ce_pool(self.plan.replicated_desc, inp, self.ar_stage_off, off,
+                                         postdiv=post, stream=s)
+        elif self.cfg.rs_engine == "ce":
             self.comm.all_reduce_ce(self.plan.replicated_desc, inp, self.ar_stage_off, self.ar_gather_off,
                                     out, postdiv=post, accumulate=accumulate, stream=s)
         else:

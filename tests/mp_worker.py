@@ -84,6 +84,11 @@ def raw_collectives(rank, world, results):
         out_ce = torch.empty(n * world, device="cuda")
         comm.all_reduce_ce((world, 1), torch.from_numpy(grads[rank]).cuda(), a, b, out_ce, postdiv=float(world))
         check(out_ce.cpu().numpy().tobytes() == exp[rank].tobytes(), f"AR-CE n={n}")
+        # pool-resident output: written in place on every member, no epilogue
+        ob = comm.alloc(n * world * 4 + 256)
+        comm.all_reduce_ce_pool((world, 1), torch.from_numpy(grads[rank]).cuda(), a, ob, postdiv=float(world))
+        check(comm.view(ob, n * world, torch.float32).cpu().numpy().tobytes() == exp[rank].tobytes(),
+              f"AR-CE pool n={n}")
         acc_full = [g.standard_normal(n * world).astype(np.float32) for g in
                     [np.random.default_rng(7 * r + n) for r in range(world)]]
         out_ce = torch.from_numpy(acc_full[rank]).cuda()

@@ -33,6 +33,9 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# NCCL's own banner ("NCCL version ...", printed when NCCL_DEBUG is set) goes
+# to stderr: stdout carries exactly one JSON line
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 METRIC = "TFLOPS/GPU and step time at 1/2/4/8 B200; AG/RS bus GB/s vs 900 GB/s NVLink"
 # NVLink roofline denominators: nominal 900 GB/s per direction; measured peer

@@ -349,7 +349,9 @@ def run_ours(args):
             traffic = None
             try:
                 with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-                    t = json.load(fh).get(f"{dom}|{args.config}|{world}")
+                    gkey = "|bf16g" if getattr(rt, "_g_arena", None) is not None and \
+                        rt._g_arena.dtype == torch.bfloat16 else ""
+                    t = json.load(fh).get(f"{dom}|{args.config}|{world}{gkey}")
                 traffic = t["bytes"] if t else None
             except Exception:
                 traffic = None

@@ -102,6 +102,16 @@ int fsdp_adam_step(float* p, const float* g, float* m, float* v, int64_t n, floa
 int fsdp_sgd_step(float* p, const float* g, int64_t n, float lr, const float* skip_flag,
                   void* p_lowp, void* stream);
 
+/* The same two steps reading a bf16 gradient (W = 1: the write-back lands in
+ * a bf16 arena and the optimizer reads it directly, 2 B/elem less on each
+ * side).  bf16 -> fp32 is exact, so the result is bit-identical to running
+ * fsdp_adam_step / fsdp_sgd_step on the fp32 copy of the same gradient. */
+int fsdp_adam_step_bf16g(float* p, const void* g_bf16, float* m, float* v, int64_t n, float lr,
+                         float b1, float omb1, float b2, float omb2, float bc1, float bc2, float eps,
+                         const float* skip_flag, void* p_lowp, void* stream);
+int fsdp_sgd_step_bf16g(float* p, const void* g_bf16, int64_t n, float lr, const float* skip_flag,
+                        void* p_lowp, void* stream);
+
 /* ------------------------------------------------------------------------
  * Communicator: CUDA-IPC symmetric pool + SM-driven collectives over
  * NVLink/NVSwitch peer pointers                           (collectives.py)

@@ -57,6 +57,9 @@ _SIGS = {
     "fsdp_adam_step": (_i32, [_vp, _vp, _vp, _vp, _i64, _f32, _f32, _f32, _f32, _f32, _f32,
                               _f32, _f32, _vp, _vp, _vp]),
     "fsdp_sgd_step": (_i32, [_vp, _vp, _i64, _f32, _vp, _vp, _vp]),
+    "fsdp_adam_step_bf16g": (_i32, [_vp, _vp, _vp, _vp, _i64, _f32, _f32, _f32, _f32, _f32, _f32,
+                                    _f32, _f32, _vp, _vp, _vp]),
+    "fsdp_sgd_step_bf16g": (_i32, [_vp, _vp, _i64, _f32, _vp, _vp, _vp]),
     "fsdp_comm_create": (_i32, [_i32, _i32, _i64, _i32, C.POINTER(_vp)]),
     "fsdp_comm_create_emulated": (_i32, [_i32, _i64, _i32, C.POINTER(_vp)]),
     "fsdp_comm_ipc_handle": (_i32, [_vp, _vp]),

@@ -30,22 +30,33 @@ __device__ __forceinline__ void adam1(float& p, float g, float& m, float& v, con
   p = __fsub_rn(p, __fdiv_rn(__fmul_rn(s.lr, mh), den));
 }
 
+// 4 gradient elements as floats (bf16 -> fp32 is exact: same bits as an
+// fp32 gradient arena holding the bf16 write-back)
+__device__ __forceinline__ float4 ld_grad4(const float* g, int64_t i4) {
+  return __ldcs(reinterpret_cast<const float4*>(g) + i4);
+}
+__device__ __forceinline__ float4 ld_grad4(const __nv_bfloat16* g, int64_t i4) {
+  const uint2 r = __ldcs(reinterpret_cast<const uint2*>(g) + i4);
+  return make_float4(bf16lo(r.x), bf16hi(r.x), bf16lo(r.y), bf16hi(r.y));
+}
+
+template <typename G>
 __global__ void __launch_bounds__(kOptThreads)
-adam_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+adam_kernel(float* __restrict__ p, const G* __restrict__ g, float* __restrict__ m,
             float* __restrict__ v, int64_t n, AdamScalars s, const float* __restrict__ skip,
             __nv_bfloat16* __restrict__ plow) {
   if (skip != nullptr && *skip > 0.f) return;      // world verdict: skip step
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool vec = aligned16(p) && aligned16(g) && aligned16(m) && aligned16(v) &&
+  const bool vec = aligned16(p) && ((uintptr_t)g % (4 * sizeof(G)) == 0) && aligned16(m) && aligned16(v) &&
                    (plow == nullptr || aligned16(plow));
   int64_t done = 0;
   if (vec) {
     const int64_t n4 = n >> 2;
-    float4* p4 = (float4*)p; const float4* g4 = (const float4*)g;
+    float4* p4 = (float4*)p;
     float4* m4 = (float4*)m; float4* v4 = (float4*)v;
     for (int64_t i = tid; i < n4; i += stride) {
-      float4 pp = p4[i], gg = __ldcs(g4 + i), mm = m4[i], vv = v4[i];
+      float4 pp = p4[i], gg = ld_grad4(g, i), mm = m4[i], vv = v4[i];
       adam1(pp.x, gg.x, mm.x, vv.x, s); adam1(pp.y, gg.y, mm.y, vv.y, s);
       adam1(pp.z, gg.z, mm.z, vv.z, s); adam1(pp.w, gg.w, mm.w, vv.w, s);
       p4[i] = pp; __stcs(m4 + i, mm); __stcs(v4 + i, vv);
@@ -58,7 +69,7 @@ adam_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restric
   }
   for (int64_t i = done + tid; i < n; i += stride) {
     float pp = p[i], mm = m[i], vv = v[i];
-    adam1(pp, g[i], mm, vv, s);
+    adam1(pp, to_f<G>(g[i]), mm, vv, s);
     p[i] = pp; m[i] = mm; v[i] = vv;
     if (plow) plow[i] = __float2bfloat16_rn(pp);
   }
@@ -71,17 +82,17 @@ adam_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restric
 // on their float4s of the landed stage and store p, m, v (+ bf16 copy)
 // straight from registers.  Persistent grid (ctas_per_sm CTAs per SM).  Same
 // bits as adam_kernel.
-template <int TILE, int STAGES, bool CONTIG, int THREADS>
+template <int TILE, int STAGES, bool CONTIG, int THREADS, typename G = float>
 __global__ void __launch_bounds__(THREADS)
-adam_tma_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+adam_tma_kernel(float* __restrict__ p, const G* __restrict__ g, float* __restrict__ m,
                 float* __restrict__ v, int64_t n, AdamScalars s, const float* __restrict__ skip,
                 __nv_bfloat16* __restrict__ plow) {
-  constexpr int kStageBytes = 4 * TILE * 4;           // p, g, m, v
+  // stage = [p fp32 | m fp32 | v fp32 | g G] tiles
+  constexpr int kStageBytes = TILE * (12 + (int)sizeof(G));
   constexpr int kPer = TILE / THREADS;                // elements per thread per stage (multiple of 4)
   static_assert(kPer % 4 == 0, "tile must give every thread whole float4s");
   if (skip != nullptr && *skip > 0.f) return;
   extern __shared__ __align__(128) unsigned char smem[];
-  float* ring = reinterpret_cast<float*>(smem);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStageBytes);
   const int64_t ntiles = n / TILE;                    // full tiles; the tail is scalar
   // CONTIG: CTA b streams the contiguous tile range [b*T/G, (b+1)*T/G);
@@ -98,28 +109,34 @@ adam_tma_kernel(float* __restrict__ p, const float* __restrict__ g, float* __res
   auto issue = [&](int64_t k) {
     const int st = (int)(k % STAGES);
     const int64_t e0 = tile_of(k) * (int64_t)TILE;
-    float* base = ring + st * (4 * TILE);
+    float* base = reinterpret_cast<float*>(smem + (size_t)st * kStageBytes);
     mbar_expect_tx(&full[st], kStageBytes);
     tma_load_1d(base, p + e0, TILE * 4, &full[st]);
-    tma_load_1d(base + TILE, g + e0, TILE * 4, &full[st]);
-    tma_load_1d(base + 2 * TILE, m + e0, TILE * 4, &full[st]);
-    tma_load_1d(base + 3 * TILE, v + e0, TILE * 4, &full[st]);
+    tma_load_1d(base + TILE, m + e0, TILE * 4, &full[st]);
+    tma_load_1d(base + 2 * TILE, v + e0, TILE * 4, &full[st]);
+    tma_load_1d(base + 3 * TILE, g + e0, TILE * (int)sizeof(G), &full[st]);
   };
   if (threadIdx.x == 0)
     for (int64_t k = 0; k < mine && k < STAGES; ++k) issue(k);
   for (int64_t k = 0; k < mine; ++k) {
     const int st = (int)(k % STAGES);
     mbar_wait(&full[st], (uint32_t)((k / STAGES) & 1));
-    const float* base = ring + st * (4 * TILE);
+    const float* base = reinterpret_cast<const float*>(smem + (size_t)st * kStageBytes);
+    const G* gbase = reinterpret_cast<const G*>(base + 3 * TILE);
     const int64_t e0 = tile_of(k) * (int64_t)TILE;
     float4 pp[kPer / 4], gg[kPer / 4], mm[kPer / 4], vv[kPer / 4];
 #pragma unroll
     for (int q = 0; q < kPer / 4; ++q) {               // warp-contiguous float4s
       const int i = (q * THREADS + threadIdx.x) * 4;
       pp[q] = *reinterpret_cast<const float4*>(base + i);
-      gg[q] = *reinterpret_cast<const float4*>(base + TILE + i);
-      mm[q] = *reinterpret_cast<const float4*>(base + 2 * TILE + i);
-      vv[q] = *reinterpret_cast<const float4*>(base + 3 * TILE + i);
+      mm[q] = *reinterpret_cast<const float4*>(base + TILE + i);
+      vv[q] = *reinterpret_cast<const float4*>(base + 2 * TILE + i);
+      if constexpr (sizeof(G) == 4) {
+        gg[q] = *reinterpret_cast<const float4*>(gbase + i);
+      } else {
+        const uint2 r = *reinterpret_cast<const uint2*>(gbase + i);
+        gg[q] = make_float4(bf16lo(r.x), bf16hi(r.x), bf16lo(r.y), bf16hi(r.y));
+      }
     }
     __syncthreads();                                  // stage st fully read: refill it
     if (threadIdx.x == 0 && k + STAGES < mine) {
@@ -145,7 +162,7 @@ adam_tma_kernel(float* __restrict__ p, const float* __restrict__ g, float* __res
   for (int64_t i = t0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     float pp = p[i], mm = m[i], vv = v[i];
-    adam1(pp, g[i], mm, vv, s);
+    adam1(pp, to_f<G>(g[i]), mm, vv, s);
     p[i] = pp; m[i] = mm; v[i] = vv;
     if (plow) plow[i] = __float2bfloat16_rn(pp);
   }
@@ -155,6 +172,7 @@ adam_tma_kernel(float* __restrict__ p, const float* __restrict__ g, float* __res
 struct AdamVariant {
   void* fn;
   int tile, stages, ctas_per_sm, threads;
+  void* fn_bf16g;                 // same geometry, bf16 gradient (W = 1 write-back arena)
 };
 // Measured on the GPT-1.3B arena at N=1 (1.32 G elements; tools/adam_bench.py
 // standalone, bench.py FSDP_ADAM_VARIANT=k in-step; profiles/r1/adam/).
@@ -166,19 +184,24 @@ struct AdamVariant {
 // divides + a sqrt per element) needs warps to hide its latency: 256-thread
 // CTAs drop to 0.78 there, 768-thread CTAs give 0.906 (first version 0.895).
 static const AdamVariant kAdamVariants[] = {
-    {(void*)adam_tma_kernel<6144, 2, true, 768>, 6144, 2, 1, 768},    // 0 (default)
-    {(void*)adam_tma_kernel<6144, 2, true, 256>, 6144, 2, 1, 256},    // 1: best standalone
-    {(void*)adam_tma_kernel<1024, 4, false, 256>, 1024, 4, 3, 256},   // 2: the first version
-    {(void*)adam_tma_kernel<4096, 3, true, 1024>, 4096, 3, 1, 1024},  // 3
+    {(void*)adam_tma_kernel<6144, 2, true, 768>, 6144, 2, 1, 768,
+     (void*)adam_tma_kernel<6144, 2, true, 768, __nv_bfloat16>},     // 0 (default)
+    {(void*)adam_tma_kernel<6144, 2, true, 256>, 6144, 2, 1, 256,
+     (void*)adam_tma_kernel<6144, 2, true, 256, __nv_bfloat16>},     // 1: best standalone
+    {(void*)adam_tma_kernel<1024, 4, false, 256>, 1024, 4, 3, 256,
+     (void*)adam_tma_kernel<1024, 4, false, 256, __nv_bfloat16>},    // 2: the first version
+    {(void*)adam_tma_kernel<4096, 3, true, 1024>, 4096, 3, 1, 1024,
+     (void*)adam_tma_kernel<4096, 3, true, 1024, __nv_bfloat16>},    // 3
 };
 
+template <typename G>
 __global__ void __launch_bounds__(kOptThreads)
-sgd_kernel(float* __restrict__ p, const float* __restrict__ g, int64_t n, float lr,
+sgd_kernel(float* __restrict__ p, const G* __restrict__ g, int64_t n, float lr,
            const float* __restrict__ skip, __nv_bfloat16* __restrict__ plow) {
   if (skip != nullptr && *skip > 0.f) return;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const float pp = __fsub_rn(p[i], __fmul_rn(lr, g[i]));   // param -= lr * grad
+    const float pp = __fsub_rn(p[i], __fmul_rn(lr, to_f<G>(g[i])));   // param -= lr * grad
     p[i] = pp;
     if (plow) plow[i] = __float2bfloat16_rn(pp);
   }
@@ -212,13 +235,8 @@ static int opt_grid(int64_t n) {
 
 using namespace fsdp;
 
-extern "C" int fsdp_adam_step(float* p, const float* g, float* m, float* v, int64_t n, float lr,
-                              float b1, float omb1, float b2, float omb2, float bc1, float bc2,
-                              float eps, const float* skip_flag, void* p_lowp, void* stream) {
-  if (n < 0) return fail(FSDP_E_INVALID, "fsdp_adam_step: negative n");
-  if (n == 0) return 0;
-  if (!p || !g || !m || !v) return fail(FSDP_E_INVALID, "fsdp_adam_step: null buffer");
-  AdamScalars s{lr, b1, omb1, b2, omb2, bc1, bc2, eps};
+static int adam_launch(float* p, const void* g, int g_bf16, float* m, float* v, int64_t n,
+                       const AdamScalars& s, const float* skip_flag, void* p_lowp, cudaStream_t stream) {
   static int use_tma = -1;      // FSDP_ADAM_TMA=0 selects the register-streaming kernel
   static int var = 0;
   if (use_tma < 0) {
@@ -227,34 +245,71 @@ extern "C" int fsdp_adam_step(float* p, const float* g, float* m, float* v, int6
     if (const char* ev = getenv("FSDP_ADAM_VARIANT"))
       var = std::max(0, std::min((int)(sizeof(kAdamVariants) / sizeof(kAdamVariants[0])) - 1, atoi(ev)));
     const AdamVariant& av = kAdamVariants[var];
-    if (use_tma && cudaFuncSetAttribute(av.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        av.stages * 16 * av.tile + 64) != cudaSuccess)
+    if (use_tma && (cudaFuncSetAttribute(av.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         av.stages * 16 * av.tile + 64) != cudaSuccess ||
+                    cudaFuncSetAttribute(av.fn_bf16g, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         av.stages * 14 * av.tile + 64) != cudaSuccess))
       use_tma = 0;
   }
   const AdamVariant& av = kAdamVariants[var];
+  const size_t gs = g_bf16 ? 2 : 4;
   const bool al = aligned16(p) && aligned16(g) && aligned16(m) && aligned16(v) &&
                   (p_lowp == nullptr || ((uintptr_t)p_lowp & 7) == 0);
   if (use_tma && al && n >= (int64_t)av.tile * kNumSMs) {
     const int64_t tiles = n / av.tile;
     const int grid = (int)std::min<int64_t>(tiles, (int64_t)kNumSMs * av.ctas_per_sm);
     __nv_bfloat16* pl = (__nv_bfloat16*)p_lowp;
-    void* args[] = {&p, &g, &m, &v, &n, &s, &skip_flag, &pl};
-    FSDP_CUDA(cudaLaunchKernel(av.fn, dim3(grid), dim3(av.threads), args,
-                               (size_t)av.stages * 16 * av.tile + 64, (cudaStream_t)stream));
+    AdamScalars sc = s;
+    void* args[] = {&p, (void*)&g, &m, &v, &n, &sc, (void*)&skip_flag, &pl};
+    FSDP_CUDA(cudaLaunchKernel(g_bf16 ? av.fn_bf16g : av.fn, dim3(grid), dim3(av.threads), args,
+                               (size_t)av.stages * (12 + gs) * av.tile + 64, stream));
+  } else if (g_bf16) {
+    adam_kernel<__nv_bfloat16><<<opt_grid(n), kOptThreads, 0, stream>>>(
+        p, (const __nv_bfloat16*)g, m, v, n, s, skip_flag, (__nv_bfloat16*)p_lowp);
   } else {
-    adam_kernel<<<opt_grid(n), kOptThreads, 0, (cudaStream_t)stream>>>(
-        p, g, m, v, n, s, skip_flag, (__nv_bfloat16*)p_lowp);
+    adam_kernel<float><<<opt_grid(n), kOptThreads, 0, stream>>>(
+        p, (const float*)g, m, v, n, s, skip_flag, (__nv_bfloat16*)p_lowp);
   }
   FSDP_LAUNCHED();
   return 0;
+}
+
+extern "C" int fsdp_adam_step(float* p, const float* g, float* m, float* v, int64_t n, float lr,
+                              float b1, float omb1, float b2, float omb2, float bc1, float bc2,
+                              float eps, const float* skip_flag, void* p_lowp, void* stream) {
+  if (n < 0) return fail(FSDP_E_INVALID, "fsdp_adam_step: negative n");
+  if (n == 0) return 0;
+  if (!p || !g || !m || !v) return fail(FSDP_E_INVALID, "fsdp_adam_step: null buffer");
+  AdamScalars s{lr, b1, omb1, b2, omb2, bc1, bc2, eps};
+  return adam_launch(p, g, 0, m, v, n, s, skip_flag, p_lowp, (cudaStream_t)stream);
+}
+
+extern "C" int fsdp_adam_step_bf16g(float* p, const void* g_bf16, float* m, float* v, int64_t n, float lr,
+                                    float b1, float omb1, float b2, float omb2, float bc1, float bc2,
+                                    float eps, const float* skip_flag, void* p_lowp, void* stream) {
+  if (n < 0) return fail(FSDP_E_INVALID, "fsdp_adam_step_bf16g: negative n");
+  if (n == 0) return 0;
+  if (!p || !g_bf16 || !m || !v) return fail(FSDP_E_INVALID, "fsdp_adam_step_bf16g: null buffer");
+  AdamScalars s{lr, b1, omb1, b2, omb2, bc1, bc2, eps};
+  return adam_launch(p, g_bf16, 1, m, v, n, s, skip_flag, p_lowp, (cudaStream_t)stream);
 }
 
 extern "C" int fsdp_sgd_step(float* p, const float* g, int64_t n, float lr, const float* skip_flag,
                              void* p_lowp, void* stream) {
   if (n < 0) return fail(FSDP_E_INVALID, "fsdp_sgd_step: negative n");
   if (n == 0) return 0;
-  sgd_kernel<<<opt_grid(n), kOptThreads, 0, (cudaStream_t)stream>>>(p, g, n, lr, skip_flag,
-                                                                    (__nv_bfloat16*)p_lowp);
+  sgd_kernel<float><<<opt_grid(n), kOptThreads, 0, (cudaStream_t)stream>>>(p, g, n, lr, skip_flag,
+                                                                           (__nv_bfloat16*)p_lowp);
+  FSDP_LAUNCHED();
+  return 0;
+}
+
+extern "C" int fsdp_sgd_step_bf16g(float* p, const void* g_bf16, int64_t n, float lr, const float* skip_flag,
+                                   void* p_lowp, void* stream) {
+  if (n < 0) return fail(FSDP_E_INVALID, "fsdp_sgd_step_bf16g: negative n");
+  if (n == 0) return 0;
+  sgd_kernel<__nv_bfloat16><<<opt_grid(n), kOptThreads, 0, (cudaStream_t)stream>>>(
+      p, (const __nv_bfloat16*)g_bf16, n, lr, skip_flag, (__nv_bfloat16*)p_lowp);
   FSDP_LAUNCHED();
   return 0;
 }

@@ -103,10 +103,12 @@ def adam_step(p: torch.Tensor, g: torch.Tensor, m: torch.Tensor, v: torch.Tensor
               p_lowp: torch.Tensor | None = None, stream=None) -> None:
     for x in (p, g, m, v):
         _cuda(x, "adam_step")
-        if x.dtype != torch.float32 or x.numel() != p.numel():
-            raise ValueError("adam_step: param/grad/state must be fp32 of equal length")
+        if x.numel() != p.numel() or x.dtype != (torch.float32 if (x is not g or g.dtype != torch.bfloat16)
+                                                 else torch.bfloat16):
+            raise ValueError("adam_step: param/state fp32 and grad fp32 or bf16, of equal length")
     s = adam_scalars(lr, betas, eps, t)
-    check(lib.fsdp_adam_step(p.data_ptr(), g.data_ptr(), m.data_ptr(), v.data_ptr(), p.numel(),
+    fn = lib.fsdp_adam_step_bf16g if g.dtype == torch.bfloat16 else lib.fsdp_adam_step
+    check(fn(p.data_ptr(), g.data_ptr(), m.data_ptr(), v.data_ptr(), p.numel(),
                              *s, skip_flag.data_ptr() if skip_flag is not None else None,
                              p_lowp.data_ptr() if p_lowp is not None else None,
                              stream_ptr(stream)), "adam_step")
@@ -116,7 +118,10 @@ def sgd_step(p: torch.Tensor, g: torch.Tensor, *, lr: float, skip_flag=None, p_l
              stream=None) -> None:
     _cuda(p, "sgd_step")
     _cuda(g, "sgd_step")
-    check(lib.fsdp_sgd_step(p.data_ptr(), g.data_ptr(), p.numel(), _f32(lr),
+    if g.dtype not in (torch.float32, torch.bfloat16) or g.numel() != p.numel():
+        raise ValueError("sgd_step: grad must be fp32 or bf16 of the param's length")
+    fn = lib.fsdp_sgd_step_bf16g if g.dtype == torch.bfloat16 else lib.fsdp_sgd_step
+    check(fn(p.data_ptr(), g.data_ptr(), p.numel(), _f32(lr),
                             skip_flag.data_ptr() if skip_flag is not None else None,
                             p_lowp.data_ptr() if p_lowp is not None else None,
                             stream_ptr(stream)), "sgd_step")

@@ -123,6 +123,12 @@ class RuntimeConfig:
     # all-gathers wait only for it and overlap the launch over the rest of
     # the arena (0 = one launch).  Same arithmetic, elementwise.
     opt_split_first: int = 2
+    # world of one, bf16 payload: the fused write-back lands in a bf16 grad
+    # arena and the optimizer reads bf16 gradients (bf16 -> fp32 is exact,
+    # so the update is bit-identical); 2 B/elem less written by the
+    # write-back and read by Adam.  A second reduction of a unit in the same
+    # step (accumulation), the loss scaler or no_sync() continue in fp32.
+    w1_bf16_grad: bool = True
     # the north star's fused path: gather the fp32 master shard with the
     # fp32 -> bf16 cast fused into the all-gather kernel (SM push / NVLS / LL),
     # instead of gathering the bf16 copy Adam's epilogue writes (copy
@@ -180,6 +186,8 @@ class UnitState:
         self.reduces_this_step = 0
         self.bwd_done = False
         self.stepped = False           # optimizer already applied this step (in backward)
+        self.grad_low: torch.Tensor | None = None   # W = 1 bf16 reduced-gradient slice
+        self.grad_is_low = False       # this step's reduced gradient is (only) in grad_low
 
 
 class SlotPool:
@@ -382,9 +390,12 @@ class FSDPRuntime:
         self.exp_avg_sq = torch.zeros(total, **f32) if self.cfg.optimizer == "adam" else None
         keep_low = self.cfg.mixed and not (self.cfg.fused_cast_ag and self.plan.shard_factor > 1)
         self.low = torch.zeros(total, dtype=torch.bfloat16, device=self.device) if keep_low else None
+        w1_low = (self.cfg.w1_bf16_grad and self.plan.world_size == 1 and self.cfg.mixed
+                  and self.cfg.reduce_in_low)
+        self.grad_low = torch.zeros(total, dtype=torch.bfloat16, device=self.device) if w1_low else None
         self._resident_torch_bytes = sum(t.numel() * t.element_size() for t in
                                          (self.master, None if self.grad_pool_off is not None else self.grad,
-                                          self.exp_avg, self.exp_avg_sq, self.low)
+                                          self.exp_avg, self.exp_avg_sq, self.low, self.grad_low)
                                          if t is not None)
         for u, o in zip(self.units, offs):
             n = u.layout.shard_numel
@@ -399,6 +410,8 @@ class FSDPRuntime:
                 u.exp_avg_sq = self.exp_avg_sq[o:o + n]
             if self.low is not None:
                 u.low = self.low[o:o + n]
+            if self.grad_low is not None:
+                u.grad_low = self.grad_low[o:o + n]
 
     def _alloc_pool_regions(self) -> None:
         W, F = self.plan.world_size, self.plan.shard_factor
@@ -831,6 +844,7 @@ class FSDPRuntime:
         for u in self.units:
             u.reduces_this_step = 0
             u.stepped = False
+            u.grad_is_low = False
         self.micro_index = 0
 
     def _step_in_backward(self) -> bool:
@@ -868,21 +882,35 @@ class FSDPRuntime:
             raise DeadlockError("the communicator was aborted (a cross-GPU collective wait timed out); "
                                 "no optimizer update was applied after the abort")
 
+    def _grad_to_fp32(self, u: UnitState, stream: torch.cuda.Stream) -> None:
+        """Move a unit's bf16-only reduced gradient into the fp32 arena (exact)
+        before anything accumulates onto it or reads it as fp32."""
+        if u.grad_is_low:
+            kernels.cast(u.grad_low, u.grad, stream=stream)
+            u.grad_is_low = False
+
+    def reduced_grad(self, uid: int) -> torch.Tensor:
+        """The unit's reduced fp32 gradient shard of this step (a copy when it
+        lives in the bf16 arena)."""
+        u = self.units[uid]
+        return u.grad_low.float() if u.grad_is_low else u.grad
+
     def _step_unit(self, uid: int, stream: torch.cuda.Stream) -> None:
         """Optimizer on one unit's shard slice (same arithmetic as the arena
         launch, t = the step about to be taken)."""
         u = self.units[uid]
         cfg = self.cfg
         n = u.layout.shard_numel
+        g = u.grad_low if u.grad_is_low else u.grad
         skip = self._abort_skip(stream)
         with self.timed(cfg.optimizer + "_step", stream, n * (28 if cfg.optimizer == "adam" else 12)
                         + (2 * n if u.low is not None else 0)):
             if cfg.optimizer == "adam":
-                kernels.adam_step(u.master, u.grad, u.exp_avg, u.exp_avg_sq, lr=cfg.lr,
+                kernels.adam_step(u.master, g, u.exp_avg, u.exp_avg_sq, lr=cfg.lr,
                                   betas=cfg.betas, eps=cfg.eps, t=self.adam_steps + 1,
                                   skip_flag=skip, p_lowp=u.low, stream=stream)
             else:
-                kernels.sgd_step(u.master, u.grad, lr=cfg.lr, skip_flag=skip, p_lowp=u.low, stream=stream)
+                kernels.sgd_step(u.master, g, lr=cfg.lr, skip_flag=skip, p_lowp=u.low, stream=stream)
         u.stepped = True
 
     def begin_micro(self, final: bool) -> None:
@@ -963,12 +991,18 @@ class FSDPRuntime:
                 and u.accum_unsharded is None and not injected
                 and self.cfg.gradient_predivide == 1.0):
             # world of one: the write-back and the (identity) reduction fuse into
-            # one flatten straight into the fp32 grad shard, accumulating over
-            # micro-batches (engine.py:527-535 + :817-820 with W = 1)
+            # one flatten straight into the grad shard, accumulating over
+            # micro-batches (engine.py:527-535 + :817-820 with W = 1); the
+            # first reduction of a step lands in the bf16 arena when there is one
+            low = u.grad_low is not None and u.reduces_this_step == 0 and gdt == torch.bfloat16
+            if not low:
+                self._grad_to_fp32(u, self.compute_stream)
+            dst = u.grad_low if low else u.grad
             with self.timed("flatten_grad", self.compute_stream,
-                            sum(g.numel() for g in srcs if g is not None) * (gdt.itemsize + 4)):
-                kernels.flatten(srcs, lay.offsets, u.grad, accumulate=u.reduces_this_step > 0,
+                            sum(g.numel() for g in srcs if g is not None) * (gdt.itemsize + dst.element_size())):
+                kernels.flatten(srcs, lay.offsets, dst, accumulate=u.reduces_this_step > 0,
                                 stream=self.compute_stream)
+            u.grad_is_low = low
             u.reduces_this_step += 1
             u.grad_pending -= 1
             self._finalize(uid, reduced=True)
@@ -1121,6 +1155,7 @@ class FSDPRuntime:
                 pass
             elif W == 1:
                 # world of one: the "reduction" is the fp32 cast (+ accumulate)
+                self._grad_to_fp32(u, self.rs_stream)
                 with self.timed("reduce_w1", self.rs_stream, n * (payload.element_size() + 4)):
                     kernels.flatten([payload], [0], u.grad, accumulate=accumulate,
                                     stream=self.rs_stream)
@@ -1208,6 +1243,13 @@ class FSDPRuntime:
         by an earlier step's fold raises DeadlockError here; this step's own
         launch is skipped on device if the error word is set by then."""
         self.raise_if_aborted()
+        # W = 1 bf16 gradient arena: used when every visited unit's reduced
+        # gradient lives only there (one reduction this step) and no scaler
+        # has to unscale it in fp32
+        low_arena = (self.grad_low is not None and scale is None
+                     and any(u.grad_is_low for u in self.units)
+                     and all(u.grad_is_low or (u.reduces_this_step == 0 and not u.stepped)
+                             for u in self.units))
         for u in self.units:          # gathered copies would be stale after the update
             if u.unsharded is not None:
                 if u.pending:
@@ -1220,7 +1262,10 @@ class FSDPRuntime:
                 # never a stale one from an earlier step
                 self.compute_stream.wait_stream(self.rs_stream)
                 self.compute_stream.wait_stream(self.ar_stream)
-                u.grad.zero_()
+                (u.grad_low if low_arena else u.grad).zero_()
+            elif not low_arena:
+                self._grad_to_fp32(u, self.compute_stream)
+        self._g_arena = self.grad_low if low_arena else self.grad
         skip = None
         if scale is not None:
             self.found_inf.zero_()
@@ -1255,10 +1300,10 @@ class FSDPRuntime:
             raise EngineError("optimizer_in_backward stepped only part of the units; "
                               "every backward must be followed by an optimizer step")
         n = self.master.numel()
-        if cfg.optimizer == "adam":
-            nb = n * (28 + (2 if self.low is not None else 0))
-        else:
-            nb = n * (12 + (2 if self.low is not None else 0))
+        gs = self._g_arena.element_size()
+        lw = 2 if self.low is not None else 0
+        # algorithmic bytes: Adam reads p, g, m, v and writes p, m, v (+ bf16 p); SGD p, g -> p (+ bf16 p)
+        nb = n * ((24 + gs + lw) if cfg.optimizer == "adam" else (8 + gs + lw))
         k = self._early_prefix_units()
         t = self._adam_t(skip) if cfg.optimizer == "adam" else 0
         self.opt_early, self.opt_early_units = None, 0
@@ -1292,11 +1337,12 @@ class FSDPRuntime:
         """One optimizer launch over arena elements [a, b)."""
         cfg = self.cfg
         low = self.low[a:b] if self.low is not None else None
+        g = self._g_arena[a:b]
         if cfg.optimizer == "adam":
-            kernels.adam_step(self.master[a:b], self.grad[a:b], self.exp_avg[a:b], self.exp_avg_sq[a:b],
+            kernels.adam_step(self.master[a:b], g, self.exp_avg[a:b], self.exp_avg_sq[a:b],
                               lr=cfg.lr, betas=cfg.betas, eps=cfg.eps, t=t, skip_flag=skip, p_lowp=low)
         else:
-            kernels.sgd_step(self.master[a:b], self.grad[a:b], lr=cfg.lr, skip_flag=skip, p_lowp=low)
+            kernels.sgd_step(self.master[a:b], g, lr=cfg.lr, skip_flag=skip, p_lowp=low)
 
     def _adam_t(self, skip) -> int:
         # Adam's t counts TAKEN steps (numerics.py:276).  A skipped step is

@@ -131,6 +131,32 @@ def test_adam_large_with_lowp_and_skip(K, n):
     assert torch.equal(p, before)
 
 
+@pytest.mark.parametrize("n", [1000, (1 << 20) + 3, 6144 * 148 * 2 + 6144 * 5 + 11])
+def test_adam_bf16_grad_matches_fp32_grad(K, n):
+    """The W = 1 bf16-gradient optimizer (fsdp_adam_step_bf16g /
+    fsdp_sgd_step_bf16g) against the fp32-gradient kernels on the exact fp32
+    copy of the same bf16 gradient, and against the oracle: bit-identical for
+    the register kernel (small n) and the TMA kernel (+ scalar tail)."""
+    rng = np.random.default_rng(7 + n)
+    p0 = rng.standard_normal(n).astype(np.float32)
+    g16 = torch.from_numpy((rng.standard_normal(n) * 1e-2).astype(np.float32)).to(torch.bfloat16).cuda()
+    g32 = g16.float()
+    pa, pb = torch.from_numpy(p0).cuda(), torch.from_numpy(p0).cuda()
+    ma, va, mb, vb = (torch.zeros(n, device="cuda") for _ in range(4))
+    la = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+    lb = torch.empty_like(la)
+    pe, st = p0.copy(), sp.adam_init(n, np.float32)
+    for t in (1, 2):
+        K.adam_step(pa, g16, ma, va, lr=1e-3, betas=(0.9, 0.999), eps=1e-8, t=t, p_lowp=la)
+        K.adam_step(pb, g32, mb, vb, lr=1e-3, betas=(0.9, 0.999), eps=1e-8, t=t, p_lowp=lb)
+        sp.adam_step(pe, g32.cpu().numpy(), st, lr=1e-3)
+        assert torch.equal(pa, pb) and torch.equal(ma, mb) and torch.equal(va, vb) and torch.equal(la, lb)
+        assert pa.cpu().numpy().tobytes() == pe.tobytes()
+    K.sgd_step(pa, g16, lr=0.03125)
+    K.sgd_step(pb, g32, lr=0.03125)
+    assert torch.equal(pa, pb)
+
+
 def test_sgd_golden(K, golden):
     arrays, _ = golden
     p = torch.from_numpy(arrays["sgd/p0"].copy()).cuda()

@@ -41,14 +41,17 @@ def test_wrapped_step_matches_unwrapped_and_oracle():
     lref.backward()
     assert loss.item() == lref.item()
     before = [u.master.clone() for u in m.rt.units]
-    for lay, u in zip(m.layouts, m.rt.units):
+    grads = [m.rt.reduced_grad(i).clone() for i in range(len(m.rt.units))]
+    # W = 1 bf16 payload: the reduced gradient lives in the bf16 arena (exact)
+    assert all(u.grad_is_low for u in m.rt.units)
+    for lay, g in zip(m.layouts, grads):
         exp = flat_grads_of(ref, lay)
-        assert np.array_equal(u.grad.cpu().numpy(), exp), f"unit {lay.unit_id} grad"
+        assert np.array_equal(g.cpu().numpy(), exp), f"unit {lay.unit_id} grad"
     m.optimizer(lr=1e-3).step()
     torch.cuda.synchronize()
-    for b, u in zip(before, m.rt.units):
+    for b, g, u in zip(before, grads, m.rt.units):
         p = b.cpu().numpy().copy()
-        sp.adam_step(p, u.grad.cpu().numpy(), sp.adam_init(p.size, np.float32), lr=1e-3)
+        sp.adam_step(p, g.cpu().numpy(), sp.adam_init(p.size, np.float32), lr=1e-3)
         assert u.master.cpu().numpy().tobytes() == p.tobytes()
         assert torch.equal(u.low, u.master.to(torch.bfloat16))
 

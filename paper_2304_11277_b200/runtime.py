@@ -129,6 +129,9 @@ class RuntimeConfig:
     # write-back and read by Adam.  A second reduction of a unit in the same
     # step (accumulation), the loss scaler or no_sync() continue in fp32.
     w1_bf16_grad: bool = True
+    # HYBRID / NO_SHARD: keep the fp32 gradient arena in the symmetric pool so
+    # the replica all-reduce lands in place (fsdp_allreduce_ce_pool)
+    ar_in_pool: bool = True
     # the north star's fused path: gather the fp32 master shard with the
     # fp32 -> bf16 cast fused into the all-gather kernel (SM push / NVLS / LL),
     # instead of gathering the bf16 copy Adam's epilogue writes (copy
@@ -474,8 +477,8 @@ class FSDPRuntime:
     def _grad_in_pool(plan: ShardingPlan, cfg: RuntimeConfig) -> bool:
         """HYBRID / NO_SHARD on the ipc copy-engine path: the fp32 gradient
         arena is a pool region so the all-reduce lands in it directly."""
-        return (plan.world_size > 1 and plan.shard_factor < plan.world_size and cfg.comm_backend == "ipc"
-                and cfg.rs_engine == "ce")
+        return (cfg.ar_in_pool and plan.world_size > 1 and plan.shard_factor < plan.world_size
+                and cfg.comm_backend == "ipc" and cfg.rs_engine == "ce")
 
     def _ll_shard_max(self, units, F: int, es: int) -> int:
         """Largest shard length among units small enough for the LL path."""

@@ -5,7 +5,7 @@ push the same bf16 shard to each peer in turn (serial staggered), plus its
 own chunk as a local copy.  Whether the W-1 re-reads of the shard hit L2 or
 DRAM shows in GPU 0's dram__bytes_read.
 
-    ncu --replay-mode range --profile-from-start off \\
+    ncu --replay-mode range \\
         --metrics dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum \\
         python tools/ncu_dma_range.py [shard_mb]
 """

@@ -172,7 +172,8 @@ adam_tma_kernel(float* __restrict__ p, const G* __restrict__ g, float* __restric
 struct AdamVariant {
   void* fn;
   int tile, stages, ctas_per_sm, threads;
-  void* fn_bf16g;                 // same geometry, bf16 gradient (W = 1 write-back arena)
+  void* fn_bf16g;                 // bf16 gradient (W = 1 write-back arena), with its own
+  int stages_bf16g, tile_bf16g;   // ring (14 B/elem stages fit deeper rings)
 };
 // Measured on the GPT-1.3B arena at N=1 (1.32 G elements; tools/adam_bench.py
 // standalone, bench.py FSDP_ADAM_VARIANT=k in-step; profiles/r1/adam/).
@@ -185,13 +186,17 @@ struct AdamVariant {
 // CTAs drop to 0.78 there, 768-thread CTAs give 0.906 (first version 0.895).
 static const AdamVariant kAdamVariants[] = {
     {(void*)adam_tma_kernel<6144, 2, true, 768>, 6144, 2, 1, 768,
-     (void*)adam_tma_kernel<6144, 2, true, 768, __nv_bfloat16>},     // 0 (default)
+     (void*)adam_tma_kernel<6144, 2, true, 768, __nv_bfloat16>, 2, 6144},     // 0 (default)
     {(void*)adam_tma_kernel<6144, 2, true, 256>, 6144, 2, 1, 256,
-     (void*)adam_tma_kernel<6144, 2, true, 256, __nv_bfloat16>},     // 1: best standalone
+     (void*)adam_tma_kernel<6144, 2, true, 256, __nv_bfloat16>, 2, 6144},     // 1: best standalone
     {(void*)adam_tma_kernel<1024, 4, false, 256>, 1024, 4, 3, 256,
-     (void*)adam_tma_kernel<1024, 4, false, 256, __nv_bfloat16>},    // 2: the first version
+     (void*)adam_tma_kernel<1024, 4, false, 256, __nv_bfloat16>, 4, 1024},    // 2: the first version
     {(void*)adam_tma_kernel<4096, 3, true, 1024>, 4096, 3, 1, 1024,
-     (void*)adam_tma_kernel<4096, 3, true, 1024, __nv_bfloat16>},    // 3
+     (void*)adam_tma_kernel<4096, 3, true, 1024, __nv_bfloat16>, 3, 4096},    // 3
+    {(void*)adam_tma_kernel<4096, 3, true, 1024>, 4096, 3, 1, 1024,
+     (void*)adam_tma_kernel<4096, 4, true, 1024, __nv_bfloat16>, 4, 4096},    // 4: bf16 grad, 4-deep ring
+    {(void*)adam_tma_kernel<6144, 2, true, 768>, 6144, 2, 1, 768,
+     (void*)adam_tma_kernel<3072, 4, true, 768, __nv_bfloat16>, 4, 3072},     // 5: bf16 grad, 3072 x 4
 };
 
 template <typename G>
@@ -248,21 +253,23 @@ static int adam_launch(float* p, const void* g, int g_bf16, float* m, float* v, 
     if (use_tma && (cudaFuncSetAttribute(av.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          av.stages * 16 * av.tile + 64) != cudaSuccess ||
                     cudaFuncSetAttribute(av.fn_bf16g, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         av.stages * 14 * av.tile + 64) != cudaSuccess))
+                                         av.stages_bf16g * 14 * av.tile_bf16g + 64) != cudaSuccess))
       use_tma = 0;
   }
   const AdamVariant& av = kAdamVariants[var];
   const size_t gs = g_bf16 ? 2 : 4;
   const bool al = aligned16(p) && aligned16(g) && aligned16(m) && aligned16(v) &&
                   (p_lowp == nullptr || ((uintptr_t)p_lowp & 7) == 0);
-  if (use_tma && al && n >= (int64_t)av.tile * kNumSMs) {
-    const int64_t tiles = n / av.tile;
+  const int tile = g_bf16 ? av.tile_bf16g : av.tile;
+  const int stages = g_bf16 ? av.stages_bf16g : av.stages;
+  if (use_tma && al && n >= (int64_t)tile * kNumSMs) {
+    const int64_t tiles = n / tile;
     const int grid = (int)std::min<int64_t>(tiles, (int64_t)kNumSMs * av.ctas_per_sm);
     __nv_bfloat16* pl = (__nv_bfloat16*)p_lowp;
     AdamScalars sc = s;
     void* args[] = {&p, (void*)&g, &m, &v, &n, &sc, (void*)&skip_flag, &pl};
     FSDP_CUDA(cudaLaunchKernel(g_bf16 ? av.fn_bf16g : av.fn, dim3(grid), dim3(av.threads), args,
-                               (size_t)av.stages * (12 + gs) * av.tile + 64, stream));
+                               (size_t)stages * (12 + gs) * tile + 64, stream));
   } else if (g_bf16) {
     adam_kernel<__nv_bfloat16><<<opt_grid(n), kOptThreads, 0, stream>>>(
         p, (const __nv_bfloat16*)g, m, v, n, s, skip_flag, (__nv_bfloat16*)p_lowp);

@@ -74,35 +74,6 @@ def main():
             ms = a.elapsed_time(b) / 5
             res.append({"lanes": lanes, "piece_mb": piece >> 20, "copies": len(dst) * (total // piece),
                         "ms": round(ms, 4), "gbs": round(len(dst) * total / (ms * 1e-3) / 1e9, 1)})
-    # one cudaMemcpyBatchAsync per run (the driver may schedule the copies of
-    # a batch in any order / concurrently)
-    try:
-        attr = rt.cudaMemcpyAttributes()
-        attr.srcAccessOrder = rt.cudaMemcpySrcAccessOrder.cudaMemcpySrcAccessOrderStream
-        for piece in (4 << 20, 16 << 20, 64 << 20, 256 << 20):
-            dsts, srcs, sizes = [], [], []
-            for d in dst:
-                for off in range(0, total, piece):
-                    dsts.append(d.data_ptr() + off)
-                    srcs.append(src.data_ptr() + off)
-                    sizes.append(piece)
-
-            def runb():
-                ck(rt.cudaMemcpyBatchAsync(dsts, srcs, sizes, len(sizes), [attr], [0], 1, main_s.cuda_stream))
-            for _ in range(3):
-                runb()
-            torch.cuda.synchronize()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(main_s)
-            for _ in range(5):
-                runb()
-            b.record(main_s)
-            torch.cuda.synchronize()
-            ms = a.elapsed_time(b) / 5
-            res.append({"lanes": "batch", "piece_mb": piece >> 20, "copies": len(sizes), "ms": round(ms, 4),
-                        "gbs": round(len(dst) * total / (ms * 1e-3) / 1e9, 1)})
-    except Exception as exc:  # noqa: BLE001 — report, keep the other numbers
-        res.append({"lanes": "batch", "error": repr(exc)[:200]})
     fixed = {}
     for lanes in (1, 2, 4):
         rows = [r for r in res if r.get("lanes") == lanes]

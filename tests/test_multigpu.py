@@ -113,3 +113,12 @@ def test_multigpu_cli_sweep():
     # F=1 (NO_SHARD): no gathers, all-reduce only; F=2 RAF re-gathers in backward, NRAF does not
     assert int(by[("1", "RAF")][1]) == 0 and int(by[("1", "RAF")][3]) > 0
     assert int(by[("2", "RAF")][1]) > int(by[("2", "NRAF")][1]) > 0
+
+
+def test_multigpu_cli_run():
+    """`run` (cli.py:428-456) on 2 ranks: one JSON record per step."""
+    r = _torchrun(2, ["-m", "paper_2304_11277_b200", "run", "--model", "tiny", "--steps", "2"], timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    recs = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    assert [x["step"] for x in recs] == [0, 1]
+    assert all(x["loss"] > 0 for x in recs)

@@ -251,7 +251,7 @@ class FullyShardedDataParallel(nn.Module):
         pgs = {}
         if world > 1 and comm_backend == "ipc":
             comm = DeviceComm.create(FSDPRuntime.pool_bytes_for(layouts, plan, cfg), max_ctas=max(ag_ctas, rs_ctas),
-                                     group=process_group,
+                                     group=pg,
                                      nvls_group=plan.shard_factor if ag_engine == "nvls" else None)
         elif world > 1:
             pgs = _nccl_groups(plan, rank)

@@ -430,6 +430,56 @@ def deadlock_detection(rank, world, results):
     results["deadlock_detection"] = "ok (split and LL)"
 
 
+def wrapper_mesh(rank, world, results):
+    """HYBRID_SHARD named three ways gives the same sharding and bit-identical
+    training: hybrid_shard_size=F, a 2-D device_mesh (replicate, shard), and
+    process_group=(shard_group, replicate_group) (collectives.py:63-72)."""
+    import torch.distributed as dist
+    from paper_2304_11277_b200.fsdp import (FullyShardedDataParallel, MixedPrecision, ModuleWrapPolicy,
+                                            ShardingStrategy)
+    from paper_2304_11277_b200.workloads import CONFIGS, GPT, Block, init_gpt_, synthetic_batch
+    cfg = CONFIGS["tiny"]
+    F = 2
+    R = world // F
+    shard_pgs = [dist.new_group(list(range(g * F, (g + 1) * F))) for g in range(R)]
+    rep_pgs = [dist.new_group(list(range(k, world, F))) for k in range(F)]
+    mesh_kind = "stub"
+    try:
+        from torch.distributed.device_mesh import DeviceMesh
+        mesh = DeviceMesh("cuda", torch.arange(world).view(R, F), mesh_dim_names=("replicate", "shard"))
+        mesh_kind = "torch DeviceMesh"
+    except Exception:  # noqa: BLE001 — e.g. ranks sharing one GPU
+        class _M:
+            pass
+        mesh = _M()
+        mesh.mesh, mesh.mesh_dim_names = torch.arange(world).view(R, F), ("replicate", "shard")
+    variants = {"hybrid_shard_size": dict(hybrid_shard_size=F), "device_mesh": dict(device_mesh=mesh),
+                "group_tuple": dict(process_group=(shard_pgs[rank // F], rep_pgs[rank % F]))}
+    got = {}
+    for name, kw in variants.items():
+        fsdp = FullyShardedDataParallel(init_gpt_(GPT(cfg), seed=0), sharding_strategy=ShardingStrategy.HYBRID_SHARD,
+                                        auto_wrap_policy=ModuleWrapPolicy({Block}),
+                                        mixed_precision=MixedPrecision(param_dtype=torch.bfloat16), lr=1e-3, **kw)
+        check(fsdp.plan.shard_factor == F, f"{name}: F = {fsdp.plan.shard_factor}")
+        x, y = synthetic_batch(cfg, 2, seed=400 + rank, device="cuda")
+        loss = fsdp(x, y)
+        loss.backward()
+        fsdp.optimizer().step()
+        torch.cuda.synchronize()
+        got[name] = (loss.item(), torch.cat([u.master for u in fsdp.rt.units]).cpu())
+        fsdp.close()
+    ref = got["hybrid_shard_size"]
+    for name, (l, m) in got.items():
+        check(l == ref[0] and torch.equal(m, ref[1]), f"{name}: differs from hybrid_shard_size")
+    try:
+        FullyShardedDataParallel(init_gpt_(GPT(cfg), seed=0), sharding_strategy=ShardingStrategy.HYBRID_SHARD,
+                                 auto_wrap_policy=ModuleWrapPolicy({Block}))
+        check(False, "HYBRID_SHARD without a shard-group size did not raise")
+    except ValueError:
+        pass
+    results["wrapper_mesh"] = f"bit-identical ({mesh_kind}, group tuple, hybrid_shard_size; F={F})"
+
+
 def abort_in_step(rank, world, results):
     """A member stalls past the timeout INSIDE a wrapped training step (its
     compute stream sleeps before the step's first all-gather): the waiting
@@ -666,6 +716,8 @@ def main():
                 ("ce_schedules", ce_schedules), ("session_parity", session_parity)]
         scen += [("fsdp_step", lambda r, w, res, s=s, h=h, kw=kw: fsdp_step_parity(r, w, s, h, res, **kw))
                  for s, h, kw in steps]
+        if world >= 4:
+            scen += [("wrapper_mesh", wrapper_mesh)]
         scen += [("deadlock_detection", deadlock_detection), ("abort_in_step", abort_in_step)]
         # MP_SCENARIOS: comma list of scenario names to run (default: all)
         pick = os.environ.get("MP_SCENARIOS")

@@ -50,7 +50,7 @@ def _worlds():
 # W = 8 on a shared GPU: eight contexts time-slicing one device make every
 # barrier a context switch, so run the scenarios that need W = 8 (F = 8 and
 # the 4 x 2 / 2 x 4 hybrids) rather than repeating the W = 2 / 4 coverage
-_SHARED8 = "raw_collectives,fsdp_step,abort_in_step"
+_SHARED8 = "raw_collectives,fsdp_step,wrapper_mesh,abort_in_step"
 
 
 @pytest.mark.parametrize("w", _worlds())
@@ -68,6 +68,7 @@ def test_multigpu_parity(w):
     assert any(k.startswith("FULL_SHARD") for k in strategies)
     if w >= 4:
         assert any(k.startswith("HYBRID_SHARD") for k in strategies), strategies
+        assert "wrapper_mesh" in res
 
 
 def test_multigpu_cli_verify():

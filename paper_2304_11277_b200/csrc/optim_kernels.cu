@@ -197,6 +197,12 @@ static const AdamVariant kAdamVariants[] = {
      (void*)adam_tma_kernel<4096, 4, true, 1024, __nv_bfloat16>, 4, 4096},    // 4: bf16 grad, 4-deep ring
     {(void*)adam_tma_kernel<6144, 2, true, 768>, 6144, 2, 1, 768,
      (void*)adam_tma_kernel<3072, 4, true, 768, __nv_bfloat16>, 4, 3072},     // 5: bf16 grad, 3072 x 4
+    {(void*)adam_tma_kernel<3072, 4, true, 768>, 3072, 4, 1, 768,
+     (void*)adam_tma_kernel<3072, 4, true, 768, __nv_bfloat16>, 4, 3072},     // 6: 3072 x 4 both
+    {(void*)adam_tma_kernel<2048, 6, true, 512>, 2048, 6, 1, 512,
+     (void*)adam_tma_kernel<2048, 7, true, 512, __nv_bfloat16>, 7, 2048},     // 7: 2048 x 6 / 7
+    {(void*)adam_tma_kernel<3072, 4, true, 768>, 3072, 4, 1, 768,
+     (void*)adam_tma_kernel<2048, 7, true, 512, __nv_bfloat16>, 7, 2048},     // 8
 };
 
 template <typename G>

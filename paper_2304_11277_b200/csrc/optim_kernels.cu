@@ -175,37 +175,31 @@ struct AdamVariant {
   void* fn_bf16g;                 // bf16 gradient (W = 1 write-back arena), with its own
   int stages_bf16g, tile_bf16g;   // ring (14 B/elem stages fit deeper rings)
 };
-// Measured on the GPT-1.3B arena at N=1 (1.32 G elements; tools/adam_bench.py
-// standalone, bench.py FSDP_ADAM_VARIANT=k in-step; profiles/r1/adam/).
-// Long contiguous per-array bursts are what the DRAM read/write mix wants:
-// 6144-element tiles streamed through a contiguous range per CTA reach 0.94-
-// 0.97 of the measured copy peak standalone, vs 0.90-0.92 for 1024-element
-// round-robin tiles and for the register kernel.  Inside the step the SM
-// clock is power-capped (~1.6 GHz) and the exact-rounding math (3 IEEE
-// divides + a sqrt per element) needs warps to hide its latency: 256-thread
-// CTAs drop to 0.78 there, 768-thread CTAs give 0.906 (first version 0.895).
+// Measured in the step at N=1 on the GPT-1.3B arena (1.32 G elements;
+// bench.py FSDP_ADAM_VARIANT=k, profiles/r2/adam_ring/; round 1:
+// profiles/r1/adam/).  The SM clock is power-capped (~1.6 GHz) there, so the
+// exact-rounding math (3 IEEE divides + a sqrt per element) must overlap the
+// DRAM stream: what matters is how many bytes are still in flight while a
+// CTA computes on a landed stage.  Two 6144-element stages leave one stage
+// (86 KB) in flight; four 3072-element stages leave three (129 KB): bf16-g
+// Adam 5.67 vs 6.36 ms (0.99 vs 0.89 of the measured copy peak).  For fp32
+// gradients (16 B/elem) six 2048-element stages of 512 threads give 6.40 vs
+// 6.73 ms.  256-thread CTAs starve the math of warps (round 1: 0.78).
 static const AdamVariant kAdamVariants[] = {
-    {(void*)adam_tma_kernel<6144, 2, true, 768>, 6144, 2, 1, 768,
-     (void*)adam_tma_kernel<6144, 2, true, 768, __nv_bfloat16>, 2, 6144},     // 0 (default)
-    {(void*)adam_tma_kernel<6144, 2, true, 256>, 6144, 2, 1, 256,
-     (void*)adam_tma_kernel<6144, 2, true, 256, __nv_bfloat16>, 2, 6144},     // 1: best standalone
-    {(void*)adam_tma_kernel<1024, 4, false, 256>, 1024, 4, 3, 256,
-     (void*)adam_tma_kernel<1024, 4, false, 256, __nv_bfloat16>, 4, 1024},    // 2: the first version
-    {(void*)adam_tma_kernel<4096, 3, true, 1024>, 4096, 3, 1, 1024,
-     (void*)adam_tma_kernel<4096, 3, true, 1024, __nv_bfloat16>, 3, 4096},    // 3
-    {(void*)adam_tma_kernel<4096, 3, true, 1024>, 4096, 3, 1, 1024,
-     (void*)adam_tma_kernel<4096, 4, true, 1024, __nv_bfloat16>, 4, 4096},    // 4: bf16 grad, 4-deep ring
-    {(void*)adam_tma_kernel<6144, 2, true, 768>, 6144, 2, 1, 768,
-     (void*)adam_tma_kernel<3072, 4, true, 768, __nv_bfloat16>, 4, 3072},     // 5: bf16 grad, 3072 x 4
-    {(void*)adam_tma_kernel<3072, 4, true, 768>, 3072, 4, 1, 768,
-     (void*)adam_tma_kernel<3072, 4, true, 768, __nv_bfloat16>, 4, 3072},     // 6: 3072 x 4 both
     {(void*)adam_tma_kernel<2048, 6, true, 512>, 2048, 6, 1, 512,
-     (void*)adam_tma_kernel<2048, 7, true, 512, __nv_bfloat16>, 7, 2048},     // 7: 2048 x 6 / 7
+     (void*)adam_tma_kernel<3072, 4, true, 768, __nv_bfloat16>, 4, 3072},     // 0 (default)
+    {(void*)adam_tma_kernel<6144, 2, true, 768>, 6144, 2, 1, 768,
+     (void*)adam_tma_kernel<6144, 2, true, 768, __nv_bfloat16>, 2, 6144},     // 1: round-1 default
+    {(void*)adam_tma_kernel<6144, 2, true, 256>, 6144, 2, 1, 256,
+     (void*)adam_tma_kernel<6144, 2, true, 256, __nv_bfloat16>, 2, 6144},     // 2: best standalone (r1)
+    {(void*)adam_tma_kernel<1024, 4, false, 256>, 1024, 4, 3, 256,
+     (void*)adam_tma_kernel<1024, 4, false, 256, __nv_bfloat16>, 4, 1024},    // 3: the first version
+    {(void*)adam_tma_kernel<4096, 3, true, 1024>, 4096, 3, 1, 1024,
+     (void*)adam_tma_kernel<4096, 4, true, 1024, __nv_bfloat16>, 4, 4096},    // 4
     {(void*)adam_tma_kernel<3072, 4, true, 768>, 3072, 4, 1, 768,
-     (void*)adam_tma_kernel<2048, 7, true, 512, __nv_bfloat16>, 7, 2048},     // 8
+     (void*)adam_tma_kernel<2048, 7, true, 512, __nv_bfloat16>, 7, 2048},     // 5
 };
 
-template <typename G>
 __global__ void __launch_bounds__(kOptThreads)
 sgd_kernel(float* __restrict__ p, const G* __restrict__ g, int64_t n, float lr,
            const float* __restrict__ skip, __nv_bfloat16* __restrict__ plow) {

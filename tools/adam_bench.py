@@ -15,7 +15,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 VARIANTS = [("register", {"FSDP_ADAM_TMA": "0"})] + \
-    [(f"tma{v}", {"FSDP_ADAM_TMA": "1", "FSDP_ADAM_VARIANT": str(v)}) for v in range(4)]
+    [(f"tma{v}", {"FSDP_ADAM_TMA": "1", "FSDP_ADAM_VARIANT": str(v)}) for v in range(6)]
 
 
 def one(n: int) -> dict:

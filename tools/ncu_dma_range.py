@@ -26,20 +26,22 @@ def main():
     own = torch.empty(shard, dtype=torch.uint8, device=0)
     dst = [torch.empty(shard, dtype=torch.uint8, device=d) for d in range(1, n)]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=0)
+    marker = torch.zeros(1, device=0)
     s = torch.cuda.Stream(0)
     kind = rt.cudaMemcpyKind.cudaMemcpyDeviceToDevice
     for rep in range(2):
         flush.zero_()                                   # src out of L2 before the range
         torch.cuda.synchronize()
         if rep == 1:
-            rt.cudaProfilerStart()
+            torch.cuda.profiler.start()               # cudaProfilerStart: opens ncu's range
+            marker.add_(1)                            # a kernel in the range (ranges need one)
         for d in dst:                                   # remote copies, one destination at a time
             assert rt.cudaMemcpyAsync(d.data_ptr(), src.data_ptr(), shard, kind, s.cuda_stream)[0] == \
                 rt.cudaError_t.cudaSuccess
         rt.cudaMemcpyAsync(own.data_ptr(), src.data_ptr(), shard, kind, s.cuda_stream)
         s.synchronize()
         if rep == 1:
-            rt.cudaProfilerStop()
+            torch.cuda.profiler.stop()
     print(f"shard {shard} B, {len(dst)} peers + own copy: algorithmic DRAM read on GPU 0 = "
           f"{shard} B (once) vs {shard * (len(dst) + 1)} B (once per copy); write = {shard} B (own chunk)")
 

@@ -200,6 +200,7 @@ static const AdamVariant kAdamVariants[] = {
      (void*)adam_tma_kernel<2048, 7, true, 512, __nv_bfloat16>, 7, 2048},     // 5
 };
 
+template <typename G>
 __global__ void __launch_bounds__(kOptThreads)
 sgd_kernel(float* __restrict__ p, const G* __restrict__ g, int64_t n, float lr,
            const float* __restrict__ skip, __nv_bfloat16* __restrict__ plow) {

@@ -286,6 +286,18 @@ __global__ void __launch_bounds__(32) coll_signal_kernel(const __grid_constant__
   }
 }
 
+// Copy-engine path, fused signal + exit barrier (one launch instead of two):
+// publish "my DMA is done" to every member, then wait for every member's.
+__global__ void __launch_bounds__(32) coll_signal_exit_kernel(const __grid_constant__ CollParams p) {
+  const Group g = make_group(p);
+  if ((int)threadIdx.x < g.size) {
+    const int peer = g.member(threadIdx.x);
+    __threadfence_system();
+    st_release_sys(flag_ptr(p.bases[peer], p.channel, 1, g.rank, 0), p.epoch);
+    wait_flag(p, g, flag_ptr(p.bases[g.rank], p.channel, 1, peer, 0));
+  }
+}
+
 // Pipelined copy-engine push: after piece q's DMA writes into every member's
 // staging (stream order on the copy side stream), publish "piece q landed"
 // (phase 1, slot q) to every member; the receiving stream waits for slot q
@@ -1796,8 +1808,7 @@ extern "C" int fsdp_allgather_ce(fsdp_comm_t* c, int channel, int gsize, int gst
   if (c->timing) { a = take_event(c); b = take_event(c); FSDP_CUDA(cudaEventRecord(a, s)); }
   if (int rc = ce_fork_join(c, 0, s, gsize, pos, dst, src, (size_t)n * es)) return rc;
   if (c->timing) { FSDP_CUDA(cudaEventRecord(b, s)); c->timed[FSDP_KIND_AG].emplace_back(a, b); }
-  if (int rc = launch(c, coll_signal_kernel, p, 1, 32, s)) return rc;
-  return launch(c, coll_exit_kernel, p, 1, 256, s);
+  return launch(c, coll_signal_exit_kernel, p, 1, 32, s);   // my copies landed; so did everyone's
 }
 
 extern "C" int fsdp_reduce_scatter_ce(fsdp_comm_t* c, int channel, int gsize, int gstride,
@@ -1986,13 +1997,14 @@ extern "C" int fsdp_reduce_scatter_ce(fsdp_comm_t* c, int channel, int gsize, in
   }
   if (int rc = ce_fork_join(c, 1, s, gsize, pos, dst, src, (size_t)n * es)) return rc;
   if (c->timing) { FSDP_CUDA(cudaEventRecord(b, s)); c->timed[FSDP_KIND_RS].emplace_back(a, b); }
-  if (int rc = launch(c, coll_signal_kernel, p, 1, 32, s)) return rc;   // my copies are done
   if (push) {
-    // every member's pushes into my staging have landed; my payload was
-    // only read by my own copies, so nothing waits after the reduction
-    if (int rc = launch(c, coll_exit_kernel, p, 1, 256, s)) return rc;
+    // my copies are done and every member's pushes into my staging have
+    // landed; my payload was only read by my own copies, so nothing waits
+    // after the reduction
+    if (int rc = launch(c, coll_signal_exit_kernel, p, 1, 32, s)) return rc;
     return reduce_piece(0, n);
   }
+  if (int rc = launch(c, coll_signal_kernel, p, 1, 32, s)) return rc;   // done reading my peers
   if (int rc = reduce_piece(0, n)) return rc;
   return launch(c, coll_exit_kernel, p, 1, 256, s);     // peers done reading mine
 }

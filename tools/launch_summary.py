@@ -13,7 +13,7 @@ from collections import defaultdict
 # without the fsdp:: namespace depending on its name-base setting)
 OURS = ("adam_kernel", "adam_tma_kernel", "allgather_kernel", "allgather_ll_kernel", "allgather_nvls_kernel",
         "allreduce_kernel", "ar_epilogue_kernel", "cast_kernel", "ce_reduce_kernel", "coll_enter_kernel",
-        "coll_exit_kernel", "coll_signal_kernel", "coll_signal_slot_kernel", "coll_wait_slot_kernel",
+        "coll_exit_kernel", "coll_signal_kernel", "coll_signal_exit_kernel", "fold_error_kernel", "coll_signal_slot_kernel", "coll_wait_slot_kernel",
         "flatten_kernel", "reduce_scatter_kernel", "reduce_scatter_ll_kernel", "reduce_scatter_pull_kernel",
         "reduce_scatter_tma_kernel", "scalar_allreduce_kernel", "sgd_kernel", "unflatten_kernel",
         "unscale_kernel", "shard_copy_kernel")

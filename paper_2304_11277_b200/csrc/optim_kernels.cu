@@ -173,7 +173,8 @@ struct AdamVariant {
   void* fn;
   int tile, stages, ctas_per_sm, threads;
   void* fn_bf16g;                 // bf16 gradient (W = 1 write-back arena), with its own
-  int stages_bf16g, tile_bf16g;   // ring (14 B/elem stages fit deeper rings)
+  int stages_bf16g, tile_bf16g;   // ring (14 B/elem stages fit deeper rings) and CTA size
+  int threads_bf16g;
 };
 // Measured in the step at N=1 on the GPT-1.3B arena (1.32 G elements;
 // bench.py FSDP_ADAM_VARIANT=k, profiles/r2/adam_ring/; round 1:
@@ -187,17 +188,17 @@ struct AdamVariant {
 // 6.73 ms.  256-thread CTAs starve the math of warps (round 1: 0.78).
 static const AdamVariant kAdamVariants[] = {
     {(void*)adam_tma_kernel<2048, 6, true, 512>, 2048, 6, 1, 512,
-     (void*)adam_tma_kernel<3072, 4, true, 768, __nv_bfloat16>, 4, 3072},     // 0 (default)
+     (void*)adam_tma_kernel<3072, 4, true, 768, __nv_bfloat16>, 4, 3072, 768},     // 0 (default)
     {(void*)adam_tma_kernel<6144, 2, true, 768>, 6144, 2, 1, 768,
-     (void*)adam_tma_kernel<6144, 2, true, 768, __nv_bfloat16>, 2, 6144},     // 1: round-1 default
+     (void*)adam_tma_kernel<6144, 2, true, 768, __nv_bfloat16>, 2, 6144, 768},     // 1: round-1 default
     {(void*)adam_tma_kernel<6144, 2, true, 256>, 6144, 2, 1, 256,
-     (void*)adam_tma_kernel<6144, 2, true, 256, __nv_bfloat16>, 2, 6144},     // 2: best standalone (r1)
+     (void*)adam_tma_kernel<6144, 2, true, 256, __nv_bfloat16>, 2, 6144, 256},     // 2: best standalone (r1)
     {(void*)adam_tma_kernel<1024, 4, false, 256>, 1024, 4, 3, 256,
-     (void*)adam_tma_kernel<1024, 4, false, 256, __nv_bfloat16>, 4, 1024},    // 3: the first version
+     (void*)adam_tma_kernel<1024, 4, false, 256, __nv_bfloat16>, 4, 1024, 256},    // 3: the first version
     {(void*)adam_tma_kernel<4096, 3, true, 1024>, 4096, 3, 1, 1024,
-     (void*)adam_tma_kernel<4096, 4, true, 1024, __nv_bfloat16>, 4, 4096},    // 4
+     (void*)adam_tma_kernel<4096, 4, true, 1024, __nv_bfloat16>, 4, 4096, 1024},    // 4
     {(void*)adam_tma_kernel<3072, 4, true, 768>, 3072, 4, 1, 768,
-     (void*)adam_tma_kernel<2048, 7, true, 512, __nv_bfloat16>, 7, 2048},     // 5
+     (void*)adam_tma_kernel<2048, 7, true, 512, __nv_bfloat16>, 7, 2048, 512},     // 5
 };
 
 template <typename G>
@@ -269,7 +270,7 @@ static int adam_launch(float* p, const void* g, int g_bf16, float* m, float* v, 
     __nv_bfloat16* pl = (__nv_bfloat16*)p_lowp;
     AdamScalars sc = s;
     void* args[] = {&p, (void*)&g, &m, &v, &n, &sc, (void*)&skip_flag, &pl};
-    FSDP_CUDA(cudaLaunchKernel(g_bf16 ? av.fn_bf16g : av.fn, dim3(grid), dim3(av.threads), args,
+    FSDP_CUDA(cudaLaunchKernel(g_bf16 ? av.fn_bf16g : av.fn, dim3(grid), dim3(g_bf16 ? av.threads_bf16g : av.threads), args,
                                (size_t)stages * (12 + gs) * tile + 64, stream));
   } else if (g_bf16) {
     adam_kernel<__nv_bfloat16><<<opt_grid(n), kOptThreads, 0, stream>>>(

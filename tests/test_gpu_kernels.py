@@ -157,6 +157,18 @@ def test_adam_bf16_grad_matches_fp32_grad(K, n):
     assert torch.equal(pa, pb)
 
 
+@pytest.mark.parametrize("variant", range(6))
+def test_adam_every_ring_variant_bit_exact(variant):
+    """Every TMA ring geometry of the Adam kernel (FSDP_ADAM_VARIANT, one per
+    process), fp32 and bf16 gradients, against the oracle."""
+    import subprocess
+    import sys
+    root = __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "tools/adam_check.py"], cwd=root, capture_output=True, text=True,
+                       timeout=300, env=dict(__import__("os").environ, FSDP_ADAM_VARIANT=str(variant)))
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
 def test_sgd_golden(K, golden):
     arrays, _ = golden
     p = torch.from_numpy(arrays["sgd/p0"].copy()).cuda()

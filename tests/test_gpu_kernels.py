@@ -1,5 +1,9 @@
 """Parity of the copy / cast / optimizer kernels (through the C ABI) with the
 oracle and with the reference's own golden vectors.  Bit-exact."""
+import os
+import subprocess
+import sys
+
 import numpy as np
 import pytest
 import torch
@@ -161,11 +165,9 @@ def test_adam_bf16_grad_matches_fp32_grad(K, n):
 def test_adam_every_ring_variant_bit_exact(variant):
     """Every TMA ring geometry of the Adam kernel (FSDP_ADAM_VARIANT, one per
     process), fp32 and bf16 gradients, against the oracle."""
-    import subprocess
-    import sys
-    root = __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__)))
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "tools/adam_check.py"], cwd=root, capture_output=True, text=True,
-                       timeout=300, env=dict(__import__("os").environ, FSDP_ADAM_VARIANT=str(variant)))
+                       timeout=300, env=dict(os.environ, FSDP_ADAM_VARIANT=str(variant)))
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
 
 

@@ -37,14 +37,9 @@ def _torchrun(w, args, env=None, timeout=1500):
 
 
 def _worlds():
-    n = torch.cuda.device_count()
-    if n >= 8:
-        return [2, 4, 8]
-    if n >= 4:
-        return [2, 4]
-    if n >= 2:
-        return [2]
-    return [2, 4, 8]          # shared: W processes time-share cuda:0
+    # W = 2, 4, 8 on any box: one GPU per rank where there are enough, else
+    # the ranks share the GPUs round-robin (gloo bootstrap)
+    return [2, 4, 8]
 
 
 # W = 8 on a shared GPU: eight contexts time-slicing one device make every

@@ -123,6 +123,9 @@ class RuntimeConfig:
     # all-gathers wait only for it and overlap the launch over the rest of
     # the arena (0 = one launch).  Same arithmetic, elementwise.
     opt_split_first: int = 2
+    # further launches at doubling unit counts (2, 4, 8, 16 units, ...): the
+    # k-th gather of the next step waits only for the launch covering it
+    opt_split_geom: bool = False
     # world of one, bf16 payload: the fused write-back lands in a bf16 grad
     # arena and the optimizer reads bf16 gradients (bf16 -> fp32 is exact,
     # so the update is bit-identical); 2 B/elem less written by the
@@ -358,8 +361,9 @@ class FSDPRuntime:
         self.abort_flag_bwd = torch.zeros(1, dtype=torch.float32, device=self.device)
         self.err_mirror = torch.zeros(1, dtype=torch.int32).pin_memory() if comm is not None else None
         self.opt_done: torch.cuda.Event | None = None
-        self.opt_early: torch.cuda.Event | None = None   # first optimizer launch (units < opt_early_units)
-        self.opt_early_units = 0
+        # (end unit, event) per early optimizer launch: a unit's next gather
+        # waits for the launch covering its shard (units < end), else opt_done
+        self.opt_chunk_events: list[tuple[int, torch.cuda.Event]] = []
         self.adam_steps = 0
         self.max_live_slots = 0
         self.fwd_visits: dict[int, int] = {}
@@ -680,8 +684,8 @@ class FSDPRuntime:
             if free_ev is not None:
                 self.ag_stream.wait_event(free_ev)
             if self.opt_done is not None:
-                early = self.opt_early is not None and uid < self.opt_early_units
-                self.ag_stream.wait_event(self.opt_early if early else self.opt_done)
+                self.ag_stream.wait_event(next((e for end, e in self.opt_chunk_events if uid < end),
+                                               self.opt_done))
             if self.cfg.fake_comm:
                 pass
             elif self.cfg.comm_backend == "ipc":
@@ -689,7 +693,7 @@ class FSDPRuntime:
                                 lay.psi * (2 if self.cfg.mixed else 4)):
                     # the tail engine is for a first gather with nothing to
                     # overlap; after a split optimizer it overlaps the second launch
-                    first = self._ag_since_opt == 0 and self.opt_done is not None and self.opt_early is None
+                    first = self._ag_since_opt == 0 and self.opt_done is not None and not self.opt_chunk_events
                     if self._use_ll(uid):
                         self.comm.all_gather_ll(self._group_ag(), [src], self.slots.offsets[slot],
                                                 self.compute_dtype, self.ll_ag_off, stream=self.ag_stream)
@@ -1295,7 +1299,7 @@ class FSDPRuntime:
             ev.record(self.ar_stream)             # = rs_stream unless HYBRID
             self.compute_stream.wait_event(ev)
             self.opt_done = ev
-            self.opt_early, self.opt_early_units = None, 0
+            self.opt_chunk_events = []
             self._ag_since_opt = 0
             self.events.append((self.step_count - 1, "opt_step", None))
             return
@@ -1307,19 +1311,19 @@ class FSDPRuntime:
         lw = 2 if self.low is not None else 0
         # algorithmic bytes: Adam reads p, g, m, v and writes p, m, v (+ bf16 p); SGD p, g -> p (+ bf16 p)
         nb = n * ((24 + gs + lw) if cfg.optimizer == "adam" else (8 + gs + lw))
-        k = self._early_prefix_units()
+        bounds = self._opt_chunk_bounds()
         t = self._adam_t(skip) if cfg.optimizer == "adam" else 0
-        self.opt_early, self.opt_early_units = None, 0
+        self.opt_chunk_events = []
         with self.timed(cfg.optimizer + "_step", self.compute_stream, nb):
-            if k:
-                cut = self.units[k].master.storage_offset() - self.master.storage_offset()
-                self._opt_launch(skip, t, 0, cut)
-                self.opt_early = torch.cuda.Event()
-                self.opt_early.record(self.compute_stream)
-                self.opt_early_units = k
-                self._opt_launch(skip, t, cut, n)
-            else:
-                self._opt_launch(skip, t, 0, n)
+            a = 0
+            for end in bounds:
+                cut = self.units[end].master.storage_offset() - self.master.storage_offset()
+                self._opt_launch(skip, t, a, cut)
+                ev_c = torch.cuda.Event()
+                ev_c.record(self.compute_stream)
+                self.opt_chunk_events.append((end, ev_c))
+                a = cut
+            self._opt_launch(skip, t, a, n)
         ev = torch.cuda.Event()
         ev.record(self.compute_stream)
         self.opt_done = ev
@@ -1335,6 +1339,22 @@ class FSDPRuntime:
         if k <= 0 or self.direct_views or len(order) < k or sorted(order[:k]) != list(range(k)):
             return 0
         return k
+
+    def _opt_chunk_bounds(self) -> list[int]:
+        """Unit boundaries of the early optimizer launches: [k] (opt_split_first),
+        then doubling (2k, 4k, ...) with opt_split_geom while each is still a
+        forward-order prefix of the arena and leaves some arena after it."""
+        k = self._early_prefix_units()
+        if not k:
+            return []
+        bounds = [k]
+        if self.cfg.opt_split_geom:
+            order = self.prev_fwd_order or self.fwd_order
+            b = 2 * k
+            while b < len(self.units) and len(order) >= b and sorted(order[:b]) == list(range(b)):
+                bounds.append(b)
+                b *= 2
+        return bounds
 
     def _opt_launch(self, skip, t: int, a: int, b: int) -> None:
         """One optimizer launch over arena elements [a, b)."""

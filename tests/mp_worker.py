@@ -319,7 +319,7 @@ def nvls_collectives(rank, world, results):
 
 
 def fsdp_step_parity(rank, world, strategy, hybrid, results, backend="ipc", opt_in_bwd=False,
-                     engine="ce", ll=False, fused=False, num_slots=None):
+                     engine="ce", ll=False, fused=False, num_slots=None, split_geom=False):
     """ll=False pins every unit to `engine` (the tiny GPT's units are all
     small enough for the low-latency path, which ll=True exercises)."""
     from paper_2304_11277_b200 import kernels  # noqa: F401
@@ -335,7 +335,8 @@ def fsdp_step_parity(rank, world, strategy, hybrid, results, backend="ipc", opt_
                                     optimizer_in_backward=opt_in_bwd, ag_engine=engine,
                                     rs_engine="sm" if engine == "nvls" else engine,
                                     ll_max_bytes=(6 << 20) if ll else 0, fused_cast_ag=fused,
-                                    num_slots=num_slots)
+                                    num_slots=num_slots, opt_split_first=1 if split_geom else 2,
+                                    opt_split_geom=split_geom)
     plan = fsdp.plan
     ref = init_gpt_(GPT(cfg), seed=0).cuda().to(torch.bfloat16)
     x, y = synthetic_batch(cfg, 2, seed=100 + rank, device="cuda")
@@ -345,7 +346,7 @@ def fsdp_step_parity(rank, world, strategy, hybrid, results, backend="ipc", opt_
     lref.backward()
     key = (f"{strategy}{'' if hybrid is None else hybrid}/{backend}/{'ll' if ll else engine}"
            f"{'/opt-in-bwd' if opt_in_bwd else ''}{'/fused-cast-ag' if fused else ''}"
-           f"{'' if num_slots is None else '/slots%d' % num_slots}")
+           f"{'' if num_slots is None else '/slots%d' % num_slots}{'/opt-split-geom' if split_geom else ''}")
     torch.cuda.synchronize()
     # initial shards from the oracle (flatten + shard of the same init)
     vals = {k: v.detach().float().cpu().numpy() for k, v in init_gpt_(GPT(cfg), seed=0).named_parameters()}
@@ -703,7 +704,7 @@ def main():
         # backward prefetch finds no free slot and is skipped).  The default 3
         # slots already re-gather each block into a different slot in backward
         # (saved tensors re-materialise against it, pack_hook)
-        steps += [("FULL_SHARD", None, {"num_slots": 2})]
+        steps += [("FULL_SHARD", None, {"num_slots": 2}), ("FULL_SHARD", None, {"split_geom": True})]
         if not SHARED:
             steps += [("FULL_SHARD", None, {"engine": "nvls"})]
             steps += [("HYBRID_SHARD", f, {"engine": "nvls"}) for f in hybrids]

@@ -77,8 +77,9 @@ def parse():
                     help="step each unit's shard in backward (measured: slower at N=1, "
                          "Adam contends for HBM with the backward kernels)")
     ap.add_argument("--cpu-tokens", type=int, default=2048)
-    ap.add_argument("--opt-split-geom", action="store_true",
-                    help="optimizer launches at doubling unit counts (2, 4, 8, ...) of the forward order")
+    ap.add_argument("--opt-split-geom", choices=["auto", "on", "off"], default="auto",
+                    help="optimizer launches at doubling unit counts (1, 2, 4, ...) of the forward order "
+                         "(auto: when the rank's arena has >= 1 G elements)")
     ap.add_argument("--no-ar-pool", action="store_true",
                     help="HYBRID/NO_SHARD: all-reduce into a gather buffer + epilogue instead of in place")
     ap.add_argument("--no-w1-bf16-grad", action="store_true",
@@ -222,7 +223,7 @@ def run_ours(args):
         rs_engine=args.rs_engine, tail_engine=args.tail_engine, ll_max_bytes=args.ll_max_bytes,
         opt_split_first=args.opt_split_first, fused_cast_ag=args.fused_cast_ag,
         ar_in_pool=not args.no_ar_pool, w1_bf16_grad=not args.no_w1_bf16_grad,
-        opt_split_geom=args.opt_split_geom)
+        opt_split_geom={"auto": None, "on": True, "off": False}[args.opt_split_geom])
     opt = fsdp.optimizer()
     rt = fsdp.rt
     dev_inputs = tuple(h.to(dev) for h in host)
@@ -440,7 +441,7 @@ def step_config(args, world: int) -> dict:
             "opt_split_first": args.opt_split_first,
             **({"fused_cast_ag": True} if args.fused_cast_ag else {}),
             **({"ar_in_pool": False} if args.no_ar_pool else {}),
-            **({"opt_split_geom": True} if args.opt_split_geom else {}),
+            "opt_split_geom": args.opt_split_geom,
             **({"w1_bf16_grad": False} if args.no_w1_bf16_grad else {}),
             "l2": "inputs > L2 (weights+state >20 GB)"}
 

@@ -144,7 +144,7 @@ class FullyShardedDataParallel(nn.Module):
                  tail_engine: str = "sm", ll_max_bytes: int = 6 << 20, opt_split_first: int = 2,
                  rate_limit: int | None | str = "auto", keep_outermost_unsharded: bool = True,
                  fused_cast_ag: bool = False, ar_in_pool: bool = True, w1_bf16_grad: bool = True,
-                 opt_split_geom: bool = False):
+                 opt_split_geom: bool | None = None):
         super().__init__()
         if cpu_offload is not None and cpu_offload.offload_params:
             raise NotImplementedError("CPU offload is out of scope for the B200 runtime")

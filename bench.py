@@ -334,9 +334,9 @@ def run_ours(args):
     mine = {k: v for k, v in timers.items() if not k.startswith("stall_")}
     # dominant SM kernel of this library; collectives moved by copy engines
     # (DMA, no SM code) are reported separately as bus bandwidth
-    dma = {k for k in ("allgather", "reduce_scatter")
+    dma = {k for k in ("allgather", "reduce_scatter", "allreduce")
            if (k == "allgather" and args.ag_engine == "ce" and not args.fused_cast_ag)
-           or (k == "reduce_scatter" and args.rs_engine == "ce")}
+           or (k in ("reduce_scatter", "allreduce") and args.rs_engine == "ce")}
     cands = {k: v for k, v in mine.items() if k not in dma}
     dom = max(cands, key=lambda k: cands[k]["total_ms"]) if cands else None
     roof = None

@@ -376,12 +376,14 @@ def run_ours(args):
                       **({"data_kernel_mean_ms": round(v["data_mean_ms"], 4)} if "data_mean_ms" in v else {})}
                   for k, v in mine.items()}
     comm_bw = {}
-    for k in ("allgather", "reduce_scatter"):
+    for k in ("allgather", "reduce_scatter", "allreduce"):
         if k in mine and world > 1:
             d = mine[k]
             F = rt.plan.shard_factor
-            comm_bw[k + "_busbw_gbs"] = round(d["bytes_total"] / max(1, d["count"]) * (F - 1) / F
-                                              / (d.get("data_mean_ms", d["mean_ms"]) * 1e-3) / 1e9, 1)
+            g, f = (world // F, 2.0) if k == "allreduce" else (F, 1.0)   # all-reduce: 2 (g-1)/g
+            if g > 1:
+                comm_bw[k + "_busbw_gbs"] = round(d["bytes_total"] / max(1, d["count"]) * f * (g - 1) / g
+                                                  / (d.get("data_mean_ms", d["mean_ms"]) * 1e-3) / 1e9, 1)
     out = None
     if rank == 0:
         out = {

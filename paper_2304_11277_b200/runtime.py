@@ -625,7 +625,8 @@ class FSDPRuntime:
         if self.comm is not None and self.profile:
             # the data kernels alone (the 1-CTA enter/exit barrier kernels
             # around them absorb waiting for late peers)
-            for name, kind in (("allgather", self.comm.KIND_AG), ("reduce_scatter", self.comm.KIND_RS)):
+            for name, kind in (("allgather", self.comm.KIND_AG), ("reduce_scatter", self.comm.KIND_RS),
+                               ("allreduce", self.comm.KIND_AR)):
                 d = self.comm.timing_drain(kind)
                 if name in out and d:
                     out[name]["data_mean_ms"] = sum(d) / len(d)

@@ -189,11 +189,15 @@ def ce_schedules(rank, world, results):
     # 5 at 512K)
     # last case: hybrid -- copy engines for 75 % of every chunk, an SM TMA
     # pull reducing the last 25 % from the peers (FSDP_CE_RS_SM_FRAC)
-    for n, serial, push, minp, smf in ((262144 + 8, 1, 0, 0, 0), ((1 << 23) + 24, 1, 0, 1 << 21, 0),
-                                       ((1 << 23) + 24, 1, 1, 1 << 21, 0), ((1 << 23) + 24, 1, 1, 1 << 19, 0),
-                                       (262144 + 8, 1, 1, 0, 0),
-                                       (262144 + 8, 0, 0, 0, 0), (262144 + 8, 0, 1, 0, 0),
-                                       ((1 << 23) + 24, 1, 1, 1 << 21, 0.25)):
+    # last-but-one: piece-major all-gather DMA (FSDP_CE_AG_PIECE = 4 MB: 5 pieces
+    # of the 16.8 MB bf16 shard, every peer per piece)
+    for n, serial, push, minp, smf, agp in ((262144 + 8, 1, 0, 0, 0, 0), ((1 << 23) + 24, 1, 0, 1 << 21, 0, 0),
+                                            ((1 << 23) + 24, 1, 1, 1 << 21, 0, 0),
+                                            ((1 << 23) + 24, 1, 1, 1 << 19, 0, 0),
+                                            (262144 + 8, 1, 1, 0, 0, 0),
+                                            (262144 + 8, 0, 0, 0, 0, 0), (262144 + 8, 0, 1, 0, 0, 0),
+                                            ((1 << 23) + 24, 1, 0, 0, 0, 4 << 20),
+                                            ((1 << 23) + 24, 1, 1, 1 << 21, 0.25, 0)):
         rngs = [np.random.default_rng(555 + r) for r in range(world)]
         shards = [g.standard_normal(n).astype(np.float32) for g in rngs]
         grads = [round_to_bf16(g.standard_normal(n * world).astype(np.float32)) for g in rngs]
@@ -206,6 +210,7 @@ def ce_schedules(rank, world, results):
         os.environ["FSDP_CE_RS_PIPE_MIN"] = str(2 * minp if minp else (64 << 20))
         os.environ["FSDP_CE_RS_GEOM"] = "0" if (minp and not push) else "1"
         os.environ["FSDP_CE_RS_SM_FRAC"] = str(smf)
+        os.environ["FSDP_CE_AG_PIECE"] = str(agp)
         nb = n * world * 2 + (1 << 20)
         comm = DeviceComm.create(3 * nb + (4 << 20), max_ctas=32)
         try:
@@ -226,9 +231,10 @@ def ce_schedules(rank, world, results):
         finally:
             comm.close()
             for k in ("FSDP_CE_SERIAL", "FSDP_CE_RS_PUSH", "FSDP_CE_RS_MIN_PIECE", "FSDP_CE_RS_PIPE_MIN",
-                      "FSDP_CE_RS_GEOM", "FSDP_CE_RS_SM_FRAC"):
+                      "FSDP_CE_RS_GEOM", "FSDP_CE_RS_SM_FRAC", "FSDP_CE_AG_PIECE"):
                 del os.environ[k]
-        done.append(f"n={n}/serial={serial}/push={push}/min_piece={minp}" + (f"/sm_frac={smf}" if smf else ""))
+        done.append(f"n={n}/serial={serial}/push={push}/min_piece={minp}" + (f"/sm_frac={smf}" if smf else "")
+                    + (f"/ag_piece={agp}" if agp else ""))
     results["ce_schedules"] = done
 
 

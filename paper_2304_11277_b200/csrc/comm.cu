@@ -1186,7 +1186,7 @@ struct fsdp_comm {
   int ce_reduce_cap = 0;                      // FSDP_CE_REDUCE_CAP: grid cap of every CE reduction (0: 4 CTAs/SM)
   bool ce_rs_noreduce = false;
   int misorder_rs = 0;                        // fault hook (fsdp_comm_set_fault)
-  size_t ce_ag_piece = 0;                     // FSDP_CE_AG_PIECE: piece-major all-gather DMA (0: off)
+  int64_t ce_ag_piece = -1;                   // FSDP_CE_AG_PIECE: piece-major all-gather DMA (-1 auto, 0 off, N bytes)
   int rs_tma_ring = -1;
   float ce_rs_sm_frac = 0.f;                  // FSDP_CE_RS_SM_FRAC: tail fraction of a pipelined chunk pulled by SM TMA                       // FSDP_RS_TMA_RING: TMA-pull ring geometry (-1: not read yet)                // FSDP_CE_RS_NOREDUCE=1: DIAGNOSTIC ONLY, skip the reductions (wrong results)
   std::vector<cudaEvent_t> ce_events;
@@ -1717,7 +1717,7 @@ static int ce_prepare(fsdp_comm_t* c) {
     if (const char* e = getenv("FSDP_CE_RS_NOREDUCE")) c->ce_rs_noreduce = atoi(e) != 0;
     if (const char* e = getenv("FSDP_CE_REDUCE_CAP")) c->ce_reduce_cap = std::max(0, atoi(e));
     if (const char* e = getenv("FSDP_CE_RS_SM_FRAC")) c->ce_rs_sm_frac = std::max(0.f, std::min(0.9f, (float)atof(e)));
-    if (const char* e = getenv("FSDP_CE_AG_PIECE")) c->ce_ag_piece = (size_t)std::max(0LL, atoll(e));
+    if (const char* e = getenv("FSDP_CE_AG_PIECE")) c->ce_ag_piece = std::max<int64_t>(-1, atoll(e));
     for (int k = 0; k < 3; ++k)
       for (int r = 0; r < FSDP_MAX_RANKS * c->ce_split; ++r)
         FSDP_CUDA(cudaStreamCreateWithFlags(&c->ce_stream[k][r], cudaStreamNonBlocking));
@@ -1747,12 +1747,19 @@ static int ce_fork_join(fsdp_comm_t* c, int kind, cudaStream_t s, int gsize, int
     cudaStream_t* row = c->ce_stream[c->ce_shared_streams ? 0 : kind];
     cudaStream_t cs = row[0];
     FSDP_CUDA(cudaStreamWaitEvent(cs, fork, 0));
-    // piece-major (FSDP_CE_AG_PIECE, all-gather sources larger than it):
-    // every destination gets piece q while q is still in L2, so the shard
-    // is read from DRAM once instead of once per peer (measured: a 134 MB
-    // shard was read 3.95x at W = 4); costs one copy start per piece and peer
-    const size_t piece = (kind == 0 && c->ce_ag_piece > 0 && bytes > c->ce_ag_piece)
-                             ? (c->ce_ag_piece + 255) / 256 * 256 : bytes;
+    // piece-major all-gather: every destination gets piece q while q is
+    // still in L2, so the shard is read from DRAM once instead of once per
+    // peer (measured: a 134 MB shard was read 3.95x at W = 4), at one copy
+    // start per piece and peer.  Auto (ce_ag_piece < 0): 32 MB pieces for
+    // shards of 48-256 MB -- below that L2 already absorbs the re-reads,
+    // above it the extra copy starts cost more than the DRAM reads saved
+    // (T5-11B 134 MB shards: +2 %; GPT-30B 308 MB shards: -2 %, N = 4).
+    size_t ag_piece = 0;
+    if (kind == 0) {
+      if (c->ce_ag_piece > 0) ag_piece = (size_t)c->ce_ag_piece;
+      else if (c->ce_ag_piece < 0 && bytes > (48u << 20) && bytes <= (256u << 20)) ag_piece = 32u << 20;
+    }
+    const size_t piece = (ag_piece > 0 && bytes > ag_piece) ? (ag_piece + 255) / 256 * 256 : bytes;
     for (size_t off = 0; off < bytes; off += piece) {
       const size_t len = std::min(piece, bytes - off);
       for (int jj = 0; jj + 1 < gsize; ++jj) {

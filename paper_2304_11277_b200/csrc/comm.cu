@@ -1757,7 +1757,8 @@ static int ce_fork_join(fsdp_comm_t* c, int kind, cudaStream_t s, int gsize, int
     size_t ag_piece = 0;
     if (kind == 0) {
       if (c->ce_ag_piece > 0) ag_piece = (size_t)c->ce_ag_piece;
-      else if (c->ce_ag_piece < 0 && bytes > (48u << 20) && bytes <= (256u << 20)) ag_piece = 32u << 20;
+      else if (c->ce_ag_piece < 0 && gsize >= 3 && bytes > (48u << 20) && bytes <= (256u << 20))
+        ag_piece = 32u << 20;   // (with one peer there is no re-read to save)
     }
     const size_t piece = (ag_piece > 0 && bytes > ag_piece) ? (ag_piece + 255) / 256 * 256 : bytes;
     for (size_t off = 0; off < bytes; off += piece) {

@@ -14,10 +14,14 @@ token batch resident in HBM; `e2e` is the same through the public API with
 the token ids copied from pinned host memory and the loss read back every
 step.  Timing: CUDA events on the compute stream, barrier + synchronize on
 both sides, max over ranks; inputs (weights + optimizer state, >20 GB) are
-far larger than the 126 MB L2.
+far larger than the 126 MB L2.  The headline timed region carries no
+instrumentation; a second pass of the same K steps with CUDA events around
+every launch and wait gives the kernel timers (roofline) and stall breakdown.
+Without a launcher, --gpus N > 1 starts N ranks itself (torch.distributed.run).
 
 --impl reference times the reference algorithm (oracle port of shardsim,
-numpy + torch CPU) on this box's host cores on a bounded sample.
+numpy + torch CPU) on this box's host cores: one full sequence per simulated
+rank and step, N simulated ranks for --gpus N, same `config` as our arm.
 --mode sweep measures the flat-parameter all-gather / reduce-scatter bus
 bandwidth 1 MB..2 GB against NCCL (BASELINE configs[4]).
 """

@@ -76,7 +76,9 @@ def parse():
     ap.add_argument("--opt-split-first", type=int, default=2,
                     help="optimizer launch over the first N forward units first (0: one launch)")
     ap.add_argument("--exposed", action="store_true",
-                    help="also time the step with collectives replaced by no-ops")
+                    help="also time the step with collectives replaced by no-ops (default at N > 1)")
+    ap.add_argument("--no-exposed", action="store_true",
+                    help="skip the no-collectives pass at N > 1")
     ap.add_argument("--opt-in-bwd", action="store_true",
                     help="step each unit's shard in backward (measured: slower at N=1, "
                          "Adam contends for HBM with the backward kernels)")
@@ -297,7 +299,7 @@ def run_ours(args):
     ms_e2e = te0.elapsed_time(te1) / args.steps
     clocks = sampler.stop() if rank == 0 else None
     ms_nocomm = 0.0
-    if args.exposed and world > 1:
+    if (args.exposed or not args.no_exposed) and world > 1:
         # same step with every collective replaced by a no-op (values become
         # garbage; timing only): exposed comm = step - step_without_comm
         rt.cfg.fake_comm = True

@@ -104,8 +104,22 @@ def dist_env():
 
 
 def init_dist(world, local):
+    """Process group + NCCL communicator bring-up with fd 1 pointed at stderr:
+    NCCL prints its version banner straight to stdout when NCCL_DEBUG is set,
+    and stdout must carry exactly one JSON line."""
+    import torch.distributed as dist
     from paper_2304_11277_b200.dist_util import init_from_env
-    init_from_env()
+    sys.stdout.flush()
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    try:
+        init_from_env()
+        if world > 1:
+            dist.barrier()                 # eager communicator init happens here at the latest
+    finally:
+        sys.stdout.flush()
+        os.dup2(saved, 1)
+        os.close(saved)
 
 
 def self_launch(args) -> int:

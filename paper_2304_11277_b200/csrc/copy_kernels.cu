@@ -319,33 +319,9 @@ static int copy_grid(K kernel, int64_t nvec, int unroll) {
   return blocks < 1 ? 1 : (int)blocks;
 }
 
-// 2-byte to 2-byte flatten (the bf16 gradient write-back, every unit every
-// step): a quad is 8 bytes, so twice the vectors per thread keep the same
-// bytes in flight as the 4-byte cases (FSDP_COPY_U16=4 restores 4)
-static int u16_unroll() {
-  static int u = 0;
-  if (!u) {
-    const char* e = getenv("FSDP_COPY_U16");
-    u = (e && atoi(e) == 4) ? 4 : 8;
-  }
-  return u;
-}
-
 template <typename Tin, typename Tout>
 static void launch_flatten(const TensorTable& t, void* flat, int64_t psi, int acc, cudaStream_t s) {
   const int64_t nvec = ((psi + 255) >> 8) << 5;
-  if constexpr (sizeof(Tin) == 2 && sizeof(Tout) == 2) {
-    if (u16_unroll() == 8) {
-      if (acc) {
-        auto k = flatten_kernel<Tin, Tout, true, 8>;
-        k<<<copy_grid(k, nvec, 8), kCopyThreads, 0, s>>>(t, (Tout*)flat, psi);
-      } else {
-        auto k = flatten_kernel<Tin, Tout, false, 8>;
-        k<<<copy_grid(k, nvec, 8), kCopyThreads, 0, s>>>(t, (Tout*)flat, psi);
-      }
-      return;
-    }
-  }
   if (acc) {
     auto k = flatten_kernel<Tin, Tout, true, kCopyUnroll>;
     k<<<copy_grid(k, nvec, kCopyUnroll), kCopyThreads, 0, s>>>(t, (Tout*)flat, psi);

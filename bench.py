@@ -208,7 +208,7 @@ def run_ours(args):
                                                  T5DecoderBlock, T5EncoderBlock, param_init_fn)
 
     torch.backends.cuda.matmul.allow_tf32 = True
-    dev = torch.device("cuda", local)
+    dev = torch.device("cuda", torch.cuda.current_device())
     torch.manual_seed(1234)
     B = args.micro
     g = torch.Generator(device="cpu").manual_seed(1 + rank)
@@ -264,7 +264,7 @@ def run_ours(args):
     for _ in range(args.warmup):
         step(*dev_inputs)
     barrier()
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(torch.cuda.current_device())
     if rank == 0:
         sampler.start()
     # headline: no instrumentation inside the timed region (no per-launch
@@ -331,15 +331,14 @@ def run_ours(args):
     # per-rank no-comm step times: how far ranks drift apart on compute alone
     # (each GPU runs at its own clock under the power cap)
     spread = None
+    from paper_2304_11277_b200.dist_util import all_gather as _ag, all_reduce_ as _ar
     if world > 1 and ms_nocomm > 0:
-        allr = [torch.zeros(1, device=dev) for _ in range(world)]
-        dist.all_gather(allr, torch.tensor([ms_nocomm], device=dev))
-        v = [t.item() for t in allr]
+        v = [t.item() for t in _ag(torch.tensor([ms_nocomm], device=dev))]
         spread = {"ms_per_step_without_comm_per_rank": [round(x, 3) for x in v],
                   "spread_ms": round(max(v) - min(v), 3)}
     tmax = torch.tensor([ms, ms_e2e, ms_nocomm], device=dev)
     if world > 1:
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        _ar(tmax, op=dist.ReduceOp.MAX)
     ms, ms_e2e, ms_nocomm = tmax.tolist()
     tflops_gpu = flops_step / (ms * 1e-3) / 1e12
     value = tflops_gpu * world
@@ -480,7 +479,7 @@ def run_torch_unsharded(args):
     torch.cuda.set_device(local)
     from paper_2304_11277_b200.workloads import CONFIGS, GPT, param_init_fn
     torch.backends.cuda.matmul.allow_tf32 = True
-    dev = torch.device("cuda", local)
+    dev = torch.device("cuda", torch.cuda.current_device())
     cfg = CONFIGS[args.config]
     with torch.device("meta"):
         model = GPT(cfg)
@@ -504,7 +503,7 @@ def run_torch_unsharded(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(torch.cuda.current_device())
     sampler.start()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
@@ -628,7 +627,7 @@ def run_sweep(args):
     ll_dst = ll_comm.alloc(ll_max_mb << 20)
     ll_ag = ll_comm.alloc(4 * (ll_max_mb << 20), 16)
     ll_rs = ll_comm.alloc(4 * (ll_max_mb << 20), 16)
-    dev = torch.device("cuda", local)
+    dev = torch.device("cuda", torch.cuda.current_device())
     res = []
     for mb in sizes_mb:
         S = int(mb * (1 << 20))                 # unsharded bf16 bytes
@@ -721,7 +720,7 @@ def run_copy(args):
     torch.cuda.set_device(local)
     from paper_2304_11277_b200 import kernels
     from paper_2304_11277_b200.workloads import CONFIGS, T5_CONFIGS, Block, T5DecoderBlock
-    dev = torch.device("cuda", local)
+    dev = torch.device("cuda", torch.cuda.current_device())
     if args.config in T5_CONFIGS:
         c = T5_CONFIGS[args.config]
         with torch.device("meta"):

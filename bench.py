@@ -90,6 +90,9 @@ def parse():
                     help="HYBRID/NO_SHARD: all-reduce into a gather buffer + epilogue instead of in place")
     ap.add_argument("--no-w1-bf16-grad", action="store_true",
                     help="W=1: fp32 gradient write-back arena (Adam reads fp32 gradients)")
+    ap.add_argument("--check-replicas", action="store_true",
+                    help="after the timed steps, compare digests of the master / Adam shards across "
+                         "replicas (HYBRID_SHARD / NO_SHARD: ranks r, r+F hold the same shard)")
     ap.add_argument("--fused-cast-ag", action="store_true",
                     help="gather the fp32 master shard with the bf16 cast fused into the (SM/LL) "
                          "all-gather instead of the bf16 copy Adam writes (copy engines)")
@@ -195,6 +198,38 @@ def load_peaks():
 
 
 # --------------------------------------------------------------------------
+def replica_check(rt, world, dev):
+    """Size-independent property of the hybrid reduction at full size: the
+    replicated group's all-reduce leaves every replica of a shard (ranks r,
+    r + F, ...; collectives.py:63-72) bit-identical in master weights and Adam
+    state, although each rank trained on its own token ids.  Digest = wrapped
+    int64 sums of the fp32 bit patterns, plain and position-weighted, per arena."""
+    import torch
+    from paper_2304_11277_b200.dist_util import all_gather as _ag
+    F = rt.plan.shard_factor
+    arenas = [a for a in (rt.master, rt.exp_avg, rt.exp_avg_sq) if a is not None]
+    dig = []
+    chunk = 1 << 26
+    for a in arenas:
+        s0 = torch.zeros((), dtype=torch.int64, device=dev)
+        s1 = torch.zeros((), dtype=torch.int64, device=dev)
+        for off in range(0, a.numel(), chunk):
+            x = a[off:off + chunk].view(torch.int32).to(torch.int64)
+            w = torch.arange(off, off + x.numel(), device=dev, dtype=torch.int64) % 65521 + 1
+            s0 += x.sum()
+            s1 += (x * w).sum()
+        dig += [s0, s1]
+    mine = torch.stack(dig)
+    every = [t.tolist() for t in _ag(mine)]
+    groups = {}
+    for r in range(world):
+        groups.setdefault(r % F, []).append(r)
+    ok = all(every[r] == every[grp[0]] for grp in groups.values() for r in grp)
+    differs = len({tuple(every[grp[0]]) for grp in groups.values()}) == len(groups)
+    return {"replica_groups": list(groups.values()), "identical_within_groups": ok,
+            "shards_differ_across_positions": differs, "arenas": ["master", "exp_avg", "exp_avg_sq"][:len(arenas)]}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -312,6 +347,7 @@ def run_ours(args):
     barrier()
     ms_e2e = te0.elapsed_time(te1) / args.steps
     clocks = sampler.stop() if rank == 0 else None
+    replicas = replica_check(rt, world, dev) if args.check_replicas and world > 1 else None
     ms_nocomm = 0.0
     if (args.exposed or not args.no_exposed) and world > 1:
         # same step with every collective replaced by a no-op (values become
@@ -421,6 +457,7 @@ def run_ours(args):
                     "h2d_bytes_per_step": int(sum(h.numel() * h.element_size() for h in host)),
                     "d2h_bytes_per_step": 4, "ms_per_step": round(ms_e2e, 3)},
             "gpu_launches": int(launches), "clocks": clocks, "loss": round(losses[-1], 4),
+            **({"replica_check": replicas} if replicas is not None else {}),
             **({"comm_stalls": stalls,
                 "comm_stalls_top_units": {k: [{"unit": u, "ms_total": t, "waits": c} for u, t, c in v]
                                           for k, v in stall_units.items()}} if stalls else {}),

@@ -90,6 +90,9 @@ def parse():
                     help="HYBRID/NO_SHARD: all-reduce into a gather buffer + epilogue instead of in place")
     ap.add_argument("--no-w1-bf16-grad", action="store_true",
                     help="W=1: fp32 gradient write-back arena (Adam reads fp32 gradients)")
+    ap.add_argument("--hybrid-stage2", choices=["fp32", "reduce"], default="fp32",
+                    help="HYBRID_SHARD all-reduce payload: fp32 partial sums (default) or the partial "
+                         "rounded to the reduce dtype (bf16), as the reference and torch FSDP send it")
     ap.add_argument("--check-replicas", action="store_true",
                     help="after the timed steps, compare digests of the master / Adam shards across "
                          "replicas (HYBRID_SHARD / NO_SHARD: ranks r, r+F hold the same shard)")
@@ -277,6 +280,7 @@ def run_ours(args):
         ag_ctas=args.ctas, rs_ctas=args.rs_ctas, ag_engine=args.ag_engine,
         rs_engine=args.rs_engine, tail_engine=args.tail_engine, ll_max_bytes=args.ll_max_bytes,
         opt_split_first=args.opt_split_first, fused_cast_ag=args.fused_cast_ag,
+        hybrid_stage2=args.hybrid_stage2,
         ar_in_pool=not args.no_ar_pool, w1_bf16_grad=not args.no_w1_bf16_grad,
         opt_split_geom={"auto": None, "on": True, "off": False}[args.opt_split_geom])
     opt = fsdp.optimizer()
@@ -498,6 +502,7 @@ def step_config(args, world: int) -> dict:
                             "low_latency_max_bytes": args.ll_max_bytes},
             "opt_split_first": args.opt_split_first,
             **({"fused_cast_ag": True} if args.fused_cast_ag else {}),
+            **({"hybrid_stage2": args.hybrid_stage2} if args.strategy == "HYBRID_SHARD" else {}),
             **({"ar_in_pool": False} if args.no_ar_pool else {}),
             "opt_split_geom": args.opt_split_geom,
             **({"w1_bf16_grad": False} if args.no_w1_bf16_grad else {}),

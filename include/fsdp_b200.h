@@ -240,6 +240,14 @@ int fsdp_allgather_ce(fsdp_comm_t* c, int channel, int gsize, int gstride, const
 int fsdp_reduce_scatter_ce(fsdp_comm_t* c, int channel, int gsize, int gstride, int64_t src_off,
                            int src_dtype, int64_t n, int64_t stage_off, float* out, float prediv,
                            float postdiv, int accumulate, void* stream);
+/* Same, with the result in out_dtype (FSDP_F32, or FSDP_BF16 = the fp32 sum
+ * / postdiv rounded once to bf16, accumulate = 0): HYBRID_SHARD's stage-1
+ * partial in the reduce dtype, which is what the reference sends to the
+ * replica all-reduce (engine.py:789-790, :798-810: the reduce-scatter output
+ * is the all-reduce payload). */
+int fsdp_reduce_scatter_ce_out(fsdp_comm_t* c, int channel, int gsize, int gstride, int64_t src_off,
+                               int src_dtype, int64_t n, int64_t stage_off, void* out, int out_dtype,
+                               float prediv, float postdiv, int accumulate, void* stream);
 
 /* All-reduce (collectives.py:298-301; hybrid stage 2, engine.py:804-816):
  * two-shot push (reduce-scatter to owners, ascending-rank fp32 sum, then

@@ -220,9 +220,13 @@ def all_reduce(inputs: Sequence[np.ndarray], acc_dtype=None) -> np.ndarray:
     return fabric_reduce(inputs, acc_dtype)
 
 
-def hybrid_reduce(grads: Sequence[np.ndarray], plan: Plan, acc_dtype=None) -> list:
+def hybrid_reduce(grads: Sequence[np.ndarray], plan: Plan, acc_dtype=None, stage2_dtype=None) -> list:
     """collectives.py:377-397 (Eq. 1): RS in the sharded group, then AR in
-    the replicated group; degenerates to RS at F=W and AR at F=1."""
+    the replicated group; degenerates to RS at F=W and AR at F=1.
+
+    stage2_dtype: the partial is cast to it before the all-reduce (the
+    reference's flow: the reduce-scatter output, in the payload dtype, is the
+    all-reduce payload, engine.py:798-810); None keeps the acc_dtype partial."""
     w, f = plan.world_size, plan.shard_factor
     out = [None] * w
     if f == 1:
@@ -232,7 +236,7 @@ def hybrid_reduce(grads: Sequence[np.ndarray], plan: Plan, acc_dtype=None) -> li
     for g in plan.sharded_groups:
         res = reduce_scatter([grads[r] for r in g], acc_dtype)
         for pos, r in enumerate(g):
-            partial[r] = res[pos]
+            partial[r] = res[pos] if stage2_dtype is None or f == w else cast(res[pos], stage2_dtype)
     if f == w:
         return partial
     for g in plan.replicated_groups:
@@ -267,14 +271,14 @@ def writeback_grad(layout: UnitLayout, grads: dict, dtype, out=None):
 
 def reduce_unit(flat_grads: Sequence[np.ndarray], plan: Plan, *, reduce_dtype,
                 full_dtype, acc_dtype=None, mean: bool = True,
-                accum: Sequence[np.ndarray] | None = None) -> list:
+                accum: Sequence[np.ndarray] | None = None, stage2_dtype=None) -> list:
     """engine.py:787-820 for every rank at once: payload = grad in the reduce
     dtype (:789-790); RS in the sharded group then AR in the replicated group
     (:798-816); astype(full) (:817); / W when the loss is a mean (:818-819);
     accum += (:820; a fresh accumulator starts at zeros, :791-796)."""
     w = plan.world_size
     payload = [cast(g, reduce_dtype) for g in flat_grads]
-    reduced = hybrid_reduce(payload, plan, acc_dtype)
+    reduced = hybrid_reduce(payload, plan, acc_dtype, stage2_dtype)
     out = []
     for r in range(w):
         red = np.asarray(reduced[r]).astype(full_dtype)
@@ -621,14 +625,15 @@ def fsdp_reduce_and_step(flat_grads_by_rank, shards_by_rank, plan: Plan, *,
                          optimizer="adam", opt_states=None, lr=None,
                          betas=(0.9, 0.999), eps=1e-8, mean=True,
                          reduce_dtype=BF16, full=np.float32, acc_dtype=np.float32,
-                         scale: float | None = None):
+                         scale: float | None = None, stage2_dtype=None):
     """The B200 build's epilogue for one unit and one step, every rank:
     payload cast -> RS(+AR) with fp32 accumulation -> / W -> unscale ->
     world verdict -> optimizer on the shard.  (engine.py:771-820, :563-589.)
     Mutates shards/opt_states in place; returns (accums, found_inf)."""
     w = plan.world_size
     accums = reduce_unit(flat_grads_by_rank, plan, reduce_dtype=reduce_dtype,
-                         full_dtype=full, acc_dtype=acc_dtype, mean=mean)
+                         full_dtype=full, acc_dtype=acc_dtype, mean=mean,
+                         stage2_dtype=stage2_dtype)
     found = False
     if scale is not None:
         flags = [unscale_and_check([accums[r]], scale) for r in range(w)]

@@ -88,6 +88,8 @@ _SIGS = {
     "fsdp_allgather_ce": (_i32, [_vp, _i32, _i32, _i32, _vp, _i32, _i64, _i64, _vp]),
     "fsdp_reduce_scatter_ce": (_i32, [_vp, _i32, _i32, _i32, _i64, _i32, _i64, _i64, _vp, _f32,
                                       _f32, _i32, _vp]),
+    "fsdp_reduce_scatter_ce_out": (_i32, [_vp, _i32, _i32, _i32, _i64, _i32, _i64, _i64, _vp, _i32,
+                                          _f32, _f32, _i32, _vp]),
     "fsdp_allreduce": (_i32, [_vp, _i32, _i32, _i32, _vpp, _i32, _i64, _i64, _i64, _vpp, _f32,
                               _i32, _vp]),
     "fsdp_allreduce_ce": (_i32, [_vp, _i32, _i32, _i32, _vp, _i32, _i64, _i64, _i64, _vp, _f32, _i32, _vp]),

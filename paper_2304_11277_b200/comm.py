@@ -416,11 +416,13 @@ class DeviceComm:
     def reduce_scatter_ce(self, gdesc, src_off: int, src_dtype: torch.dtype, stage_off: int,
                           out: torch.Tensor, prediv: float = 1.0, postdiv: float = 1.0,
                           accumulate: bool = False, stream=None, channel: int = _lib.CH_RS) -> None:
-        """Copy-engine pull of the peers' chunks + local ascending fp32 reduction."""
-        check(lib.fsdp_reduce_scatter_ce(self._h, channel, gdesc[0], gdesc[1], src_off,
-                                         dtype_code(src_dtype), out.numel(), stage_off,
-                                         out.data_ptr(), float(prediv), float(postdiv),
-                                         int(accumulate), stream_ptr(stream)), "reduce_scatter_ce")
+        """Copy-engine pull of the peers' chunks + local ascending fp32 reduction
+        (`out` fp32, or bf16: the sum rounded once, no accumulate)."""
+        check(lib.fsdp_reduce_scatter_ce_out(self._h, channel, gdesc[0], gdesc[1], src_off,
+                                             dtype_code(src_dtype), out.numel(), stage_off,
+                                             out.data_ptr(), dtype_code(out.dtype), float(prediv),
+                                             float(postdiv), int(accumulate), stream_ptr(stream)),
+              "reduce_scatter_ce")
 
     def all_reduce(self, gdesc, ins: Sequence[torch.Tensor], stage_off: int, gather_off: int,
                    outs: Sequence[torch.Tensor], postdiv: float = 1.0, accumulate: bool = False,

@@ -325,21 +325,24 @@ struct CeReduceArgs {
   const void* own;        // own payload, chunk pos (element 0 of the chunk)
   const void* stage;      // staging base (slot 0, element 0)
   int64_t stride;         // elements between staging slots (= chunk length n)
-  float* out;             // output chunk (element 0)
+  void* out;              // output chunk (element 0): fp32, or bf16 when out_bf16
   int64_t e0, len;        // this piece
   int gsize, pos;
   float prediv, postdiv;
   int accumulate;
   int store_raw;          // 1: out = sum/postdiv as is (all-reduce owner phase), else (acc ? out : 0) + that
+  int out_bf16;           // 1: the fp32 result is rounded to bf16 (hybrid stage-1 partial; no accumulate)
 };
 
-template <typename Tin, int MAXW>
+// Tout = bf16: the reduce-scatter result is the next stage's payload
+// (hybrid stage 2 in the reduce dtype); the fp32 value is rounded once.
+template <typename Tin, typename Tout, int MAXW>
 __global__ void __launch_bounds__(256)
 ce_reduce_kernel(const __grid_constant__ CeReduceArgs a) {
   constexpr int U = 2;                                 // vectors per thread per iteration
   const Tin* own = (const Tin*)a.own + a.e0;
   const Tin* stage = (const Tin*)a.stage + a.e0;
-  float* __restrict__ out = a.out + a.e0;
+  Tout* __restrict__ out = (Tout*)a.out + a.e0;
   const int64_t n = a.len;
   const bool pre = a.prediv != 1.0f, post = a.postdiv != 1.0f;
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
@@ -372,13 +375,13 @@ ce_reduce_kernel(const __grid_constant__ CeReduceArgs a) {
           for (int q = 0; q < 8; ++q) acc.v[q] = __fadd_rn(acc.v[q], pre ? __fdiv_rn(x.v[q], a.prediv) : x.v[q]);
         }
         V8F base;
-        if (a.accumulate) base = unpack8<float>(ldcg8<float>(out + v * kVec));
+        if (a.accumulate) base = unpack8<Tout>(ldcg8<Tout>(out + v * kVec));
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const float rr = post ? __fdiv_rn(acc.v[q], a.postdiv) : acc.v[q];
           acc.v[q] = a.store_raw ? rr : __fadd_rn(a.accumulate ? base.v[q] : 0.0f, rr);
         }
-        st8<float>(out + v * kVec, pack8<float>(acc));
+        st8<Tout>(out + v * kVec, pack8<Tout>(acc));
       }
     }
   } else {
@@ -389,7 +392,7 @@ ce_reduce_kernel(const __grid_constant__ CeReduceArgs a) {
         acc = __fadd_rn(acc, pre ? __fdiv_rn(x, a.prediv) : x);
       }
       const float r = post ? __fdiv_rn(acc, a.postdiv) : acc;
-      out[i] = a.store_raw ? r : __fadd_rn(a.accumulate ? out[i] : 0.0f, r);
+      out[i] = from_f<Tout>(a.store_raw ? r : __fadd_rn(a.accumulate ? to_f<Tout>(out[i]) : 0.0f, r));
     }
   }
 }
@@ -1690,14 +1693,25 @@ static int launch_ce_reduce(CeReduceArgs ra, int64_t e0, int64_t len, int src_dt
   int grid = (int)std::min<int64_t>((nv + 255) / 256, (int64_t)kNumSMs * 4);
   if (grid_cap > 0) grid = std::min(grid, grid_cap);
   const int mw = ra.gsize <= 2 ? 2 : (ra.gsize <= 4 ? 4 : 8);
-  if (src_dtype == FSDP_BF16) {
-    if (mw == 2) ce_reduce_kernel<__nv_bfloat16, 2><<<grid, 256, 0, s>>>(ra);
-    else if (mw == 4) ce_reduce_kernel<__nv_bfloat16, 4><<<grid, 256, 0, s>>>(ra);
-    else ce_reduce_kernel<__nv_bfloat16, 8><<<grid, 256, 0, s>>>(ra);
+  using bf = __nv_bfloat16;
+  if (ra.out_bf16) {
+    if (src_dtype == FSDP_BF16) {
+      if (mw == 2) ce_reduce_kernel<bf, bf, 2><<<grid, 256, 0, s>>>(ra);
+      else if (mw == 4) ce_reduce_kernel<bf, bf, 4><<<grid, 256, 0, s>>>(ra);
+      else ce_reduce_kernel<bf, bf, 8><<<grid, 256, 0, s>>>(ra);
+    } else {
+      if (mw == 2) ce_reduce_kernel<float, bf, 2><<<grid, 256, 0, s>>>(ra);
+      else if (mw == 4) ce_reduce_kernel<float, bf, 4><<<grid, 256, 0, s>>>(ra);
+      else ce_reduce_kernel<float, bf, 8><<<grid, 256, 0, s>>>(ra);
+    }
+  } else if (src_dtype == FSDP_BF16) {
+    if (mw == 2) ce_reduce_kernel<bf, float, 2><<<grid, 256, 0, s>>>(ra);
+    else if (mw == 4) ce_reduce_kernel<bf, float, 4><<<grid, 256, 0, s>>>(ra);
+    else ce_reduce_kernel<bf, float, 8><<<grid, 256, 0, s>>>(ra);
   } else {
-    if (mw == 2) ce_reduce_kernel<float, 2><<<grid, 256, 0, s>>>(ra);
-    else if (mw == 4) ce_reduce_kernel<float, 4><<<grid, 256, 0, s>>>(ra);
-    else ce_reduce_kernel<float, 8><<<grid, 256, 0, s>>>(ra);
+    if (mw == 2) ce_reduce_kernel<float, float, 2><<<grid, 256, 0, s>>>(ra);
+    else if (mw == 4) ce_reduce_kernel<float, float, 4><<<grid, 256, 0, s>>>(ra);
+    else ce_reduce_kernel<float, float, 8><<<grid, 256, 0, s>>>(ra);
   }
   FSDP_LAUNCHED();
   return 0;
@@ -1831,14 +1845,19 @@ extern "C" int fsdp_allgather_ce(fsdp_comm_t* c, int channel, int gsize, int gst
   return launch(c, coll_signal_exit_kernel, p, 1, 32, s);   // my copies landed; so did everyone's
 }
 
-extern "C" int fsdp_reduce_scatter_ce(fsdp_comm_t* c, int channel, int gsize, int gstride,
-                                      int64_t src_off, int src_dtype, int64_t n,
-                                      int64_t stage_off, float* out, float prediv, float postdiv,
-                                      int accumulate, void* stream) {
+extern "C" int fsdp_reduce_scatter_ce_out(fsdp_comm_t* c, int channel, int gsize, int gstride,
+                                          int64_t src_off, int src_dtype, int64_t n,
+                                          int64_t stage_off, void* out, int out_dtype, float prediv,
+                                          float postdiv, int accumulate, void* stream) {
   if (int rc = validate_group(c, channel, gsize, gstride)) return rc;
   if (c->emulated) return fail(FSDP_E_UNSUPPORTED, "copy-engine collectives need a real communicator");
   const int es = elem_size(src_dtype);
   if (n < 0 || !out || !es) return fail(FSDP_E_INVALID, "fsdp_reduce_scatter_ce: bad args");
+  if (out_dtype != FSDP_F32 && out_dtype != FSDP_BF16)
+    return fail(FSDP_E_INVALID, "fsdp_reduce_scatter_ce: out dtype must be fp32 or bf16");
+  const bool out_bf16 = out_dtype == FSDP_BF16;
+  if (out_bf16 && accumulate)
+    return fail(FSDP_E_INVALID, "fsdp_reduce_scatter_ce: a bf16 result cannot accumulate");
   if (!(prediv > 0.f) || !(postdiv > 0.f)) return fail(FSDP_E_INVALID, "divisors must be > 0");
   if (int rc = check_range(c, src_off, n * gsize * es, "fsdp_reduce_scatter_ce(src)")) return rc;
   if (int rc = check_range(c, stage_off, n * gsize * es, "fsdp_reduce_scatter_ce(stage)")) return rc;
@@ -1863,6 +1882,7 @@ extern "C" int fsdp_reduce_scatter_ce(fsdp_comm_t* c, int channel, int gsize, in
   ra.gsize = gsize; ra.pos = pos;
   ra.prediv = prediv; ra.postdiv = postdiv; ra.accumulate = accumulate ? 1 : 0;
   ra.store_raw = 0;
+  ra.out_bf16 = out_bf16 ? 1 : 0;
   cudaEvent_t a = nullptr, b = nullptr;
   if (c->timing) { a = take_event(c); b = take_event(c); FSDP_CUDA(cudaEventRecord(a, s)); }
 
@@ -1881,7 +1901,7 @@ extern "C" int fsdp_reduce_scatter_ce(fsdp_comm_t* c, int channel, int gsize, in
   // move [0, nA) of every chunk while an SM TMA-pull kernel reduces [nA, n)
   // straight from the peers' payloads on a third side stream, so the tail of
   // the chunk needs no staging round trip.
-  const bool hyb = c->ce_rs_sm_frac > 0.f && c->ce_serial && n >= c->ce_rs_pipe_min &&
+  const bool hyb = c->ce_rs_sm_frac > 0.f && !out_bf16 && c->ce_serial && n >= c->ce_rs_pipe_min &&
                    c->ce_rs_push != 0 && (n % kVec == 0) && (src_off % 16 == 0) && aligned16(out);
   const int64_t nA = hyb ? std::min(n, round8((int64_t)((double)n * (1.0 - c->ce_rs_sm_frac)))) : n;
   if (!c->ce_serial || n < c->ce_rs_pipe_min) {
@@ -1935,7 +1955,7 @@ extern "C" int fsdp_reduce_scatter_ce(fsdp_comm_t* c, int channel, int gsize, in
       p2.n = n - nA;
       p2.off_a = src_off + nA * es;
       p2.off_b = n;                                  // members' chunks stay n elements apart
-      p2.out[0] = out + nA;
+      p2.out[0] = (float*)out + nA;
       p2.prediv = prediv; p2.postdiv = postdiv; p2.accumulate = accumulate ? 1 : 0;
       p2.split = 0;
       const int64_t T = (kTmaStageBytes / (gsize * es)) / kVec * kVec;
@@ -2083,7 +2103,7 @@ static int allreduce_ce_impl(fsdp_comm_t* c, int channel, int gsize, int gstride
   ra.stride = ch;
   ra.out = (float*)(mine + res_off) + (int64_t)pos * ch;
   ra.gsize = gsize; ra.pos = pos;
-  ra.prediv = 1.0f; ra.postdiv = postdiv; ra.accumulate = 0; ra.store_raw = 1;
+  ra.prediv = 1.0f; ra.postdiv = postdiv; ra.accumulate = 0; ra.store_raw = 1; ra.out_bf16 = 0;
   if (int rc = launch_ce_reduce(ra, 0, clen(pos), src_dtype, c->ce_reduce_cap, s)) return rc;
   // 3. all-gather push of my reduced chunk
   cudaEvent_t reduced = ce_event(c);
@@ -2113,6 +2133,13 @@ static int allreduce_ce_impl(fsdp_comm_t* c, int channel, int gsize, int gstride
   return 0;
 }
 
+extern "C" int fsdp_reduce_scatter_ce(fsdp_comm_t* c, int channel, int gsize, int gstride,
+                                      int64_t src_off, int src_dtype, int64_t n,
+                                      int64_t stage_off, float* out, float prediv, float postdiv,
+                                      int accumulate, void* stream) {
+  return fsdp_reduce_scatter_ce_out(c, channel, gsize, gstride, src_off, src_dtype, n, stage_off, out,
+                                    FSDP_F32, prediv, postdiv, accumulate, stream);
+}
 extern "C" int fsdp_allreduce_ce(fsdp_comm_t* c, int channel, int gsize, int gstride, const void* in,
                                  int src_dtype, int64_t n, int64_t stage_off, int64_t gather_off,
                                  float* out, float postdiv, int accumulate, void* stream) {

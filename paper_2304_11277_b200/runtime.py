@@ -145,6 +145,14 @@ class RuntimeConfig:
     # the bf16 copy's memory; the gather reads 4 B/elem instead of 2 and runs
     # on SMs.  Same bits either way (cast-then-gather == gather-then-cast).
     fused_cast_ag: bool = False
+    # HYBRID_SHARD stage-2 payload: "fp32" sends the fp32 partial sums of the
+    # reduce-scatter to the replica all-reduce (this build's default: one
+    # rounding, at the very end); "reduce" rounds the partial once to the
+    # reduce dtype and all-reduces that, as the reference does (its
+    # reduce-scatter output is the all-reduce payload, engine.py:798-810) and
+    # as torch FSDP does: half the all-reduce bytes and HBM traffic.  Sums stay
+    # fp32 and ascending in both.
+    hybrid_stage2: str = "fp32"
 
     def __post_init__(self):
         if self.reshard_after_forward not in (RAF, NRAF):
@@ -157,6 +165,8 @@ class RuntimeConfig:
             raise EngineError("backward_prefetch must be None, 'pre' or 'post'")
         if self.comm_backend not in ("ipc", "nccl"):
             raise EngineError("comm_backend must be 'ipc' or 'nccl'")
+        if self.hybrid_stage2 not in ("fp32", "reduce"):
+            raise EngineError("hybrid_stage2 must be 'fp32' or 'reduce'")
 
 
 class _Window:
@@ -1079,9 +1089,18 @@ class FSDPRuntime:
 
     def _rs(self, gslot: int, dtype: torch.dtype, out: torch.Tensor, pre: float, post: float,
             accumulate: bool, tail: bool = False) -> None:
-        """Reduce-scatter of the payload in symmetric gradient slot `gslot`."""
+        """Reduce-scatter of the payload in symmetric gradient slot `gslot`
+        into `out` (fp32; or bf16: the fp32 sum rounded once)."""
         F = self.plan.shard_factor
-        if self.ll_rs_off is not None and out.numel() * F * self.compute_dtype.itemsize <= self.cfg.ll_max_bytes:
+        ll = self.ll_rs_off is not None and out.numel() * F * self.compute_dtype.itemsize <= self.cfg.ll_max_bytes
+        sm_tail = tail and self.cfg.tail_engine == "sm"
+        if out.dtype != torch.float32 and (ll or sm_tail or self.cfg.rs_engine != "ce"):
+            # the SM / LL kernels write fp32: reduce there, then round once
+            t32 = torch.empty(out.numel(), dtype=torch.float32, device=self.device)
+            self._rs(gslot, dtype, t32, pre, post, accumulate, tail)
+            kernels.cast(t32, out, stream=self.rs_stream)
+            return
+        if ll:
             # same unit-size criterion as the all-gather (psi = F * shard length)
             flat = self.comm.view(self.gslot_offs[gslot], out.numel() * F, dtype)
             self.comm.reduce_scatter_ll(self.plan.sharded_desc, [flat], self.ll_rs_off, [out], prediv=pre,
@@ -1179,15 +1198,16 @@ class FSDPRuntime:
                 with self.timed("allreduce", self.rs_stream, payload.numel() * payload.element_size()):
                     self._ar(payload, u.grad, post, accumulate)
             else:
-                tmp = torch.empty(n, dtype=torch.float32, device=self.device)
+                low2 = self.cfg.hybrid_stage2 == "reduce" and payload.dtype != torch.float32
+                tmp = torch.empty(n, dtype=payload.dtype if low2 else torch.float32, device=self.device)
                 with self.timed("reduce_scatter", self.rs_stream, payload.numel() * payload.element_size()):
                     self._rs(gslot, payload.dtype, tmp, pre, 1.0, False, tail)
                 self.events.append((self.step_count, "reduce_stage2", uid))
-                self.trace.record("AR_issue", uid, n * 4)
+                self.trace.record("AR_issue", uid, n * tmp.element_size())
                 rs_done = torch.cuda.Event()
                 rs_done.record(self.rs_stream)
                 self.ar_stream.wait_event(rs_done)
-                with self.timed("allreduce", self.ar_stream, n * 4):
+                with self.timed("allreduce", self.ar_stream, n * tmp.element_size()):
                     self._ar(tmp, u.grad, post, accumulate, stream=self.ar_stream)
                 tmp.record_stream(self.ar_stream)
             payload.record_stream(self.rs_stream)

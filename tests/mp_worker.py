@@ -205,6 +205,7 @@ def ce_schedules(rank, world, results):
         exp_ag = sp.cast(sp.all_gather(shards), sp.BF16)
         exp_rs = sp.reduce_unit(grads, sp.Plan(world, world), reduce_dtype=sp.BF16, full_dtype=np.float32,
                                 acc_dtype=np.float32, mean=True, accum=acc0)
+        exp_rs_b = sp.cast(sp.reduce_scatter(grads, np.float32)[rank], sp.BF16)
         os.environ["FSDP_CE_SERIAL"], os.environ["FSDP_CE_RS_PUSH"] = str(serial), str(push)
         os.environ["FSDP_CE_RS_MIN_PIECE"] = str(minp or (4 << 20))
         os.environ["FSDP_CE_RS_PIPE_MIN"] = str(2 * minp if minp else (64 << 20))
@@ -226,6 +227,11 @@ def ce_schedules(rank, world, results):
                                        accumulate=True)
                 check(out.cpu().numpy().tobytes() == exp_rs[rank].tobytes(),
                       f"RS-CE serial={serial} push={push}")
+                # bf16 result (hybrid stage-1 partial in the reduce dtype): the
+                # ascending fp32 sum rounded once
+                outb = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+                comm.reduce_scatter_ce((world, 1), b, torch.bfloat16, st, outb)
+                check(np.array_equal(outb.float().cpu().numpy(), exp_rs_b), f"RS-CE bf16 out serial={serial} push={push}")
             torch.cuda.synchronize()
             check(comm.device_error() == 0, "device error word (CE)")
         finally:
@@ -325,7 +331,8 @@ def nvls_collectives(rank, world, results):
 
 
 def fsdp_step_parity(rank, world, strategy, hybrid, results, backend="ipc", opt_in_bwd=False,
-                     engine="ce", ll=False, fused=False, num_slots=None, split_geom=False):
+                     engine="ce", ll=False, fused=False, num_slots=None, split_geom=False,
+                     stage2="fp32"):
     """ll=False pins every unit to `engine` (the tiny GPT's units are all
     small enough for the low-latency path, which ll=True exercises)."""
     from paper_2304_11277_b200 import kernels  # noqa: F401
@@ -342,7 +349,7 @@ def fsdp_step_parity(rank, world, strategy, hybrid, results, backend="ipc", opt_
                                     rs_engine="sm" if engine == "nvls" else engine,
                                     ll_max_bytes=(6 << 20) if ll else 0, fused_cast_ag=fused,
                                     num_slots=num_slots, opt_split_first=1 if split_geom else 2,
-                                    opt_split_geom=split_geom)
+                                    opt_split_geom=split_geom, hybrid_stage2=stage2)
     plan = fsdp.plan
     ref = init_gpt_(GPT(cfg), seed=0).cuda().to(torch.bfloat16)
     x, y = synthetic_batch(cfg, 2, seed=100 + rank, device="cuda")
@@ -352,7 +359,8 @@ def fsdp_step_parity(rank, world, strategy, hybrid, results, backend="ipc", opt_
     lref.backward()
     key = (f"{strategy}{'' if hybrid is None else hybrid}/{backend}/{'ll' if ll else engine}"
            f"{'/opt-in-bwd' if opt_in_bwd else ''}{'/fused-cast-ag' if fused else ''}"
-           f"{'' if num_slots is None else '/slots%d' % num_slots}{'/opt-split-geom' if split_geom else ''}")
+           f"{'' if num_slots is None else '/slots%d' % num_slots}{'/opt-split-geom' if split_geom else ''}"
+           f"{'/stage2-reduce-dtype' if stage2 == 'reduce' else ''}")
     torch.cuda.synchronize()
     # initial shards from the oracle (flatten + shard of the same init)
     vals = {k: v.detach().float().cpu().numpy() for k, v in init_gpt_(GPT(cfg), seed=0).named_parameters()}
@@ -365,7 +373,8 @@ def fsdp_step_parity(rank, world, strategy, hybrid, results, backend="ipc", opt_
             flat = sp.writeback_grad(lay, g, np.float32)[0]
             flats = gather_np(flat)
             exp = sp.reduce_unit(flats, sp.Plan(plan.world_size, plan.shard_factor), reduce_dtype=sp.BF16,
-                                 full_dtype=np.float32, acc_dtype=np.float32, mean=True)
+                                 full_dtype=np.float32, acc_dtype=np.float32, mean=True,
+                                 stage2_dtype=sp.BF16 if stage2 == "reduce" else None)
             check(u.grad.cpu().numpy().tobytes() == exp[rank].tobytes(),
                   f"{key}: reduced grad of unit {lay.unit_id}")
     fsdp.optimizer().step()
@@ -716,6 +725,10 @@ def main():
             steps += [("HYBRID_SHARD", f, {"engine": "nvls"}) for f in hybrids]
         steps += [("HYBRID_SHARD", f, {"engine": "sm"}) for f in hybrids]
         steps += [("HYBRID_SHARD", f, {"opt_in_bwd": True}) for f in hybrids]
+        # stage-2 payload in the reduce dtype: copy-engine reduce-scatter
+        # writing bf16, the SM tail and the LL path through fp32 + one rounding
+        steps += [("HYBRID_SHARD", f, {"stage2": "reduce"}) for f in hybrids]
+        steps += [("HYBRID_SHARD", f, {"stage2": "reduce", "ll": True}) for f in hybrids[:1]]
         if not SHARED:
             steps += [("FULL_SHARD", None, {"backend": "nccl"})]
         scen = [("raw_collectives", raw_collectives), ("full_size_properties", full_size_properties),

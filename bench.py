@@ -90,9 +90,10 @@ def parse():
                     help="HYBRID/NO_SHARD: all-reduce into a gather buffer + epilogue instead of in place")
     ap.add_argument("--no-w1-bf16-grad", action="store_true",
                     help="W=1: fp32 gradient write-back arena (Adam reads fp32 gradients)")
-    ap.add_argument("--hybrid-stage2", choices=["fp32", "reduce"], default="fp32",
-                    help="HYBRID_SHARD all-reduce payload: fp32 partial sums (default) or the partial "
-                         "rounded to the reduce dtype (bf16), as the reference and torch FSDP send it")
+    ap.add_argument("--hybrid-stage2", choices=["fp32", "reduce"], default="reduce",
+                    help="HYBRID_SHARD all-reduce payload: the partial rounded to the reduce dtype "
+                         "(bf16; the wrapper's default, as the reference and torch FSDP send it) or "
+                         "the fp32 partial sums")
     ap.add_argument("--check-replicas", action="store_true",
                     help="after the timed steps, compare digests of the master / Adam shards across "
                          "replicas (HYBRID_SHARD / NO_SHARD: ranks r, r+F hold the same shard)")

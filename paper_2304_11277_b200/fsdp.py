@@ -26,6 +26,11 @@ Mapping to the reference engine (`engine.py:165-207`, EngineConfig):
   keep_outermost_unsharded=         keep_outermost_unsharded (default True, as torch)
   MixedPrecision(param_dtype=bf16)  PrecisionPolicy(mixed=True)
   MixedPrecision(reduce_dtype=fp32) PrecisionPolicy(reduce_in_low=False)
+  hybrid_stage2="reduce" (default)  HYBRID's replica all-reduce moves the
+                                    reduce-scatter's partial in the reduce dtype
+                                    (as torch FSDP and engine.py:798-810; sums
+                                    in fp32); "fp32" keeps fp32 partials (the
+                                    Session / RuntimeConfig default)
   no_sync()                         accumulation = no_comm (engine.py:547-556)
   (root unit kept after forward)    keep_outermost_unsharded = True
 
@@ -144,7 +149,7 @@ class FullyShardedDataParallel(nn.Module):
                  tail_engine: str = "sm", ll_max_bytes: int = 6 << 20, opt_split_first: int = 2,
                  rate_limit: int | None | str = "auto", keep_outermost_unsharded: bool = True,
                  fused_cast_ag: bool = False, ar_in_pool: bool = True, w1_bf16_grad: bool = True,
-                 opt_split_geom: bool | None = None, hybrid_stage2: str = "fp32"):
+                 opt_split_geom: bool | None = None, hybrid_stage2: str = "reduce"):
         super().__init__()
         if cpu_offload is not None and cpu_offload.offload_params:
             raise NotImplementedError("CPU offload is out of scope for the B200 runtime")

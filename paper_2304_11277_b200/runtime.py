@@ -153,12 +153,6 @@ class RuntimeConfig:
     # as torch FSDP does: half the all-reduce bytes and HBM traffic.  Sums stay
     # fp32 and ascending in both.
     hybrid_stage2: str = "fp32"
-    # W > 1: the gradient write-back of a unit (autograd's per-parameter
-    # grads -> its symmetric gradient slot) runs on the reduce-scatter stream,
-    # right before that unit's reduction, instead of on the compute stream:
-    # the next unit's backward GEMMs start at once and the HBM-bound copy
-    # overlaps them.  The per-parameter grads are held until it has run.
-    side_flatten: bool = True
 
     def __post_init__(self):
         if self.reshard_after_forward not in (RAF, NRAF):
@@ -1041,34 +1035,19 @@ class FSDPRuntime:
                 self._step_unit(uid, self.rs_stream)
             self.release_use(uid, "backward", None)
             return
-        side = None
         if first and self.gslot_offs and u.grad_pending == 1 and not self.defer_reduce \
                 and u.accum_unsharded is None:
             # write-back straight into a symmetric gradient slot: the pull
             # reduce-scatter reads it from every peer, no copy in between
             u.gslot, u.flat_grad = self._acquire_gslot(lay.psi)
-            if self.cfg.side_flatten and not injected:
-                # the slot's only next reader is this unit's reduction on the
-                # reduce-scatter stream: write it there (stream order), off
-                # the compute stream
-                side = self.rs_stream
         elif first:
             u.flat_grad = torch.empty(lay.psi, dtype=gdt, device=self.device)
         if first:
             self.ledger.alloc("grads", lay.psi * u.flat_grad.element_size(), lay.psi)   # engine.py:530
-        fs = self.compute_stream
-        if side is not None:
-            produced = torch.cuda.Event()
-            produced.record(self.compute_stream)
-            side.wait_event(produced)
-            fs = side
-        with self.timed("flatten_grad", fs,
+        with self.timed("flatten_grad", self.compute_stream,
                         sum(g.numel() for g in srcs if g is not None) * 2 * u.flat_grad.element_size()):
-            kernels.flatten(srcs, lay.offsets, u.flat_grad, accumulate=not first, stream=fs)
-        if side is not None:
-            for g in srcs:
-                if g is not None:
-                    g.record_stream(side)        # autograd's grads live until the copy has run
+            kernels.flatten(srcs, lay.offsets, u.flat_grad, accumulate=not first,
+                            stream=self.compute_stream)
         u.grad_pending -= 1
         if u.grad_pending <= 0:
             self._finalize(uid)

@@ -82,33 +82,35 @@ def test_spec_collective_examples():
     assert np.array_equal(sp.all_gather(sp.reduce_scatter(xs)), sp.all_reduce(xs))
 
 
-def test_hybrid_stage2_in_reduce_dtype():
+@pytest.mark.parametrize("W,F", [(4, 2), (8, 4), (8, 2)])
+def test_hybrid_stage2_in_reduce_dtype(W, F):
     """engine.py:789-810: the reduce-scatter output is the all-reduce payload.
     stage2_dtype rounds the fp32 partial once to bf16; the all-reduce sums the
     rounded partials in fp32; F = W and F = 1 have no stage 2 to round."""
-    rng = np.random.default_rng(3)
-    grads = [sp.cast(rng.standard_normal(16).astype(np.float32), sp.BF16) for _ in range(4)]
-    plan = sp.Plan(4, 2)
+    rng = np.random.default_rng(3 + W + F)
+    c = 8
+    grads = [sp.cast(rng.standard_normal(c * F).astype(np.float32), sp.BF16) for _ in range(W)]
+    plan = sp.Plan(W, F)
     hi = sp.hybrid_reduce(grads, plan, np.float32)
     lo = sp.hybrid_reduce(grads, plan, np.float32, stage2_dtype=sp.BF16)
-    for r in range(4):
+    for r in range(W):
         g = [q for q in plan.sharded_groups if r in q][0]
-        pos = g.index(r)
+        pos = list(g).index(r)
         parts = []
-        for rr in plan.replicated_groups[[i for i, q in enumerate(plan.replicated_groups) if r in q][0]]:
+        for rr in [q for q in plan.replicated_groups if r in q][0]:       # ascending replica order
             gg = [q for q in plan.sharded_groups if rr in q][0]
-            acc = np.zeros(8, np.float32)
+            acc = np.zeros(c, np.float32)
             for m in gg:
-                acc = acc + grads[m][pos * 8:(pos + 1) * 8].astype(np.float32)
+                acc = acc + grads[m][pos * c:(pos + 1) * c].astype(np.float32)
             parts.append(sp.cast(acc, sp.BF16))
-        exp = np.zeros(8, np.float32)
+        exp = np.zeros(c, np.float32)
         for p_ in parts:
             exp = exp + p_
         assert lo[r].tobytes() == exp.tobytes()
     assert any(not np.array_equal(a, b) for a, b in zip(hi, lo))      # the rounding is visible
-    for F in (1, 4):
-        a = sp.hybrid_reduce(grads, sp.Plan(4, F), np.float32)
-        b = sp.hybrid_reduce(grads, sp.Plan(4, F), np.float32, stage2_dtype=sp.BF16)
+    for f in (1, W):                                                   # no stage 2 to round
+        a = sp.hybrid_reduce(grads, sp.Plan(W, f), np.float32)
+        b = sp.hybrid_reduce(grads, sp.Plan(W, f), np.float32, stage2_dtype=sp.BF16)
         assert all(x.tobytes() == y.tobytes() for x, y in zip(a, b))
 
 

@@ -95,8 +95,6 @@ def parse():
                     help="HYBRID_SHARD all-reduce payload: the partial rounded to the reduce dtype "
                          "(bf16; the wrapper's default, as the reference and torch FSDP send it) or "
                          "the fp32 partial sums")
-    ap.add_argument("--no-tail-ar", action="store_true",
-                    help="last unit's replica all-reduce on the copy engines too (default: SM tail kernel)")
     ap.add_argument("--check-replicas", action="store_true",
                     help="after the timed steps, compare digests of the master / Adam shards across "
                          "replicas (HYBRID_SHARD / NO_SHARD: ranks r, r+F hold the same shard)")
@@ -284,7 +282,7 @@ def run_ours(args):
         ag_ctas=args.ctas, rs_ctas=args.rs_ctas, ag_engine=args.ag_engine,
         rs_engine=args.rs_engine, tail_engine=args.tail_engine, ll_max_bytes=args.ll_max_bytes,
         opt_split_first=args.opt_split_first, fused_cast_ag=args.fused_cast_ag,
-        hybrid_stage2=args.hybrid_stage2, tail_ar=not args.no_tail_ar,
+        hybrid_stage2=args.hybrid_stage2,
         ar_in_pool=not args.no_ar_pool, w1_bf16_grad=not args.no_w1_bf16_grad,
         opt_split_geom={"auto": None, "on": True, "off": False}[args.opt_split_geom])
     opt = fsdp.optimizer()
@@ -521,7 +519,6 @@ def step_config(args, world: int) -> dict:
             **({"ar_in_pool": False} if args.no_ar_pool else {}),
             "opt_split_geom": args.opt_split_geom,
             **({"w1_bf16_grad": False} if args.no_w1_bf16_grad else {}),
-            **({"tail_ar": False} if args.no_tail_ar else {}),
             "l2": "inputs > L2 (weights+state >20 GB)"}
 
 

@@ -149,8 +149,7 @@ class FullyShardedDataParallel(nn.Module):
                  tail_engine: str = "sm", ll_max_bytes: int = 6 << 20, opt_split_first: int = 2,
                  rate_limit: int | None | str = "auto", keep_outermost_unsharded: bool = True,
                  fused_cast_ag: bool = False, ar_in_pool: bool = True, w1_bf16_grad: bool = True,
-                 opt_split_geom: bool | None = None, hybrid_stage2: str = "reduce",
-                 tail_ar: bool = True):
+                 opt_split_geom: bool | None = None, hybrid_stage2: str = "reduce"):
         super().__init__()
         if cpu_offload is not None and cpu_offload.offload_params:
             raise NotImplementedError("CPU offload is out of scope for the B200 runtime")
@@ -205,8 +204,7 @@ class FullyShardedDataParallel(nn.Module):
                             ag_engine=ag_engine, rs_engine=rs_engine, tail_engine=tail_engine,
                             ll_max_bytes=ll_max_bytes, opt_split_first=opt_split_first,
                             fused_cast_ag=fused_cast_ag, ar_in_pool=ar_in_pool, w1_bf16_grad=w1_bf16_grad,
-                            opt_split_geom=opt_split_geom, hybrid_stage2=hybrid_stage2,
-                            tail_ar=tail_ar)
+                            opt_split_geom=opt_split_geom, hybrid_stage2=hybrid_stage2)
         self.module = module
         self.plan = plan
         self.rank = rank

@@ -101,9 +101,6 @@ class RuntimeConfig:
     # "same": use ag_engine / rs_engine for them too.
     tail_engine: str = "sm"
     tail_ctas: int = 128
-    # HYBRID / NO_SHARD: the last unit's replica all-reduce is part of the
-    # same tail (SM two-shot kernel, tail_ctas CTAs) when tail_engine is "sm"
-    tail_ar: bool = True
     # units whose unsharded payload is at most this many bytes use the
     # low-latency one-kernel collectives (no barrier kernels, 2x wire bytes):
     # below a few MB, launch + flag round trips dominate the split path
@@ -1124,19 +1121,12 @@ class FSDPRuntime:
                                           stream=self.rs_stream, tma=False)
 
     def _ar(self, inp: torch.Tensor, out: torch.Tensor, post: float, accumulate: bool,
-            stream: torch.cuda.Stream | None = None, tail: bool = False) -> None:
+            stream: torch.cuda.Stream | None = None) -> None:
         """All-reduce in the replicated group (hybrid stage 2 / NO_SHARD):
         copy engines with rs_engine="ce", else the two-shot SM kernel.  A
         first reduction into the pool-resident gradient arena lands in place
         on every member (no gather buffer, no epilogue)."""
         s = stream if stream is not None else self.rs_stream
-        if tail and self.cfg.tail_engine == "sm" and self.cfg.tail_ar:
-            # nothing left to overlap: the SM kernel with the tail grid
-            self.comm.set_ctas(self.comm.KIND_AR, self.cfg.tail_ctas)
-            self.comm.all_reduce(self.plan.replicated_desc, [inp], self.ar_stage_off, self.ar_gather_off,
-                                 [out], postdiv=post, accumulate=accumulate, stream=s)
-            self.comm.set_ctas(self.comm.KIND_AR, 0)
-            return
         if (self.cfg.rs_engine == "ce" and not accumulate and self.grad_pool_off is not None
                 and out.untyped_storage().data_ptr() == self.grad.untyped_storage().data_ptr()):
             off = self.grad_pool_off + (out.storage_offset() - self.grad.storage_offset()) * 4
@@ -1206,7 +1196,7 @@ class FSDPRuntime:
                     self._rs(gslot, payload.dtype, u.grad, pre, post, accumulate, tail)
             elif F == 1:
                 with self.timed("allreduce", self.rs_stream, payload.numel() * payload.element_size()):
-                    self._ar(payload, u.grad, post, accumulate, tail=tail)
+                    self._ar(payload, u.grad, post, accumulate)
             else:
                 low2 = self.cfg.hybrid_stage2 == "reduce" and payload.dtype != torch.float32
                 tmp = torch.empty(n, dtype=payload.dtype if low2 else torch.float32, device=self.device)
@@ -1218,7 +1208,7 @@ class FSDPRuntime:
                 rs_done.record(self.rs_stream)
                 self.ar_stream.wait_event(rs_done)
                 with self.timed("allreduce", self.ar_stream, n * tmp.element_size()):
-                    self._ar(tmp, u.grad, post, accumulate, stream=self.ar_stream, tail=tail)
+                    self._ar(tmp, u.grad, post, accumulate, stream=self.ar_stream)
                 tmp.record_stream(self.ar_stream)
             payload.record_stream(self.rs_stream)
             if gslot is not None:
